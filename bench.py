@@ -1,0 +1,437 @@
+"""Benchmark of the B200 CKKS engine (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config train|bootstrap|ks]
+                    [--impl ours|reference]
+
+Workloads (BASELINE.json configs):
+  train      cfg4: one encrypted-LR minibatch at N=2^16 (P16 preset): 16
+             ciphertexts x 32 rows of 768-d synthetic embeddings, batched
+             gradient + Nesterov update + sparse-1024 bootstrap of w and u.
+             metric: encrypted LR train samples/sec (whole job).
+  bootstrap  cfg3: one sparse-1024 bootstrap at N=2^16.  metric: ms.
+  ks         cfg2: NTT/iNTT + relinearisation key switch of 64 ciphertexts at
+             the full P16 chain.  metric: key switches/sec.
+--impl reference times the reference algorithm's CPU path (the oracle port,
+oracle/, C+OpenMP kernels, all host cores) on a bounded sample.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "train"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--profile", action="store_true", help="print per-kernel-class profile")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+
+def init_dist(args):
+    import torch
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks (sampled with nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+def p16():
+    from paper_2210_02574_b200 import ckks
+
+    return ckks.get_preset("p16")
+
+
+class KsWorkload:
+    """cfg2: 64 ciphertexts at the full P16 chain: NTT + iNTT of every limb and a
+    relinearising key switch of every c1 (one batched launch sequence)."""
+
+    metric = "key switches/sec"
+    unit = "KS/s"
+    higher = True
+    batch = 64
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_2210_02574_b200 import ckks, ring
+
+        self.params = p16()
+        self.keys = ckks.keygen(self.params, rotation_steps=[1], rng_seed=7,
+                                include_conjugation=False)
+        L = self.params.max_level
+        n = self.params.ring_degree
+        host = np.empty((self.batch, 2, L + 1, n), dtype=np.uint64)
+        for i in range(self.batch):
+            rng = np.random.default_rng(1000 + i + rank * self.batch)
+            for c in range(2):
+                for j, q in enumerate(self.params.ring.moduli_chain):
+                    host[i, c, j] = rng.integers(0, q, size=n, dtype=np.uint64)
+        self.host = torch.from_numpy(host.view(np.int64)).pin_memory()
+        self.dev = self.host.to("cuda")
+        self.out_host = torch.empty((self.batch, 2, L + 1, n), dtype=torch.int64).pin_memory()
+        self.h2d = self.host.numel() * 8
+        self.d2h = self.out_host.numel() * 8
+        self.units = self.batch * world
+        self.config = {"workload": "cfg2 NTT/iNTT + key-switch microbench", "preset": "p16",
+                       "N": n, "level": L, "ciphertexts_per_gpu": self.batch,
+                       "l2": "inputs (1.4 GiB) exceed L2"}
+
+    def _run(self, data):
+        from paper_2210_02574_b200 import ring
+        from paper_2210_02574_b200.ckks import keys as K
+
+        params = self.params
+        L = params.max_level
+        sel = ring._dev.chain_primes(L + 1)
+        ev = ring._dev.empty(*data.shape)
+        ring._ntt_dev(params.ring, data, ev, L + 1, sel, False)  # all limbs -> eval
+        back = ring._dev.empty(*data.shape)
+        ring._ntt_dev(params.ring, ev, back, L + 1, sel, True)  # and back
+        d = ring.RnsPoly(params.ring, ev[:, 1], ring.EVAL, L)
+        kb, ka = K.ks_apply(self.keys, self.keys.relin_key, d)
+        return kb, ka, back
+
+    def step(self):
+        return self._run(self.dev)
+
+    def e2e_step(self):
+        dev = self.host.to("cuda", non_blocking=True)
+        kb, ka, _ = self._run(dev)
+        self.out_host[:, 0].copy_(kb.data, non_blocking=True)
+        self.out_host[:, 1].copy_(ka.data, non_blocking=True)
+
+    def oracle_sample(self):
+        """One KS at level L + NTT/iNTT of one ciphertext on the CPU oracle."""
+        from oracle import scheme as S
+
+        p = S.Params.from_text(self.params.to_config_text())
+        keys = S.keygen(p, [], 7, conj=False)
+        rng = np.random.default_rng(1000)
+        L = p.max_level
+        d = np.stack([rng.integers(0, q, size=p.n, dtype=np.uint64) for q in p.chain])
+        t0 = time.perf_counter()
+        S.ntt_fwd(p, d, p.chain)
+        S.ntt_fwd(p, d, p.chain)
+        S.ntt_inv(p, d, p.chain)
+        S.ntt_inv(p, d, p.chain)
+        S.ks_apply(p, keys.relin, d, L)
+        sec = time.perf_counter() - t0
+        return 1.0 / sec, "1 ciphertext: 2x(22-limb NTT + iNTT) + 1 top-level KS (N=2^16)"
+
+
+class BootstrapWorkload:
+    """cfg3: one sparse-1024 periodic bootstrap at N=2^16 (the w/u refresh)."""
+
+    metric = "CKKS bootstrap ms (N=2^16)"
+    unit = "ms"
+    higher = False
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_2210_02574_b200 import bootstrap as bs, ckks
+
+        self.params = p16()
+        self.ctx = bs.build_context(self.params, n_slots=1024, input_periodic=True)
+        steps = self.ctx.required_rotation_steps()
+        t0 = time.time()
+        self.keys = ckks.keygen(self.params, rotation_steps=steps, rng_seed=7)
+        self.keygen_s = time.time() - t0
+        v = np.tile(np.random.default_rng(1002).uniform(-1, 1, 1024), 32)
+        self.v = v
+        self.ct = ckks.encrypt_vector(self.params, v, self.keys, level=0, rng_seed=5)
+        self.host = torch.stack([self.ct.c0.data, self.ct.c1.data]).cpu().pin_memory()
+        self.h2d = self.host.numel() * 8
+        self.d2h = 0
+        self.units = 1
+        self.config = {"workload": "cfg3 sparse-1024 periodic bootstrap", "preset": "p16",
+                       "N": self.params.ring_degree, "n_slots": 1024,
+                       "rotation_keys": len(steps)}
+
+    def step(self):
+        from paper_2210_02574_b200 import bootstrap as bs
+
+        self.out = bs.bootstrap(self.ct, self.ctx, self.keys)
+        return self.out
+
+    def e2e_step(self):
+        from paper_2210_02574_b200 import bootstrap as bs
+        from paper_2210_02574_b200.ckks import ops
+
+        t = ops._packed(self.params, (), 0)
+        t.copy_(self.host.to("cuda", non_blocking=True))
+        ct = ops._ct(t, 0, self.ct.scale, self.ct.slot_count, self.params)
+        out = bs.bootstrap(ct, self.ctx, self.keys)
+        self.d2h = out.c0.data.numel() * 16
+        host = out.c0.data.cpu()
+        return host
+
+    def check(self):
+        from paper_2210_02574_b200 import ckks
+
+        got = ckks.decrypt_vector(self.out, self.keys)
+        return {"max_abs_err": float(np.max(np.abs(got - self.v))),
+                "output_level": self.out.level, "keygen_s": round(self.keygen_s, 1),
+                "diag_cache_gib": round(self.ctx.diag_cache_bytes() / 2 ** 30, 2)}
+
+
+WORKLOADS = {"ks": KsWorkload, "bootstrap": BootstrapWorkload}
+
+
+# ---------------------------------------------------------------------------
+# timing
+# ---------------------------------------------------------------------------
+
+
+def timed(fn, steps, world):
+    import torch
+
+    barrier(world)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        fn()
+    b.record(stream)
+    b.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    return a.elapsed_time(b)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2210_02574_b200 import _lib
+
+    rank, world = init_dist(args)
+    wl = WORKLOADS[args.config]()
+    wl.setup(rank, world)
+    for _ in range(args.warmup):
+        wl.step()
+    torch.cuda.synchronize()
+    n0 = _lib.launch_count()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+        ms = timed(wl.step, args.steps, world)
+    launches = _lib.launch_count() - n0
+    ms = max_over_ranks(ms, world)
+    ms_step = ms / args.steps
+    # end to end through the public API with host buffers
+    wl.e2e_step()
+    e2e_ms = max_over_ranks(timed(wl.e2e_step, max(1, args.steps // 2), world), world) / max(
+        1, args.steps // 2)
+    # per-kernel-class profile of one step (separate pass, not the timed one)
+    _lib.profile_enable(True)
+    wl.step()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    extra = wl.check() if hasattr(wl, "check") else {}
+    if rank != 0:
+        return
+    if wl.higher:
+        value = wl.units / (ms_step / 1e3)
+        e2e_value = wl.units / (e2e_ms / 1e3)
+    else:
+        value = ms_step
+        e2e_value = e2e_ms
+    peak, peak_kind = measured_peaks()
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    dp = prof[dom]
+    achieved = dp["bytes"] / (dp["ms"] / 1e3) / 1e9 if dp["ms"] else 0.0
+    step_ms_prof = sum(p["ms"] for p in prof.values())
+    try:
+        int_peak = _lib.modmul_peak()
+    except Exception:
+        int_peak = None
+    line = {
+        "metric": wl.metric, "value": round(value, 4), "unit": wl.unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": wl.higher, "scaling": "weak" if args.config == "ks" else "strong",
+        "vs_baseline": None, "dtype": "u64 (RNS residues mod 40-60-bit primes)",
+        "data": "synthetic", "config": wl.config,
+        "e2e": {"value": round(e2e_value, 4), "unit": wl.unit,
+                "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "share_of_step": round(dp["ms"] / step_ms_prof, 4) if step_ms_prof else None},
+        "int_roofline": {
+            "kernel": dom,
+            "achieved_modmul_per_s": round(dp["modmuls"] / (dp["ms"] / 1e3), 1) if dp["ms"] else 0,
+            "peak_modmul_per_s": int_peak,
+            "frac": round(dp["modmuls"] / (dp["ms"] / 1e3) / int_peak, 4)
+            if (dp["ms"] and int_peak) else None},
+        "kernel_profile_ms": {c: round(p["ms"], 3) for c, p in prof.items() if p["launches"]},
+        "clocks": clk.summary(),
+    }
+    line.update(extra)
+    line["cpu_baseline"] = cpu_baseline(wl)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl):
+    try:
+        from oracle import kernels as OK
+
+        if OK.clib() is None:
+            OK.build_c()
+            OK._clib = None
+        value, sample = wl.oracle_sample()
+        return {"value": round(value, 6), "unit": wl.unit, "cores": os.cpu_count(),
+                "kind": "port", "sample": sample}
+    except Exception as exc:  # the baseline must never break the GPU line
+        return {"value": None, "unit": wl.unit, "cores": os.cpu_count(), "kind": "port",
+                "sample": f"unavailable: {exc}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.config]()
+
+    class _P:  # parameters only; no GPU on this path
+        pass
+
+    from paper_2210_02574_b200.ckks import params as P
+
+    wl.params = P.get_preset("p16")
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample = wl.oracle_sample()
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {"metric": wl.metric, "value": round(value, 6), "unit": wl.unit,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": wl.higher, "impl": "reference", "data": "synthetic",
+            "config": {"workload": args.config, "preset": "p16"},
+            "cpu_baseline": {"value": round(value, 6), "unit": wl.unit,
+                             "cores": os.cpu_count(), "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": wl.unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

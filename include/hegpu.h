@@ -1,0 +1,222 @@
+/*
+ * hegpu.h -- C ABI of the B200-native CKKS engine (libhegpu.so, sm_100a).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `hebert` (/root/reference/pkg/src/hebert).  Two groups of entry points:
+ *
+ *  1. Host-array kernel table (hegpu_k_*): exactly the ten functions of the
+ *     reference kernel seam `hebert._kernels` (_kernels.py:319-328, numpy twins
+ *     :352-361), same arguments and ownership (C-contiguous uint64 arrays owned
+ *     by the caller; *_inplace mutate their first argument, the others write a
+ *     caller-provided output).  They copy to the GPU, run the device kernels and
+ *     copy back; they exist for parity and for callers that bind the kernel
+ *     table directly.
+ *
+ *  2. Device-resident entry points (hegpu_*): operate on device pointers to
+ *     limb-major RNS polynomials.  A "poly group" is n_polys polynomials of k
+ *     limbs each, poly p at ptr + p*stride (stride in uint64 elements), limb l
+ *     at +l*N.  Limb l of every poly in the group uses the ring prime with
+ *     global index primes[l] (chain primes are 0..n_chain-1, special primes
+ *     follow).  All calls are stream-ordered on `stream` (a cudaStream_t, NULL
+ *     = legacy default stream) and never synchronise unless stated.
+ *
+ * Every function returns 0 on success or a nonzero HEGPU_E_* code; the message
+ * of the last failure on the calling thread is hegpu_last_error().  The Python
+ * shim maps codes onto the reference error taxonomy (errors.py:4-75):
+ * HEGPU_E_ARG -> CryptoError, HEGPU_E_CUDA -> CryptoError (with the CUDA text),
+ * HEGPU_E_NOMEM -> CryptoError.
+ */
+#ifndef HEGPU_H_
+#define HEGPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEGPU_OK 0
+#define HEGPU_E_ARG 1
+#define HEGPU_E_CUDA 2
+#define HEGPU_E_NOMEM 3
+
+#define HEGPU_MAX_PRIMES 64
+
+typedef struct hegpu_ring* hegpu_ring_t;
+
+/* -------------------------------------------------------------------------
+ * library / ring context
+ * ---------------------------------------------------------------------- */
+
+/* Library version string. */
+const char* hegpu_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* hegpu_last_error(void);
+/* Number of visible CUDA devices (0 if none); never fails. */
+int hegpu_device_count(void);
+
+/* Total kernel launches issued by this library since load (for accounting). */
+long long hegpu_launch_count(void);
+/* Measured 64-bit Shoup modular-multiplication throughput of this GPU
+ * (modmul/s, 8 independent chains per thread, all SMs); synchronous. */
+int hegpu_bench_modmul_peak(int iters, double* modmul_per_s);
+/* Enable (1) / disable (0) per-launch CUDA-event timing; clears records. */
+int hegpu_profile_enable(int on);
+/* Synchronise the device, then report and clear, per kernel class, the
+ * accumulated device time (ms), launch count, algorithmic bytes (inputs read
+ * once + outputs written once) and modular multiplications.  Classes:
+ * 0 ntt, 1 elementwise, 2 lift, 3 automorphism, 4 tensor, 5 basis conversion,
+ * 6 key-switch inner product, 7 diagonal multiply-accumulate, 8 encrypt. */
+int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* modmuls,
+                       int n_classes);
+
+/* Build a ring context: NTT tables for every prime (psi = the first base in
+ * [2, 10^4) whose (q-1)/2N power has order 2N -- ring.py:69-78; tables in
+ * bit-reversed order -- ring.py:94-108) plus Montgomery/Shoup constants, on
+ * the current CUDA device.  Replaces RingParams/PrimeTables/StackedTables
+ * precompute (ring.py:81-177).  Primes must be < 2^62, = 1 mod 2N. */
+int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain,
+                      const uint64_t* special, int n_special, hegpu_ring_t* out);
+int hegpu_ring_destroy(hegpu_ring_t ring);
+/* Copy the device twiddle tables of global prime p to host (4 arrays of N:
+ * psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup; natural form). */
+int hegpu_ring_get_tables(hegpu_ring_t ring, int p, uint64_t* host_out4n);
+
+/* -------------------------------------------------------------------------
+ * device-resident polynomial kernels (ring.py:287-482)
+ * ---------------------------------------------------------------------- */
+
+/* Negacyclic NTT.  inverse=0: natural -> bit-reversed evaluation order
+ * (CT DIT, _kernels.py:144-171); inverse=1: GS DIF back to natural order
+ * times N^-1 (_kernels.py:173-204).  in may equal out. */
+int hegpu_ntt(hegpu_ring_t ring, int inverse, const uint64_t* in, int64_t in_stride,
+              uint64_t* out, int64_t out_stride, int n_polys, int k,
+              const int32_t* primes, void* stream);
+
+#define HEGPU_OP_ADD 0  /* a + b          (addmod_rows, _kernels.py:229-240)   */
+#define HEGPU_OP_SUB 1  /* a - b          (submod_rows, _kernels.py:242-253)   */
+#define HEGPU_OP_MUL 2  /* a * b          (elementwise_mulmod, :288-298)       */
+#define HEGPU_OP_MONT 3 /* a * b * R^-1   (elementwise_mont, :206-215)         */
+#define HEGPU_OP_NEG 4  /* -a             (ring.neg_mod, ring.py:54-57)        */
+#define HEGPU_OP_SCALAR 5 /* a * c[l], c natural per limb (poly_scalar_mul)    */
+#define HEGPU_OP_ROWMONT 6 /* a * c[l] * R^-1 (rowwise_mont, :217-227)         */
+#define HEGPU_OP_FMA 7  /* out = out + a * b (fma_inplace, :255-269)           */
+#define HEGPU_OP_COPY 8 /* out = a                                             */
+#define HEGPU_OP_ADDC 9 /* a + c[l], c natural per limb (constant add_plain)   */
+#define HEGPU_OP_REDUCE 10 /* a mod q for any 64-bit a (after a wrapping NCCL sum) */
+
+/* Elementwise op over a poly group.  b may be NULL for unary ops; consts is a
+ * host array of k per-limb scalars for SCALAR / ROWMONT. */
+int hegpu_elementwise(hegpu_ring_t ring, int op, const uint64_t* a, int64_t a_stride,
+                      const uint64_t* b, int64_t b_stride, uint64_t* out,
+                      int64_t out_stride, int n_polys, int k, const int32_t* primes,
+                      const uint64_t* consts, void* stream);
+
+/* out[l] = np.mod(src, q_l) for signed int64 coefficients (limbs_from_signed,
+ * ring.py:381-387).  src poly p at src + p*src_stride. */
+int hegpu_lift_signed(hegpu_ring_t ring, const int64_t* src, int64_t src_stride,
+                      uint64_t* out, int64_t out_stride, int n_polys, int k,
+                      const int32_t* primes, void* stream);
+
+/* Centered lift of one limb (prime src_prime, coefficient form) into k limbs:
+ * v > q/2 -> v - q, then mod q_l (rescale/ModRaise lift, ops.py:170-173,
+ * bootstrap.py:266-270). */
+int hegpu_lift_centered(hegpu_ring_t ring, const uint64_t* src, int64_t src_stride,
+                        int src_prime, uint64_t* out, int64_t out_stride, int n_polys,
+                        int k, const int32_t* primes, void* stream);
+
+/* X -> X^g.  eval_form=1: slot permutation on bit-reversed evaluation form
+ * (poly_automorphism_eval, ring.py:471-482); eval_form=0: signed coefficient
+ * permutation (poly_automorphism, ring.py:426-437).  in != out. */
+int hegpu_automorphism(hegpu_ring_t ring, int eval_form, uint64_t g, const uint64_t* in,
+                       int64_t in_stride, uint64_t* out, int64_t out_stride,
+                       int n_polys, int k, const int32_t* primes, void* stream);
+
+/* CKKS tensor product (ops.py:355-357): d0 = a0 b0, d1 = a0 b1 + a1 b0,
+ * d2 = a1 b1 over chain limbs 0..k-1.  Each operand is a poly group with its
+ * own stride. */
+int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int64_t a_stride,
+                 const uint64_t* b0, const uint64_t* b1, int64_t b_stride, uint64_t* d0,
+                 uint64_t* d1, uint64_t* d2, int64_t d_stride, int n_polys, int k,
+                 void* stream);
+
+/* -------------------------------------------------------------------------
+ * fused CKKS kernels (ckks/ops.py, ckks/keys.py, bootstrap.py)
+ * ---------------------------------------------------------------------- */
+
+/* Hybrid key switch (ks_apply, keys.py:278-339), batched over n_batch
+ * ciphertext components that share one switching key (the key is streamed
+ * once per batch).  d: eval-form polys at `level` (level+1 chain limbs).
+ * key_b/key_a: host arrays of n_digits device pointers, each digit a
+ * (key_rows, N) eval-form poly over chain primes then special primes
+ * (key_rows = n_chain + n_special).  alpha = digit size (params.py:48-51).
+ * out_b / out_a: eval-form results at `level`.  Bit-exact with the reference. */
+int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
+                   int64_t d_stride, int n_batch, const uint64_t* const* key_b,
+                   const uint64_t* const* key_a, int n_digits, uint64_t* out_b,
+                   uint64_t* out_a, int64_t out_stride, void* stream);
+
+/* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
+ * limbs (eval form), out gets `level` limbs.  in may equal out. */
+int hegpu_rescale(hegpu_ring_t ring, int level, const uint64_t* in, int64_t in_stride,
+                  uint64_t* out, int64_t out_stride, int n_polys, void* stream);
+
+/* ModRaise (_mod_raise, bootstrap.py:260-275): eval-form level-0 polys ->
+ * centered lift to chain limbs 0..to_level, eval form. */
+int hegpu_mod_raise(hegpu_ring_t ring, const uint64_t* in, int64_t in_stride,
+                    uint64_t* out, int64_t out_stride, int n_polys, int to_level,
+                    void* stream);
+
+/* Public-key encryption combine (encrypt, ops.py:102-116): given eval-form
+ * v, e0, e1, m (k limbs each) and pk (b, a) sliced to k limbs:
+ * c0 = v*b + e0 + m, c1 = v*a + e1.  m may be NULL (zero). */
+int hegpu_encrypt_combine(hegpu_ring_t ring, const uint64_t* v, const uint64_t* e0,
+                          const uint64_t* e1, const uint64_t* m, const uint64_t* pk_b,
+                          const uint64_t* pk_a, uint64_t* c0, uint64_t* c1, int k,
+                          void* stream);
+
+/* Plaintext-diagonal multiply-accumulate for the BSGS linear transforms
+ * (_apply_diag_transform, bootstrap.py:200-247): for each of n_terms terms t,
+ * out += pt[t] * ct[t] over both ciphertext components, where ct[t] is a
+ * ciphertext (c0 at ct_ptrs[t], c1 at ct_ptrs[t] + ct_c1_off) and pt[t] a
+ * plaintext poly; k chain limbs.  out c1 at out + out_c1_off.  accumulate=0
+ * overwrites out.  Host arrays of device pointers. */
+int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct_c1_off,
+                   const uint64_t* const* pt_ptrs, int n_terms, uint64_t* out,
+                   int64_t out_c1_off, int k, int accumulate, void* stream);
+
+/* -------------------------------------------------------------------------
+ * host-array kernel table: drop-in for hebert._kernels (_kernels.py:319-328)
+ * shapes are (k, n) row-major uint64; vectors are length k
+ * ---------------------------------------------------------------------- */
+int hegpu_k_ntt_forward_inplace(uint64_t* a, int k, int n, const uint64_t* psi_rev,
+                                const uint64_t* q, const uint64_t* qinv);
+int hegpu_k_ntt_inverse_inplace(uint64_t* a, int k, int n, const uint64_t* ipsi_rev,
+                                const uint64_t* ninv, const uint64_t* q,
+                                const uint64_t* qinv);
+int hegpu_k_elementwise_mont(const uint64_t* a, const uint64_t* b, uint64_t* out, int k,
+                             int n, const uint64_t* q, const uint64_t* qinv);
+int hegpu_k_elementwise_mulmod(const uint64_t* a, const uint64_t* b, uint64_t* out, int k,
+                               int n, const uint64_t* q, const uint64_t* qinv,
+                               const uint64_t* r2);
+int hegpu_k_rowwise_mont(const uint64_t* a, const uint64_t* c, uint64_t* out, int k, int n,
+                         const uint64_t* q, const uint64_t* qinv);
+int hegpu_k_addmod_rows(const uint64_t* a, const uint64_t* b, uint64_t* out, int k, int n,
+                        const uint64_t* q);
+int hegpu_k_submod_rows(const uint64_t* a, const uint64_t* b, uint64_t* out, int k, int n,
+                        const uint64_t* q);
+/* hat (l, n), punc (l, kt) Montgomery form, out (kt, n) */
+int hegpu_k_base_convert(const uint64_t* hat, int l, int n, const uint64_t* punc, int kt,
+                         const uint64_t* q_to, const uint64_t* qinv_to, uint64_t* out);
+int hegpu_k_fma_inplace(uint64_t* acc, const uint64_t* a, const uint64_t* b, int k, int n,
+                        const uint64_t* q, const uint64_t* qinv, const uint64_t* r2);
+/* key (key_rows, n); rows int64[k] */
+int hegpu_k_fma_gather_inplace(uint64_t* acc, const uint64_t* a, const uint64_t* key,
+                               int key_rows, const int64_t* rows, int k, int n,
+                               const uint64_t* q, const uint64_t* qinv,
+                               const uint64_t* r2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEGPU_H_ */

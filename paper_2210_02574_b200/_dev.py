@@ -1,0 +1,113 @@
+"""Device memory / stream plumbing (PyTorch is used only as the allocator and
+stream provider; all arithmetic runs in libhegpu).
+
+Residue limbs live in torch.int64 CUDA tensors that are bit-identical to the
+reference's uint64 limb matrices (ring.py:257-279).  A "poly group" tensor has
+shape (..., k, N) with unit stride along N and stride N along limbs; its
+leading dimensions must be uniformly strided so one C-ABI call covers them.
+"""
+
+import numpy as np
+
+from . import _lib
+from .errors import CryptoError, DeviceError
+
+try:  # torch is the device allocator; importing it is cheap after warm-up
+    import torch
+except Exception as exc:  # pragma: no cover - torch is part of the image
+    torch = None
+    _TORCH_ERR = exc
+else:
+    _TORCH_ERR = None
+
+_PRIME_CACHE = {}
+
+
+def require():
+    if torch is None:
+        raise DeviceError(f"torch unavailable: {_TORCH_ERR}")
+    _lib.require_gpu()
+    if not torch.cuda.is_available():
+        raise DeviceError("torch sees no CUDA device")
+
+
+def device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def empty(*shape):
+    return torch.empty(shape, dtype=torch.int64, device=device())
+
+
+def zeros(*shape):
+    return torch.zeros(shape, dtype=torch.int64, device=device())
+
+
+def ptr(t):
+    return t.data_ptr()
+
+
+def to_device(arr):
+    """numpy uint64/int64 array -> device int64 tensor (H2D copy)."""
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    elif a.dtype != np.int64:
+        a = a.astype(np.int64)
+    return torch.from_numpy(a).to(device(), non_blocking=False)
+
+
+def to_host(t):
+    """device int64 tensor -> numpy uint64 (D2H copy)."""
+    return t.detach().to("cpu").contiguous().numpy().view(np.uint64)
+
+
+def group(t, k, n):
+    """(ptr, n_polys, poly_stride) of a (..., k, N) tensor with uniform strides."""
+    if t.dtype != torch.int64 or not t.is_cuda:
+        raise CryptoError("limbs must be a CUDA int64 tensor")
+    if t.shape[-2:] != (k, n):
+        raise CryptoError(f"limb shape {tuple(t.shape)} inconsistent with ({k}, {n})")
+    if t.stride(-1) != 1 or (k > 1 and t.stride(-2) != n):
+        raise CryptoError("limbs must be contiguous within a poly")
+    lead = t.shape[:-2]
+    if len(lead) == 0:
+        return t.data_ptr(), 1, k * n
+    count = 1
+    for s in lead:
+        count *= s
+    if count == 1:
+        return t.data_ptr(), 1, k * n
+    # collapse leading dims: require a single uniform stride
+    strides = [t.stride(i) for i in range(len(lead))]
+    inner = strides[-1]
+    expect = inner
+    for i in range(len(lead) - 1, 0, -1):
+        expect *= lead[i]
+        if lead[i - 1] > 1 and strides[i - 1] != expect:
+            raise CryptoError("poly group is not uniformly strided")
+    return t.data_ptr(), count, inner
+
+
+def prime_array(key, values):
+    """Cached int32 numpy array of global prime indices (kept alive for ctypes)."""
+    arr = _PRIME_CACHE.get(key)
+    if arr is None:
+        arr = np.ascontiguousarray(values, dtype=np.int32)
+        _PRIME_CACHE[key] = arr
+    return arr
+
+
+def chain_primes(k):
+    return prime_array(("chain", k), range(k))
+
+
+def ext_primes(level, n_chain, n_special):
+    return prime_array(
+        ("ext", level, n_chain, n_special),
+        list(range(level + 1)) + [n_chain + i for i in range(n_special)],
+    )

@@ -1,0 +1,612 @@
+// Elementwise / gather / basis-conversion / key-switch inner-product kernels.
+//
+// All kernels are HBM-bound streaming kernels over limb-major uint64 data:
+// each thread owns 2 consecutive coefficients (128-bit loads/stores) of one
+// limb; grid.y enumerates (poly, limb) rows.  Reference semantics are cited
+// per kernel.
+#include "ring.cuh"
+
+namespace hegpu {
+
+constexpr int kEwThreads = 256;
+
+struct EwParams {
+  const uint64_t* a;
+  const uint64_t* b;
+  uint64_t* o;
+  int64_t as, bs, os;
+  int k;
+  int log_n;
+  const PrimeConst* pc;
+  uint8_t sel[kMaxPrimes];
+  uint64_t c[kMaxPrimes];
+  uint64_t csh[kMaxPrimes];
+};
+
+// One row = one limb of one poly; 2 coefficients per thread.
+template <int OP>
+__global__ void __launch_bounds__(kEwThreads) k_elementwise(const __grid_constant__ EwParams P) {
+  const int N = 1 << P.log_n;
+  const int row = blockIdx.y + blockIdx.z * 65535;
+  const int poly = row / P.k, limb = row - poly * P.k;
+  const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
+  if (x >= N) return;
+  const PrimeConst pc = P.pc[P.sel[limb]];
+  const uint64_t q = pc.q;
+  const size_t la = (size_t)limb * N + x;
+  const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(P.a + poly * P.as + la);
+  ulonglong2 vb = make_ulonglong2(0, 0);
+  if (OP == HEGPU_OP_ADD || OP == HEGPU_OP_SUB || OP == HEGPU_OP_MUL || OP == HEGPU_OP_MONT ||
+      OP == HEGPU_OP_FMA)
+    vb = *reinterpret_cast<const ulonglong2*>(P.b + poly * P.bs + la);
+  uint64_t* op = P.o + poly * P.os + la;
+  ulonglong2 r;
+  if (OP == HEGPU_OP_ADD) {
+    r.x = add_mod(va.x, vb.x, q);
+    r.y = add_mod(va.y, vb.y, q);
+  } else if (OP == HEGPU_OP_SUB) {
+    r.x = sub_mod(va.x, vb.x, q);
+    r.y = sub_mod(va.y, vb.y, q);
+  } else if (OP == HEGPU_OP_MUL) {
+    r.x = mul_mod(va.x, vb.x, pc);
+    r.y = mul_mod(va.y, vb.y, pc);
+  } else if (OP == HEGPU_OP_MONT) {
+    r.x = mont_mul(va.x, vb.x, q, pc.qinv_neg);
+    r.y = mont_mul(va.y, vb.y, q, pc.qinv_neg);
+  } else if (OP == HEGPU_OP_NEG) {
+    r.x = va.x ? q - va.x : 0;
+    r.y = va.y ? q - va.y : 0;
+  } else if (OP == HEGPU_OP_SCALAR) {
+    r.x = shoup(va.x, P.c[limb], P.csh[limb], q);
+    r.y = shoup(va.y, P.c[limb], P.csh[limb], q);
+  } else if (OP == HEGPU_OP_ROWMONT) {
+    r.x = mont_mul(va.x, P.c[limb], q, pc.qinv_neg);
+    r.y = mont_mul(va.y, P.c[limb], q, pc.qinv_neg);
+  } else if (OP == HEGPU_OP_REDUCE) {
+    r.x = reduce64(va.x, pc);
+    r.y = reduce64(va.y, pc);
+  } else if (OP == HEGPU_OP_ADDC) {
+    r.x = add_mod(va.x, P.c[limb], q);
+    r.y = add_mod(va.y, P.c[limb], q);
+  } else if (OP == HEGPU_OP_FMA) {
+    const ulonglong2 acc = *reinterpret_cast<const ulonglong2*>(op);
+    r.x = add_mod(acc.x, mul_mod(va.x, vb.x, pc), q);
+    r.y = add_mod(acc.y, mul_mod(va.y, vb.y, pc), q);
+  } else {  // COPY
+    r = va;
+  }
+  *reinterpret_cast<ulonglong2*>(op) = r;
+}
+
+static dim3 rows_grid(int n, int rows, int per_thread) {
+  int gx = (n / per_thread + kEwThreads - 1) / kEwThreads;
+  if (gx < 1) gx = 1;
+  int gy = rows < 65535 ? rows : 65535;
+  int gz = (rows + 65534) / 65535;
+  return dim3(gx, gy, gz);
+}
+
+void launch_elementwise(const PrimeConst* dpc, const std::vector<uint64_t>& hq, int log_n,
+                        const EwArgs& A, cudaStream_t st) {
+  const int rows = A.n_polys * A.k;
+  if (rows == 0) return;
+  if (A.k > kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+  EwParams P;
+  P.a = A.a;
+  P.b = A.b;
+  P.o = A.o;
+  P.as = A.as;
+  P.bs = A.bs;
+  P.os = A.os;
+  P.k = A.k;
+  P.log_n = log_n;
+  P.pc = dpc;
+  for (int l = 0; l < A.k; ++l) {
+    const int p = A.primes[l];
+    if (p < 0 || p >= (int)hq.size()) throw HegpuError{HEGPU_E_ARG, "prime index out of range"};
+    P.sel[l] = (uint8_t)p;
+    if (A.consts) {
+      const uint64_t q = hq[p];
+      P.c[l] = A.consts[l];
+      if (A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ADDC) {
+        if (A.consts[l] >= q) throw HegpuError{HEGPU_E_ARG, "scalar not reduced"};
+        P.csh[l] = h_shoup(A.consts[l], q);
+      }
+    }
+  }
+  if ((A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ROWMONT || A.op == HEGPU_OP_ADDC) &&
+      !A.consts)
+    throw HegpuError{HEGPU_E_ARG, "scalar op needs consts"};
+  const int n = 1 << log_n;
+  if (n < 2) throw HegpuError{HEGPU_E_ARG, "N too small"};
+  const dim3 grid = rows_grid(n, rows, 2);
+  const bool two_in = A.op == HEGPU_OP_ADD || A.op == HEGPU_OP_SUB || A.op == HEGPU_OP_MUL ||
+                      A.op == HEGPU_OP_MONT || A.op == HEGPU_OP_FMA;
+  const double ew_elems = (double)rows * n;
+  const double ew_mm = (A.op == HEGPU_OP_MUL || A.op == HEGPU_OP_FMA) ? 2 * ew_elems
+                       : (A.op == HEGPU_OP_MONT || A.op == HEGPU_OP_SCALAR ||
+                          A.op == HEGPU_OP_ROWMONT) ? ew_elems : 0.0;
+  ProfScope ps(PROF_ELEMENTWISE, st,
+               ew_elems * 8.0 * ((two_in ? 2 : 1) + (A.op == HEGPU_OP_FMA ? 2 : 1)), ew_mm);
+  switch (A.op) {
+    case HEGPU_OP_ADD: k_elementwise<HEGPU_OP_ADD><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_SUB: k_elementwise<HEGPU_OP_SUB><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_MUL: k_elementwise<HEGPU_OP_MUL><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_MONT: k_elementwise<HEGPU_OP_MONT><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_NEG: k_elementwise<HEGPU_OP_NEG><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_SCALAR: k_elementwise<HEGPU_OP_SCALAR><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_ROWMONT: k_elementwise<HEGPU_OP_ROWMONT><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_FMA: k_elementwise<HEGPU_OP_FMA><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_COPY: k_elementwise<HEGPU_OP_COPY><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_ADDC: k_elementwise<HEGPU_OP_ADDC><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_REDUCE: k_elementwise<HEGPU_OP_REDUCE><<<grid, kEwThreads, 0, st>>>(P); break;
+    default: throw HegpuError{HEGPU_E_ARG, "unknown elementwise op"};
+  }
+  check_cuda(cudaGetLastError(), "elementwise launch");
+}
+
+// ---------------------------------------------------------------------------
+// lifts (limbs_from_signed, ring.py:381-387; centered lifts ops.py:170-173)
+// ---------------------------------------------------------------------------
+
+struct LiftParams {
+  const void* src;
+  int64_t ss;
+  uint64_t* out;
+  int64_t os;
+  int k;
+  int log_n;
+  uint64_t src_q;  // centered mode: modulus of the source limb
+  const PrimeConst* pc;
+  uint8_t sel[kMaxPrimes];
+};
+
+template <bool CENTERED>
+__global__ void __launch_bounds__(kEwThreads) k_lift(const __grid_constant__ LiftParams P) {
+  const int N = 1 << P.log_n;
+  const int poly = blockIdx.y;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  int64_t v;
+  if (CENTERED) {
+    const uint64_t u = reinterpret_cast<const uint64_t*>(P.src)[poly * P.ss + x];
+    v = u > (P.src_q >> 1) ? (int64_t)u - (int64_t)P.src_q : (int64_t)u;
+  } else {
+    v = reinterpret_cast<const int64_t*>(P.src)[poly * P.ss + x];
+  }
+  uint64_t* o = P.out + poly * P.os + x;
+  for (int l = 0; l < P.k; ++l) o[(size_t)l * N] = signed_mod(v, P.pc[P.sel[l]]);
+}
+
+static void fill_sel(uint8_t* sel, const int32_t* primes, int k) {
+  if (k > kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+  for (int l = 0; l < k; ++l) {
+    if (primes[l] < 0 || primes[l] >= kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "bad prime index"};
+    sel[l] = (uint8_t)primes[l];
+  }
+}
+
+void launch_lift_signed(const PrimeConst* dpc, int log_n, const int64_t* src, int64_t ss,
+                        uint64_t* out, int64_t os, int n_polys, int k, const int32_t* primes,
+                        cudaStream_t st) {
+  if (n_polys == 0 || k == 0) return;
+  LiftParams P;
+  P.src = src;
+  P.ss = ss;
+  P.out = out;
+  P.os = os;
+  P.k = k;
+  P.log_n = log_n;
+  P.src_q = 0;
+  P.pc = dpc;
+  fill_sel(P.sel, primes, k);
+  const int n = 1 << log_n;
+  dim3 grid((n + kEwThreads - 1) / kEwThreads, n_polys);
+  ProfScope ps(PROF_LIFT, st, (double)n_polys * n * 8.0 * (1 + k), (double)n_polys * n * k);
+  k_lift<false><<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "lift launch");
+}
+
+void launch_lift_centered(const PrimeConst* dpc, int log_n, const uint64_t* src, int64_t ss,
+                          uint64_t src_q, uint64_t* out, int64_t os, int n_polys, int k,
+                          const int32_t* primes, cudaStream_t st) {
+  if (n_polys == 0 || k == 0) return;
+  LiftParams P;
+  P.src = src;
+  P.ss = ss;
+  P.out = out;
+  P.os = os;
+  P.k = k;
+  P.log_n = log_n;
+  P.src_q = src_q;
+  P.pc = dpc;
+  fill_sel(P.sel, primes, k);
+  const int n = 1 << log_n;
+  dim3 grid((n + kEwThreads - 1) / kEwThreads, n_polys);
+  ProfScope ps(PROF_LIFT, st, (double)n_polys * n * 8.0 * (1 + k), (double)n_polys * n * k);
+  k_lift<true><<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "lift launch");
+}
+
+// ---------------------------------------------------------------------------
+// automorphisms (ring.py:416-482)
+// ---------------------------------------------------------------------------
+
+struct AutoParams {
+  const uint64_t* in;
+  uint64_t* out;
+  int64_t is, os;
+  int k;
+  int log_n;
+  uint64_t g;  // odd, reduced mod 2N
+  const PrimeConst* pc;
+  uint8_t sel[kMaxPrimes];
+};
+
+// Eval form: slot i holds p(psi^(2 brev(i) + 1)); X -> X^g moves the value at
+// exponent e*g into slot i: out[i] = in[pos((2 brev(i) + 1) g mod 2N)] with
+// pos(e) = brev((e - 1) / 2) -- the closed form of _eval_exponent_map
+// (ring.py:440-468) for this NTT ordering.
+__global__ void __launch_bounds__(kEwThreads) k_auto_eval(const __grid_constant__ AutoParams P) {
+  const int log_n = P.log_n, N = 1 << log_n;
+  const int row = blockIdx.y + blockIdx.z * 65535;
+  const int i = blockIdx.x * kEwThreads + threadIdx.x;
+  if (i >= N) return;
+  const uint32_t mask2n = (2u << log_n) - 1u;
+  const uint32_t bi = __brev((uint32_t)i) >> (32 - log_n);
+  const uint32_t e = (uint32_t)(((uint64_t)(2u * bi + 1u) * P.g) & mask2n);
+  const uint32_t src = __brev((e - 1u) >> 1) >> (32 - log_n);
+  const int poly = row / P.k, limb = row - poly * P.k;
+  P.out[poly * P.os + (size_t)limb * N + i] = P.in[poly * P.is + (size_t)limb * N + src];
+}
+
+// Coefficient form: coefficient j moves to (j g mod 2N) with a sign flip when
+// the exponent wraps past N (X^N = -1).
+__global__ void __launch_bounds__(kEwThreads) k_auto_coeff(const __grid_constant__ AutoParams P) {
+  const int log_n = P.log_n, N = 1 << log_n;
+  const int row = blockIdx.y + blockIdx.z * 65535;
+  const int j = blockIdx.x * kEwThreads + threadIdx.x;
+  if (j >= N) return;
+  const int poly = row / P.k, limb = row - poly * P.k;
+  const uint64_t mask2n = (2ull << log_n) - 1ull;
+  const uint64_t e = ((uint64_t)j * P.g) & mask2n;
+  const uint64_t q = P.pc[P.sel[limb]].q;
+  const uint64_t v = P.in[poly * P.is + (size_t)limb * N + j];
+  const uint64_t tgt = e & (uint64_t)(N - 1);
+  P.out[poly * P.os + (size_t)limb * N + tgt] = (e >= (uint64_t)N) ? (v ? q - v : 0) : v;
+}
+
+void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint64_t g,
+                         const uint64_t* in, int64_t is, uint64_t* out, int64_t os, int n_polys,
+                         int k, const int32_t* primes, cudaStream_t st) {
+  const int rows = n_polys * k;
+  if (rows == 0) return;
+  AutoParams P;
+  P.in = in;
+  P.out = out;
+  P.is = is;
+  P.os = os;
+  P.k = k;
+  P.log_n = log_n;
+  P.g = g & ((2ull << log_n) - 1ull);
+  if ((P.g & 1ull) == 0) throw HegpuError{HEGPU_E_ARG, "automorphism exponent must be odd"};
+  P.pc = dpc;
+  fill_sel(P.sel, primes, k);
+  const dim3 grid = rows_grid(1 << log_n, rows, 1);
+  ProfScope ps(PROF_AUTOMORPHISM, st, (double)rows * (1 << log_n) * 16.0, 0.0);
+  if (eval_form)
+    k_auto_eval<<<grid, kEwThreads, 0, st>>>(P);
+  else
+    k_auto_coeff<<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "automorphism launch");
+}
+
+// ---------------------------------------------------------------------------
+// tensor product (ops.py:355-357) and encryption combine (ops.py:102-116)
+// ---------------------------------------------------------------------------
+
+
+
+// d1 = a0 b1 + a1 b0 is accumulated in 128 bits and reduced once.
+__global__ void __launch_bounds__(kEwThreads) k_tensor(const __grid_constant__ TensorParams P) {
+  const int N = 1 << P.log_n;
+  const int row = blockIdx.y + blockIdx.z * 65535;
+  const int poly = row / P.k, limb = row - poly * P.k;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const PrimeConst pc = P.pc[limb];
+  const size_t l = (size_t)limb * N + x;
+  const uint64_t a0 = P.a0[poly * P.as + l], a1 = P.a1[poly * P.as + l];
+  const uint64_t b0 = P.b0[poly * P.bs + l], b1 = P.b1[poly * P.bs + l];
+  P.d0[poly * P.ds + l] = mul_mod(a0, b0, pc);
+  Acc128 acc;
+  acc.zero();
+  acc.mac(a0, b1, pc.q);
+  acc.mac(a1, b0, pc.q);
+  P.d1[poly * P.ds + l] =
+      mont_mul(redc128(acc.hi, acc.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+  P.d2[poly * P.ds + l] = mul_mod(a1, b1, pc);
+}
+
+void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int n_polys,
+                   cudaStream_t st) {
+  const int rows = n_polys * T0.k;
+  if (rows == 0) return;
+  TensorParams T = T0;
+  T.pc = dpc;
+  T.log_n = log_n;
+  const dim3 grid = rows_grid(1 << log_n, rows, 1);
+  ProfScope ps(PROF_TENSOR, st, (double)rows * (1 << log_n) * 56.0,
+               (double)rows * (1 << log_n) * 8.0);
+  k_tensor<<<grid, kEwThreads, 0, st>>>(T);
+  check_cuda(cudaGetLastError(), "tensor launch");
+}
+
+
+
+__global__ void __launch_bounds__(kEwThreads) k_encrypt(const __grid_constant__ EncParams P) {
+  const int N = 1 << P.log_n;
+  const int limb = blockIdx.y;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const PrimeConst pc = P.pc[limb];
+  const size_t l = (size_t)limb * N + x;
+  const uint64_t v = P.v[l];
+  uint64_t c0 = add_mod(mul_mod(v, P.pb[l], pc), P.e0[l], pc.q);
+  if (P.m) c0 = add_mod(c0, P.m[l], pc.q);
+  P.c0[l] = c0;
+  P.c1[l] = add_mod(mul_mod(v, P.pa[l], pc), P.e1[l], pc.q);
+}
+
+void launch_encrypt(const PrimeConst* dpc, int log_n, const EncParams& E0, int k,
+                    cudaStream_t st) {
+  if (k == 0) return;
+  EncParams E = E0;
+  E.pc = dpc;
+  E.log_n = log_n;
+  dim3 grid(((1 << log_n) + kEwThreads - 1) / kEwThreads, k);
+  ProfScope ps(PROF_ENCRYPT, st, (double)k * (1 << log_n) * 8.0 * (E.m ? 9 : 8),
+               (double)k * (1 << log_n) * 4.0);
+  k_encrypt<<<grid, kEwThreads, 0, st>>>(E);
+  check_cuda(cudaGetLastError(), "encrypt launch");
+}
+
+// ---------------------------------------------------------------------------
+// plaintext-diagonal multiply-accumulate (bootstrap.py:222-241)
+// ---------------------------------------------------------------------------
+
+constexpr int kMaxDiagTerms = 32;
+struct DiagParams {
+  const uint64_t* ct[kMaxDiagTerms];
+  const uint64_t* pt[kMaxDiagTerms];
+  int n_terms;
+  int64_t ct_c1_off;
+  uint64_t* out;
+  int64_t out_c1_off;
+  int k, log_n;
+  int accumulate;
+  const PrimeConst* pc;
+};
+
+// out_c{0,1} (+)= sum_t pt[t] * ct[t].c{0,1}, one 128-bit accumulator per
+// component, one REDC pair per output.
+__global__ void __launch_bounds__(kEwThreads) k_diag_mac(const __grid_constant__ DiagParams P) {
+  const int N = 1 << P.log_n;
+  const int limb = blockIdx.y;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const PrimeConst pc = P.pc[limb];
+  const size_t l = (size_t)limb * N + x;
+  Acc128 a0, a1;
+  a0.zero();
+  a1.zero();
+  for (int t = 0; t < P.n_terms; ++t) {
+    const uint64_t p = P.pt[t][l];
+    a0.mac(P.ct[t][l], p, pc.q);
+    a1.mac(P.ct[t][P.ct_c1_off + l], p, pc.q);
+  }
+  uint64_t r0 = mont_mul(redc128(a0.hi, a0.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+  uint64_t r1 = mont_mul(redc128(a1.hi, a1.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+  if (P.accumulate) {
+    r0 = add_mod(r0, P.out[l], pc.q);
+    r1 = add_mod(r1, P.out[P.out_c1_off + l], pc.q);
+  }
+  P.out[l] = r0;
+  P.out[P.out_c1_off + l] = r1;
+}
+
+void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct,
+                     int64_t ct_c1_off, const uint64_t* const* pt, int n_terms, uint64_t* out,
+                     int64_t out_c1_off, int k, int accumulate, cudaStream_t st) {
+  int done = 0;
+  bool acc = accumulate != 0;
+  if (n_terms == 0 && !acc) throw HegpuError{HEGPU_E_ARG, "diag_mac with no terms"};
+  while (done < n_terms) {
+    DiagParams P;
+    P.n_terms = n_terms - done < kMaxDiagTerms ? n_terms - done : kMaxDiagTerms;
+    for (int t = 0; t < P.n_terms; ++t) {
+      P.ct[t] = ct[done + t];
+      P.pt[t] = pt[done + t];
+    }
+    P.ct_c1_off = ct_c1_off;
+    P.out = out;
+    P.out_c1_off = out_c1_off;
+    P.k = k;
+    P.log_n = log_n;
+    P.accumulate = acc ? 1 : 0;
+    P.pc = dpc;
+    dim3 grid(((1 << log_n) + kEwThreads - 1) / kEwThreads, k);
+    ProfScope ps(PROF_DIAG_MAC, st,
+                 (double)k * (1 << log_n) * 8.0 * (3.0 * P.n_terms + (acc ? 4 : 2)),
+                 (double)k * (1 << log_n) * (2.0 * P.n_terms + 4));
+    k_diag_mac<<<grid, kEwThreads, 0, st>>>(P);
+    check_cuda(cudaGetLastError(), "diag_mac launch");
+    done += P.n_terms;
+    acc = true;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fast basis conversion (BaseConverter.convert, keys.py:43-49;
+// base_convert, _kernels.py:300-317), one or several jobs per launch.
+// hat_i = x_i * (Q/q_i)^-1 mod q_i; out_t = REDC(sum_i hat_i * punc_mont[i][t]).
+// ---------------------------------------------------------------------------
+
+constexpr int kMaxConvSrc = 32;
+
+__global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ ConvParams P) {
+  const int N = 1 << P.log_n;
+  const int j = blockIdx.y;
+  const int poly = blockIdx.z;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const ConvJob& J = P.job[j];
+  uint64_t hat[kMaxConvSrc];
+  const uint64_t* src = J.src + poly * J.src_stride + x;
+#pragma unroll
+  for (int i = 0; i < kMaxConvSrc; ++i) {
+    if (i < J.n_src) {
+      const uint64_t q = P.pc[P.src_sel[j][i]].q;
+      const uint64_t v = src[(size_t)i * N];
+      hat[i] = J.inv ? shoup(v, J.inv[i], J.inv_sh[i], q) : v;
+    }
+  }
+  uint64_t* dst = J.dst + poly * J.dst_stride + x;
+  for (int t = 0; t < J.n_dst; ++t) {
+    const PrimeConst pc = P.pc[P.dst_sel[j][t]];
+    Acc128 acc;
+    acc.zero();
+#pragma unroll
+    for (int i = 0; i < kMaxConvSrc; ++i)
+      if (i < J.n_src) acc.mac(hat[i], J.punc[(size_t)i * J.punc_ld + t], pc.q);
+    dst[(size_t)t * N] = redc128(acc.hi, acc.lo, pc.q, pc.qinv_neg);
+  }
+}
+
+void launch_conv(ConvParams& P, cudaStream_t st) {
+  if (P.n_jobs == 0 || P.n_polys == 0) return;
+  for (int j = 0; j < P.n_jobs; ++j)
+    if (P.job[j].n_src > kMaxConvSrc) throw HegpuError{HEGPU_E_ARG, "too many source limbs"};
+  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_jobs, P.n_polys);
+  double cb = 0, cm = 0;
+  for (int j = 0; j < P.n_jobs; ++j) {
+    cb += (double)P.n_polys * (1 << P.log_n) * 8.0 * (P.job[j].n_src + P.job[j].n_dst);
+    cm += (double)P.n_polys * (1 << P.log_n) *
+          ((double)P.job[j].n_src * P.job[j].n_dst + P.job[j].n_src);
+  }
+  ProfScope ps(PROF_CONV, st, cb, cm);
+  k_conv<<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "conv launch");
+}
+
+// ---------------------------------------------------------------------------
+// key-switch inner product (keys.py:299-323 / fma_gather_inplace,
+// _kernels.py:271-286), batched: the (digit x row) key values of a coefficient
+// are loaded once and applied to every ciphertext of the batch.
+// ---------------------------------------------------------------------------
+
+
+
+__global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ IpParams P) {
+  const int N = 1 << P.log_n;
+  const int r = blockIdx.y;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
+  const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
+  const PrimeConst pc = P.pc[prime];
+  uint64_t kb[kMaxDigits], ka[kMaxDigits];
+#pragma unroll
+  for (int j = 0; j < kMaxDigits; ++j) {
+    if (j < P.beta) {
+      kb[j] = P.kb[j][(size_t)krow * N + x];
+      ka[j] = P.ka[j][(size_t)krow * N + x];
+    }
+  }
+  for (int b = 0; b < P.n_batch; ++b) {
+    Acc128 ab, aa;
+    ab.zero();
+    aa.zero();
+#pragma unroll
+    for (int j = 0; j < kMaxDigits; ++j) {
+      if (j < P.beta) {
+        const int g0 = j * P.alpha;
+        const int g1 = min(g0 + P.alpha, P.level + 1);
+        uint64_t v;
+        if (r >= g0 && r < g1)
+          v = P.d[b * P.ds + (size_t)r * N + x];
+        else
+          v = P.ext[b * P.ext_sb + j * P.ext_sj + (size_t)(r < g0 ? r : r - (g1 - g0)) * N + x];
+        ab.mac(v, kb[j], pc.q);
+        aa.mac(v, ka[j], pc.q);
+      }
+    }
+    uint64_t* o = P.acc + b * P.acc_sb + (size_t)r * N + x;
+    o[0] = mont_mul(redc128(ab.hi, ab.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+    o[(size_t)P.n_ext * N] =
+        mont_mul(redc128(aa.hi, aa.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+  }
+}
+
+void launch_ks_ip(IpParams& P, cudaStream_t st) {
+  if (P.beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
+  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext);
+  const double ipn = (double)(1 << P.log_n) * P.n_ext;
+  ProfScope ps(PROF_KS_IP, st, ipn * 8.0 * (2.0 * P.beta + P.n_batch * (P.beta + 2.0)),
+               ipn * P.n_batch * (2.0 * P.beta + 4));
+  k_ks_ip<<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "ks inner product launch");
+}
+
+}  // namespace hegpu
+
+namespace hegpu {
+
+// ---------------------------------------------------------------------------
+// INT64 modular-multiplication peak microbenchmark (the roofline denominator
+// for the NTT / key-switch INT bound; MEASURED_PEAKS.json has no INT peak).
+// Each thread runs 8 independent chains of Shoup (w, w') multiplications --
+// the NTT butterfly's product -- so the FMA/ALU pipes, not latency, bound it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_modmul_peak(uint64_t* sink, uint64_t q, uint64_t w,
+                                                     uint64_t wsh, int iters) {
+  uint64_t x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = (threadIdx.x * 8 + c + blockIdx.x) % q;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = shoup_lazy(x[c], w, wsh, q);
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc ^= x[c];
+  if (acc == 0x123456789ull) sink[0] = acc;  // keep the chains alive
+}
+
+double bench_modmul_peak(int iters) {
+  const uint64_t q = 0xffffffffffc0001ull;  // 60-bit prime of the P16 chain
+  const uint64_t w = 0x123456789abcdull % q;
+  const uint64_t wsh = h_shoup(w, q);
+  int dev = 0, sms = 0;
+  check_cuda(cudaGetDevice(&dev), "device");
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  uint64_t* sink = nullptr;
+  check_cuda(cudaMalloc(&sink, 8), "alloc");
+  const int blocks = sms * 8, threads = 256;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_modmul_peak<<<blocks, threads>>>(sink, q, w, wsh, 64);  // warm-up
+  cudaEventRecord(a);
+  k_modmul_peak<<<blocks, threads>>>(sink, q, w, wsh, iters);
+  cudaEventRecord(b);
+  check_cuda(cudaEventSynchronize(b), "modmul bench");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  return (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+}
+
+}  // namespace hegpu

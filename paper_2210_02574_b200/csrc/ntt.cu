@@ -1,0 +1,267 @@
+// Batched negacyclic NTT for sm_100a.
+//
+// Bit-exact with the reference transforms (hebert/_kernels.py:144-204): same
+// psi (ring.py:69-78), same bit-reversed twiddle tables (ring.py:94-108), same
+// natural -> bit-reversed (forward CT) / bit-reversed -> natural (inverse GS,
+// times N^-1) orderings.  Modular arithmetic is exact, so any schedule of the
+// same butterflies produces identical residues; ours is:
+//
+//   N = R * C with R = 2^a, a = ceil(log N / 2).
+//   forward  pass A ("cols"):  stages 0..a-1 act on R-element columns
+//                               (stride C), independent per column, same
+//                               twiddles for every column;
+//            pass B ("blocks"): stages a..logN-1 act on contiguous C-element
+//                               blocks.
+//   inverse  pass B first (stages with span < C), pass A last with N^-1 and
+//            the last twiddle folded into the final butterfly.
+//
+// Each CTA stages a 4096-element tile (32 KiB) in shared memory; a limb of
+// N = 2^16 is 16 tiles, so every launch has (16 x limbs x polys) CTAs.
+// Intermediate values stay in Harvey lazy ranges ([0,4q) forward, [0,2q)
+// inverse); outputs are fully reduced.
+#include "ring.cuh"
+
+namespace hegpu {
+
+struct NttParams {
+  SegSet S;
+  const PrimeConst* pc;
+  const uint64_t* tw;
+  int log_n;
+  int a;
+  int tile_log;  // log2 of the CPB / BPC group size
+  int epi;
+  uint64_t c[kMaxPrimes];
+  uint64_t csh[kMaxPrimes];
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(256) k_ntt_cols(const __grid_constant__ NttParams P) {
+  extern __shared__ uint64_t sm[];
+  const int log_n = P.log_n, N = 1 << log_n, a = P.a, R = 1 << a, C = N >> a;
+  const int cpb_log = P.tile_log, CPB = 1 << cpb_log;
+  const int row = blockIdx.y;
+  const int s = find_seg(P.S, row);
+  const Seg& sg = P.S.seg[s];
+  const int rr = row - sg.row_start;
+  const int poly = rr / sg.k, limb = rr - poly * sg.k;
+  const int prime = P.S.sel[s][limb];
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t q = pc.q, q2 = q << 1;
+  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
+  const uint64_t* wsh = w + N;
+  const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
+                            : (sg.in + poly * sg.in_stride + (size_t)limb * N);
+  uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
+  const int c0 = blockIdx.x << cpb_log;
+  const int tile = R << cpb_log;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    const int r = e >> cpb_log, c = e & (CPB - 1);
+    sm[e] = src[c0 + c + (size_t)C * r];
+  }
+  __syncthreads();
+  const int nb = tile >> 1;
+  if (!INV) {
+    for (int st = 0; st < a; ++st) {
+      const int hl = a - st - 1;  // log2 of the row distance
+      const int hr = 1 << hl;
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const int c = b & (CPB - 1), bi = b >> cpb_log;
+        const int grp = bi >> hl, off = bi & (hr - 1);
+        const int r0 = (grp << (hl + 1)) + off;
+        const int ti = (1 << st) + grp;
+        const int i0 = (r0 << cpb_log) + c, i1 = i0 + (hr << cpb_log);
+        uint64_t x = sm[i0];
+        const uint64_t y = sm[i1];
+        x = x >= q2 ? x - q2 : x;
+        const uint64_t v = shoup_lazy(y, w[ti], wsh[ti], q);
+        sm[i0] = x + v;
+        sm[i1] = x - v + q2;
+      }
+      __syncthreads();
+    }
+  } else {
+    const int u0 = log_n - a;
+    for (int st = 0; st < a; ++st) {
+      const int u = u0 + st;
+      const int tr = 1 << st;
+      const int h = N >> (u + 1);
+      const bool last = (st == a - 1);
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const int c = b & (CPB - 1), bi = b >> cpb_log;
+        const int grp = bi >> st, off = bi & (tr - 1);
+        const int r0 = (grp << (st + 1)) + off;
+        const int i0 = (r0 << cpb_log) + c, i1 = i0 + (tr << cpb_log);
+        const uint64_t x = sm[i0], y = sm[i1];
+        uint64_t sum = x + y;
+        sum = sum >= q2 ? sum - q2 : sum;
+        const uint64_t d = x - y + q2;
+        if (!last) {
+          const int ti = h + grp;
+          sm[i0] = sum;
+          sm[i1] = shoup_lazy(d, w[ti], wsh[ti], q);
+        } else {
+          sm[i0] = shoup(sum, pc.ninv, pc.ninv_sh, q);
+          sm[i1] = shoup(d, pc.ilast, pc.ilast_sh, q);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    const int r = e >> cpb_log, c = e & (CPB - 1);
+    dst[c0 + c + (size_t)C * r] = sm[e];
+  }
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttParams P) {
+  extern __shared__ uint64_t sm[];
+  const int log_n = P.log_n, N = 1 << log_n, a = P.a;
+  const int B = N >> a, blog = log_n - a;
+  const int bpc_log = P.tile_log;
+  const int row = blockIdx.y;
+  const int s = find_seg(P.S, row);
+  const Seg& sg = P.S.seg[s];
+  const int rr = row - sg.row_start;
+  const int poly = rr / sg.k, limb = rr - poly * sg.k;
+  const int prime = P.S.sel[s][limb];
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t q = pc.q, q2 = q << 1;
+  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
+  const uint64_t* wsh = w + N;
+  const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + (size_t)limb * N)
+                            : (sg.out + poly * sg.out_stride + (size_t)limb * N);
+  uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
+  const int blk0 = blockIdx.x << bpc_log;
+  const int tile = B << bpc_log;
+  const size_t base = (size_t)blk0 * B;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = src[base + e];
+  __syncthreads();
+  const int nb = tile >> 1;
+  const int hb_log = blog - 1;  // log2(B/2)
+  if (!INV) {
+    for (int st = a; st < log_n; ++st) {
+      const int tl = log_n - st - 1;  // log2 t
+      const int t = 1 << tl;
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const int bl = b >> hb_log, bi = b & ((1 << hb_log) - 1);
+        const int grp = bi >> tl, off = bi & (t - 1);
+        const int l0 = (grp << (tl + 1)) + off;
+        const int ti = (1 << st) + ((blk0 + bl) << (blog - tl - 1)) + grp;
+        const int i0 = (bl << blog) + l0, i1 = i0 + t;
+        uint64_t x = sm[i0];
+        const uint64_t y = sm[i1];
+        x = x >= q2 ? x - q2 : x;
+        const uint64_t v = shoup_lazy(y, w[ti], wsh[ti], q);
+        sm[i0] = x + v;
+        sm[i1] = x - v + q2;
+      }
+      __syncthreads();
+    }
+    if (P.epi) {
+      const uint64_t* other = sg.other + poly * sg.other_stride + (size_t)limb * N + base;
+      uint64_t* eout = sg.eout + poly * sg.eout_stride + (size_t)limb * N + base;
+      const uint64_t cc = P.c[limb], ccsh = P.csh[limb];
+      for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+        uint64_t y = sm[e];
+        y = y >= q2 ? y - q2 : y;
+        y = y >= q ? y - q : y;
+        eout[e] = shoup(other[e] + q - y, cc, ccsh, q);
+      }
+      return;
+    }
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+      uint64_t y = sm[e];
+      y = y >= q2 ? y - q2 : y;
+      y = y >= q ? y - q : y;
+      dst[base + e] = y;
+    }
+  } else {
+    for (int u = 0; u < blog; ++u) {
+      const int t = 1 << u;
+      const int h = N >> (u + 1);
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const int bl = b >> hb_log, bi = b & ((1 << hb_log) - 1);
+        const int grp = bi >> u, off = bi & (t - 1);
+        const int l0 = (grp << (u + 1)) + off;
+        const int ti = h + ((blk0 + bl) << (blog - u - 1)) + grp;
+        const int i0 = (bl << blog) + l0, i1 = i0 + t;
+        const uint64_t x = sm[i0], y = sm[i1];
+        uint64_t sum = x + y;
+        sum = sum >= q2 ? sum - q2 : sum;
+        sm[i0] = sum;
+        sm[i1] = shoup_lazy(x - y + q2, w[ti], wsh[ti], q);
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) dst[base + e] = sm[e];
+  }
+}
+
+static inline bool P_epi_guard(const NttEpilogue* e) { return e && e->enabled; }
+
+static inline int ilog2(int x) {
+  int r = 0;
+  while ((1 << r) < x) ++r;
+  return r;
+}
+
+void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inverse,
+                SegSet& S, const NttEpilogue* epi, cudaStream_t st) {
+  if (S.n_rows == 0) return;
+  if (S.n_rows > 65535) throw HegpuError{1, "NTT batch exceeds 65535 limbs"};
+  NttParams local;
+  local.S = S;
+  local.pc = dpc;
+  local.tw = dtw;
+  local.log_n = log_n;
+  const int a = (log_n + 1) / 2;
+  local.a = a;
+  local.epi = (epi && epi->enabled) ? 1 : 0;
+  if (local.epi) {
+    for (int i = 0; i < kMaxPrimes; ++i) {
+      local.c[i] = epi->c[i];
+      local.csh[i] = epi->csh[i];
+    }
+  }
+  const int N = 1 << log_n, R = 1 << a, C = N >> a;
+  const int kTile = 4096;
+  int cpb = kTile / R;
+  if (cpb < 1) cpb = 1;
+  if (cpb > C) cpb = C;
+  int bpc = kTile / C;
+  if (bpc < 1) bpc = 1;
+  if (bpc > R) bpc = R;
+  const int tile_a = R * cpb, tile_b = C * bpc;
+  const int thr_a = tile_a / 2 < 256 ? tile_a / 2 : 256;
+  const int thr_b = tile_b / 2 < 256 ? tile_b / 2 : 256;
+  dim3 grid_a(C / cpb, S.n_rows), grid_b(R / bpc, S.n_rows);
+  NttParams pa = local, pb = local;
+  const double rows = S.n_rows, nn = N;
+  const double bytes_pass = rows * nn * 8.0;  // half of the transform's read+write
+  const double mm_a = rows * nn / 2 * a + (inverse ? rows * nn : 0.0);
+  const double mm_b = rows * nn / 2 * (log_n - a) + ((P_epi_guard(epi)) ? rows * nn : 0.0);
+  pa.tile_log = ilog2(cpb);
+  pb.tile_log = ilog2(bpc);
+  if (!inverse) {
+    pa.epi = 0;
+    {
+      ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
+      k_ntt_cols<false><<<grid_a, thr_a, tile_a * 8, st>>>(pa);
+    }
+    // the epilogue reads one more operand per element
+    ProfScope ps(PROF_NTT, st, bytes_pass * (P_epi_guard(epi) ? 1.5 : 1.0), mm_b);
+    k_ntt_blocks<false><<<grid_b, thr_b, tile_b * 8, st>>>(pb);
+  } else {
+    {
+      ProfScope ps(PROF_NTT, st, bytes_pass, rows * nn / 2 * (log_n - a));
+      k_ntt_blocks<true><<<grid_b, thr_b, tile_b * 8, st>>>(pb);
+    }
+    ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
+    k_ntt_cols<true><<<grid_a, thr_a, tile_a * 8, st>>>(pa);
+  }
+  check_cuda(cudaGetLastError(), "ntt launch");
+}
+
+}  // namespace hegpu

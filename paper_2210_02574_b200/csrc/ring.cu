@@ -1,0 +1,980 @@
+// Ring context, fused CKKS operations (key switch, rescale, ModRaise,
+// encryption) and the C ABI of libhegpu.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ring.cuh"
+
+namespace hegpu {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& m) { g_last_error = m; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw HegpuError{HEGPU_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+// --- launch accounting / profiling ------------------------------------------
+static std::atomic<long long> g_launches{0};
+static std::atomic<bool> g_prof_on{false};
+static std::mutex g_prof_mu;
+struct ProfRec {
+  int cls;
+  double bytes, modmuls;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+
+ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double modmuls) : st(s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  ProfRec r;
+  r.cls = cls;
+  r.bytes = bytes;
+  r.modmuls = modmuls;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  slot = (int)g_prof.size();
+  g_prof.push_back(r);
+}
+ProfScope::~ProfScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventRecord(g_prof[slot].b, st);
+}
+
+// Stream-ordered scratch from the device's default memory pool (cached: the
+// pool's release threshold is raised at ring creation).
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st;
+  Scratch(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes) check_cuda(cudaMallocAsync(&p, bytes, s), "scratch alloc");
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  uint64_t* u64() const { return static_cast<uint64_t*>(p); }
+};
+
+// --- host number theory (ring.py:60-128, 217-238) ---------------------------
+
+static bool is_prime_u64(uint64_t n) {
+  if (n < 2) return false;
+  static const uint64_t small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (uint64_t p : small)
+    if (n % p == 0) return n == p;
+  uint64_t d = n - 1;
+  int s = 0;
+  while ((d & 1) == 0) {
+    d >>= 1;
+    ++s;
+  }
+  for (uint64_t a : small) {
+    uint64_t x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < s; ++r) {
+      x = h_mulmod(x, x, n);
+      if (x == n - 1) {
+        comp = false;
+        break;
+      }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
+// First base in [2, 10^4) whose (q-1)/2N power has order exactly 2N
+// (find_primitive_2n_root, ring.py:69-78).
+static uint64_t find_psi(uint64_t q, uint64_t two_n) {
+  if ((q - 1) % two_n != 0) throw HegpuError{HEGPU_E_ARG, "modulus is not NTT-friendly"};
+  const uint64_t e = (q - 1) / two_n;
+  for (uint64_t base = 2; base < 10000; ++base) {
+    const uint64_t cand = h_powmod(base, e, q);
+    if (h_powmod(cand, two_n / 2, q) == q - 1) return cand;
+  }
+  throw HegpuError{HEGPU_E_ARG, "no primitive root found"};
+}
+
+static uint64_t neg_inv_2_64(uint64_t q) {
+  uint64_t x = q;  // correct to 3 bits for odd q
+  for (int i = 0; i < 5; ++i) x *= 2 - q * x;
+  return 0 - x;
+}
+
+static inline uint32_t brev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1u) << (bits - 1 - b);
+  return r;
+}
+
+PrimeConst make_prime_const(uint64_t q, int log_n, uint64_t ipsi1) {
+  PrimeConst c;
+  c.q = q;
+  c.qinv_neg = neg_inv_2_64(q);
+  const uint64_t r = h_rmod(q);
+  c.r2 = h_mulmod(r, r, q);
+  c.bar = h_shoup(1, q);
+  c.ninv = h_inv((uint64_t)1 << log_n, q);
+  c.ninv_sh = h_shoup(c.ninv, q);
+  c.ilast = h_mulmod(ipsi1, c.ninv, q);
+  c.ilast_sh = h_shoup(c.ilast, q);
+  return c;
+}
+
+// Twiddles of one prime: psi_rev, shoup, ipsi_rev, shoup (natural form).
+static void make_twiddles(uint64_t q, int log_n, uint64_t* out4n) {
+  const uint64_t n = 1ull << log_n;
+  const uint64_t psi = find_psi(q, 2 * n);
+  const uint64_t ipsi = h_inv(psi, q);
+  std::vector<uint64_t> pw(n), ipw(n);
+  uint64_t x = 1, ix = 1;
+  for (uint64_t i = 0; i < n; ++i) {
+    pw[i] = x;
+    ipw[i] = ix;
+    x = h_mulmod(x, psi, q);
+    ix = h_mulmod(ix, ipsi, q);
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t rv = brev((uint32_t)i, log_n);
+    out4n[i] = pw[rv];
+    out4n[n + i] = h_shoup(pw[rv], q);
+    out4n[2 * n + i] = ipw[rv];
+    out4n[3 * n + i] = h_shoup(ipw[rv], q);
+  }
+}
+
+Ring::~Ring() {
+  for (auto& kv : ks)
+    if (kv.second->dmem) cudaFree(kv.second->dmem);
+  if (dpc) cudaFree(dpc);
+  if (dtw) cudaFree(dtw);
+}
+
+static uint64_t prod_mod(const std::vector<uint64_t>& ps, int skip, uint64_t m) {
+  uint64_t r = 1 % m;
+  for (int i = 0; i < (int)ps.size(); ++i)
+    if (i != skip) r = h_mulmod(r, ps[i] % m, m);
+  return r;
+}
+
+const KsLevel& Ring::ks_level(int level, int alpha) {
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(level, alpha);
+  auto it = ks.find(key);
+  if (it != ks.end()) return *it->second;
+  if (level < 0 || level >= n_chain) throw HegpuError{HEGPU_E_ARG, "level out of range"};
+  if (alpha < 1) throw HegpuError{HEGPU_E_ARG, "digit size must be >= 1"};
+  auto L = std::make_unique<KsLevel>();
+  const int k = level + 1, K = n_special, n_ext = k + K;
+  const int beta = (k + alpha - 1) / alpha;
+  L->level = level;
+  L->alpha = alpha;
+  L->beta = beta;
+  L->n_ext = n_ext;
+  L->K = K;
+  std::vector<uint64_t> mu_inv(k), mu_inv_sh(k), mu_punc((size_t)k * n_ext, 0);
+  L->dst_prime_of_digit.assign((size_t)beta * n_ext, -1);
+  for (int j = 0; j < beta; ++j) {
+    const int g0 = j * alpha, g1 = std::min(g0 + alpha, k);
+    std::vector<uint64_t> grp(primes.begin() + g0, primes.begin() + g1);
+    std::vector<int> dst;
+    for (int r = 0; r < n_ext; ++r) {
+      if (r >= g0 && r < g1) continue;
+      dst.push_back(r <= level ? r : n_chain + (r - level - 1));
+    }
+    for (int t = 0; t < (int)dst.size(); ++t) L->dst_prime_of_digit[(size_t)j * n_ext + t] = dst[t];
+    for (int i = 0; i < (int)grp.size(); ++i) {
+      const uint64_t qi = grp[i];
+      const uint64_t inv = h_inv(prod_mod(grp, i, qi), qi);
+      mu_inv[g0 + i] = inv;
+      mu_inv_sh[g0 + i] = h_shoup(inv, qi);
+      for (int t = 0; t < (int)dst.size(); ++t) {
+        const uint64_t p = primes[dst[t]];
+        mu_punc[(size_t)(g0 + i) * n_ext + t] = h_mulmod(prod_mod(grp, i, p), h_rmod(p), p);
+      }
+    }
+  }
+  std::vector<uint64_t> sp(primes.begin() + n_chain, primes.end());
+  std::vector<uint64_t> md_inv(K), md_inv_sh(K), md_punc((size_t)K * k);
+  for (int i = 0; i < K; ++i) {
+    const uint64_t si = sp[i];
+    md_inv[i] = h_inv(prod_mod(sp, i, si), si);
+    md_inv_sh[i] = h_shoup(md_inv[i], si);
+    for (int t = 0; t < k; ++t) {
+      const uint64_t q = primes[t];
+      md_punc[(size_t)i * k + t] = h_mulmod(prod_mod(sp, i, q), h_rmod(q), q);
+    }
+  }
+  L->pinv.resize(k);
+  L->pinv_sh.resize(k);
+  for (int t = 0; t < k; ++t) {
+    const uint64_t q = primes[t];
+    L->pinv[t] = h_inv(prod_mod(sp, -1, q), q);
+    L->pinv_sh[t] = h_shoup(L->pinv[t], q);
+  }
+  const size_t total = mu_inv.size() * 2 + mu_punc.size() + md_inv.size() * 2 + md_punc.size();
+  std::vector<uint64_t> host;
+  host.reserve(total);
+  auto append = [&](const std::vector<uint64_t>& v) {
+    const size_t off = host.size();
+    host.insert(host.end(), v.begin(), v.end());
+    return off;
+  };
+  const size_t o1 = append(mu_inv), o2 = append(mu_inv_sh), o3 = append(mu_punc);
+  const size_t o4 = append(md_inv), o5 = append(md_inv_sh), o6 = append(md_punc);
+  check_cuda(cudaMalloc(&L->dmem, std::max<size_t>(total, 1) * 8), "ks const alloc");
+  check_cuda(cudaMemcpy(L->dmem, host.data(), total * 8, cudaMemcpyHostToDevice), "ks const copy");
+  L->mu_inv = L->dmem + o1;
+  L->mu_inv_sh = L->dmem + o2;
+  L->mu_punc = L->dmem + o3;
+  L->md_inv = L->dmem + o4;
+  L->md_inv_sh = L->dmem + o5;
+  L->md_punc = L->dmem + o6;
+  const KsLevel& ref = *L;
+  ks[key] = std::move(L);
+  return ref;
+}
+
+const std::pair<std::vector<uint64_t>, std::vector<uint64_t>>& Ring::rescale_consts(int level) {
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = rescale.find(level);
+  if (it != rescale.end()) return it->second;
+  std::vector<uint64_t> c(level), csh(level);
+  const uint64_t ql = primes[level];
+  for (int i = 0; i < level; ++i) {
+    c[i] = h_inv(ql % primes[i], primes[i]);
+    csh[i] = h_shoup(c[i], primes[i]);
+  }
+  return rescale[level] = std::make_pair(c, csh);
+}
+
+static Ring* create_ring(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
+                         int n_special) {
+  if (log_n < 4 || log_n > 17) throw HegpuError{HEGPU_E_ARG, "ring degree must be 2^4..2^17"};
+  if (n_chain < 1 || n_special < 0 || n_chain + n_special > kMaxPrimes)
+    throw HegpuError{HEGPU_E_ARG, "bad prime counts"};
+  auto R = std::make_unique<Ring>();
+  R->log_n = log_n;
+  R->n = 1 << log_n;
+  R->n_chain = n_chain;
+  R->n_special = n_special;
+  R->n_primes = n_chain + n_special;
+  R->primes.assign(chain, chain + n_chain);
+  R->primes.insert(R->primes.end(), special, special + n_special);
+  for (size_t i = 0; i < R->primes.size(); ++i) {
+    const uint64_t q = R->primes[i];
+    if (q >= (1ull << 62)) throw HegpuError{HEGPU_E_ARG, "modulus >= 2^62"};
+    if (q % (2ull * R->n) != 1) throw HegpuError{HEGPU_E_ARG, "modulus != 1 mod 2N"};
+    if (!is_prime_u64(q)) throw HegpuError{HEGPU_E_ARG, "modulus is not prime"};
+    for (size_t j = 0; j < i; ++j)
+      if (R->primes[j] == q) throw HegpuError{HEGPU_E_ARG, "duplicate modulus"};
+  }
+  check_cuda(cudaGetDevice(&R->device), "get device");
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, R->device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  const size_t n = R->n;
+  std::vector<uint64_t> tw(R->primes.size() * 4 * n);
+  R->hpc.resize(R->primes.size());
+  for (size_t i = 0; i < R->primes.size(); ++i) {
+    uint64_t* t = tw.data() + i * 4 * n;
+    make_twiddles(R->primes[i], log_n, t);
+    R->hpc[i] = make_prime_const(R->primes[i], log_n, t[2 * n + 1]);
+  }
+  check_cuda(cudaMalloc(&R->dpc, R->hpc.size() * sizeof(PrimeConst)), "alloc consts");
+  check_cuda(cudaMemcpy(R->dpc, R->hpc.data(), R->hpc.size() * sizeof(PrimeConst),
+                        cudaMemcpyHostToDevice),
+             "copy consts");
+  check_cuda(cudaMalloc(&R->dtw, tw.size() * 8), "alloc twiddles");
+  check_cuda(cudaMemcpy(R->dtw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice),
+             "copy twiddles");
+  return R.release();
+}
+
+// --- helpers ----------------------------------------------------------------
+
+static void add_seg(SegSet& S, const uint64_t* in, int64_t is, uint64_t* out, int64_t os,
+                    int n_polys, int k, const int32_t* primes) {
+  if (S.n_seg >= kMaxSeg) throw HegpuError{HEGPU_E_ARG, "too many segments"};
+  if (k > kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+  Seg& g = S.seg[S.n_seg];
+  g.in = in;
+  g.out = out;
+  g.in_stride = is;
+  g.out_stride = os;
+  g.other = nullptr;
+  g.eout = nullptr;
+  g.other_stride = 0;
+  g.eout_stride = 0;
+  g.n_polys = n_polys;
+  g.k = k;
+  g.row_start = S.n_rows;
+  for (int l = 0; l < k; ++l) {
+    if (primes[l] < 0 || primes[l] >= kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "bad prime index"};
+    S.sel[S.n_seg][l] = (uint8_t)primes[l];
+  }
+  S.n_rows += n_polys * k;
+  S.n_seg++;
+}
+
+static std::vector<int32_t> range_primes(int first, int count) {
+  std::vector<int32_t> v(count);
+  for (int i = 0; i < count; ++i) v[i] = first + i;
+  return v;
+}
+
+static void ntt_simple(Ring& R, bool inverse, const uint64_t* in, int64_t is, uint64_t* out,
+                       int64_t os, int n_polys, int k, const int32_t* primes, cudaStream_t st) {
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  add_seg(S, in, is, out, os, n_polys, k, primes);
+  launch_ntt(R.dpc, R.dtw, R.log_n, inverse, S, nullptr, st);
+}
+
+// --- hybrid key switching (keys.py:278-339) --------------------------------
+
+static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds, int B,
+                          const uint64_t* const* key_b, const uint64_t* const* key_a,
+                          int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t os,
+                          cudaStream_t st) {
+  if (B <= 0) return;
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, K = R.n_special, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many digits"};
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  const std::vector<int32_t> chain = range_primes(0, k);
+  // 1. d -> coefficient form
+  ntt_simple(R, true, d, ds, dcoeff, (int64_t)k * N, B, k, chain.data(), st);
+  // 2. ModUp basis conversion of every digit, 3. NTT of the converted rows
+  for (int j0 = 0; j0 < beta; j0 += kMaxSeg) {
+    const int jn = std::min(kMaxSeg, beta - j0);
+    ConvParams C;
+    C.n_jobs = jn;
+    C.n_polys = B;
+    C.log_n = R.log_n;
+    C.pc = R.dpc;
+    SegSet S;
+    S.n_seg = 0;
+    S.n_rows = 0;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int j = j0 + jj;
+      const int g0 = j * alpha, g1 = std::min(g0 + alpha, k), g = g1 - g0;
+      const int n_dst = n_ext - g;
+      ConvJob& J = C.job[jj];
+      J.src = dcoeff + (size_t)g0 * N;
+      J.src_stride = (int64_t)k * N;
+      J.dst = ext + (size_t)j * n_ext * N;
+      J.dst_stride = (int64_t)beta * n_ext * N;
+      J.n_src = g;
+      J.n_dst = n_dst;
+      J.inv = L.mu_inv + g0;
+      J.inv_sh = L.mu_inv_sh + g0;
+      J.punc = L.mu_punc + (size_t)g0 * n_ext;
+      J.punc_ld = n_ext;
+      for (int i = 0; i < g; ++i) C.src_sel[jj][i] = (uint8_t)(g0 + i);
+      std::vector<int32_t> dsel(n_dst);
+      for (int t = 0; t < n_dst; ++t) {
+        dsel[t] = L.dst_prime_of_digit[(size_t)j * n_ext + t];
+        C.dst_sel[jj][t] = (uint8_t)dsel[t];
+      }
+      if (n_dst > 0)
+        add_seg(S, J.dst, J.dst_stride, J.dst, J.dst_stride, B, n_dst, dsel.data());
+    }
+    launch_conv(C, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+  }
+  // 4. inner product with the key digits
+  IpParams P;
+  P.d = d;
+  P.ds = ds;
+  P.ext = ext;
+  P.ext_sb = (int64_t)beta * n_ext * N;
+  P.ext_sj = (int64_t)n_ext * N;
+  for (int j = 0; j < beta; ++j) {
+    P.kb[j] = key_b[j];
+    P.ka[j] = key_a[j];
+  }
+  P.acc = acc;
+  P.acc_sb = (int64_t)2 * n_ext * N;
+  P.level = level;
+  P.alpha = alpha;
+  P.beta = beta;
+  P.n_ext = n_ext;
+  P.n_chain = R.n_chain;
+  P.key_sp_row0 = R.n_chain;
+  P.n_batch = B;
+  P.log_n = R.log_n;
+  P.pc = R.dpc;
+  launch_ks_ip(P, st);
+  // 5. ModDown: INTT(specials), convert specials -> chain, NTT, (acc - corr) P^-1
+  if (K > 0) {
+    const std::vector<int32_t> sp = range_primes(R.n_chain, K);
+    ntt_simple(R, true, acc + (size_t)k * N, (int64_t)n_ext * N, acc + (size_t)k * N,
+               (int64_t)n_ext * N, 2 * B, K, sp.data(), st);
+    ConvParams C;
+    C.n_jobs = 1;
+    C.n_polys = 2 * B;
+    C.log_n = R.log_n;
+    C.pc = R.dpc;
+    ConvJob& J = C.job[0];
+    J.src = acc + (size_t)k * N;
+    J.src_stride = (int64_t)n_ext * N;
+    J.dst = corr;
+    J.dst_stride = (int64_t)k * N;
+    J.n_src = K;
+    J.n_dst = k;
+    J.inv = L.md_inv;
+    J.inv_sh = L.md_inv_sh;
+    J.punc = L.md_punc;
+    J.punc_ld = k;
+    for (int i = 0; i < K; ++i) C.src_sel[0][i] = (uint8_t)(R.n_chain + i);
+    for (int t = 0; t < k; ++t) C.dst_sel[0][t] = (uint8_t)t;
+    launch_conv(C, st);
+  } else {
+    check_cuda(cudaMemsetAsync(corr, 0, sz_corr * 8, st), "memset");
+  }
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  add_seg(S, corr, (int64_t)2 * k * N, corr, (int64_t)2 * k * N, B, k, chain.data());
+  add_seg(S, corr + (size_t)k * N, (int64_t)2 * k * N, corr + (size_t)k * N, (int64_t)2 * k * N,
+          B, k, chain.data());
+  S.seg[0].other = acc;
+  S.seg[0].other_stride = (int64_t)2 * n_ext * N;
+  S.seg[0].eout = out_b;
+  S.seg[0].eout_stride = os;
+  S.seg[1].other = acc + (size_t)n_ext * N;
+  S.seg[1].other_stride = (int64_t)2 * n_ext * N;
+  S.seg[1].eout = out_a;
+  S.seg[1].eout_stride = os;
+  NttEpilogue E;
+  E.enabled = true;
+  for (int t = 0; t < k; ++t) {
+    E.c[t] = L.pinv[t];
+    E.csh[t] = L.pinv_sh[t];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+}
+
+// --- rescale (ops.py:164-189) and ModRaise (bootstrap.py:260-275) ----------
+
+static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uint64_t* out,
+                         int64_t os, int P, cudaStream_t st) {
+  if (level < 1 || level >= R.n_chain) throw HegpuError{HEGPU_E_ARG, "rescale level out of range"};
+  if (P <= 0) return;
+  const size_t N = R.n;
+  const auto& cs = R.rescale_consts(level);
+  Scratch ws((size_t)P * (1 + level) * N * 8, st);
+  uint64_t* top = ws.u64();
+  uint64_t* rest = top + (size_t)P * N;
+  const int32_t lp = level;
+  ntt_simple(R, true, in + (size_t)level * N, is, top, (int64_t)N, P, 1, &lp, st);
+  const std::vector<int32_t> chain = range_primes(0, level);
+  launch_lift_centered(R.dpc, R.log_n, top, (int64_t)N, R.primes[level], rest,
+                       (int64_t)level * N, P, level, chain.data(), st);
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  add_seg(S, rest, (int64_t)level * N, rest, (int64_t)level * N, P, level, chain.data());
+  S.seg[0].other = in;
+  S.seg[0].other_stride = is;
+  S.seg[0].eout = out;
+  S.seg[0].eout_stride = os;
+  NttEpilogue E;
+  E.enabled = true;
+  for (int i = 0; i < level; ++i) {
+    E.c[i] = cs.first[i];
+    E.csh[i] = cs.second[i];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+}
+
+static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* out, int64_t os,
+                           int P, int to_level, cudaStream_t st) {
+  if (to_level < 0 || to_level >= R.n_chain) throw HegpuError{HEGPU_E_ARG, "bad target level"};
+  if (P <= 0) return;
+  const size_t N = R.n;
+  Scratch ws((size_t)P * N * 8, st);
+  const int32_t p0 = 0;
+  ntt_simple(R, true, in, is, ws.u64(), (int64_t)N, P, 1, &p0, st);
+  const std::vector<int32_t> chain = range_primes(0, to_level + 1);
+  launch_lift_centered(R.dpc, R.log_n, ws.u64(), (int64_t)N, R.primes[0], out, os, P,
+                       to_level + 1, chain.data(), st);
+  ntt_simple(R, false, out, os, out, os, P, to_level + 1, chain.data(), st);
+}
+
+// --- host-array kernel-table shims (hebert._kernels) -----------------------
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) check_cuda(cudaMalloc(&p, bytes), "device alloc");
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  uint64_t* u64() const { return static_cast<uint64_t*>(p); }
+};
+
+static void h2d(void* d, const void* h, size_t bytes) {
+  check_cuda(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice), "H2D copy");
+}
+static void d2h(void* h, const void* d, size_t bytes) {
+  check_cuda(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost), "D2H copy");
+}
+
+static int ilog2_exact(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  if ((1 << l) != n) throw HegpuError{HEGPU_E_ARG, "n must be a power of two"};
+  return l;
+}
+
+// Per-call constant table for arbitrary primes given as (q, qinv_neg).
+static std::vector<PrimeConst> shim_consts(const uint64_t* q, int k, int log_n) {
+  if (k > kMaxPrimes) throw HegpuError{HEGPU_E_ARG, "too many rows"};
+  std::vector<PrimeConst> pc(k);
+  for (int i = 0; i < k; ++i) {
+    if (q[i] < 3 || q[i] >= (1ull << 62) || (q[i] & 1) == 0)
+      throw HegpuError{HEGPU_E_ARG, "moduli must be odd and < 2^62"};
+    pc[i] = make_prime_const(q[i], log_n, 1);
+  }
+  return pc;
+}
+
+static void shim_elementwise(int op, const uint64_t* a, const uint64_t* b, uint64_t* out, int k,
+                             int n, const uint64_t* q, const uint64_t* consts) {
+  if (k == 0 || n == 0) return;
+  const int log_n = ilog2_exact(n);
+  if (n < 2) throw HegpuError{HEGPU_E_ARG, "n too small"};
+  auto pc = shim_consts(q, k, log_n);
+  const size_t bytes = (size_t)k * n * 8;
+  DevBuf dpc(pc.size() * sizeof(PrimeConst)), da(bytes), db(b ? bytes : 0), dout(bytes);
+  h2d(dpc.p, pc.data(), pc.size() * sizeof(PrimeConst));
+  h2d(da.p, a, bytes);
+  if (b) h2d(db.p, b, bytes);
+  if (op == HEGPU_OP_FMA) h2d(dout.p, out, bytes);
+  std::vector<uint64_t> hq(q, q + k);
+  std::vector<int32_t> sel = range_primes(0, k);
+  EwArgs A{op, da.u64(), 0, b ? db.u64() : nullptr, 0, dout.u64(), 0, 1, k, sel.data(), consts};
+  launch_elementwise(static_cast<PrimeConst*>(dpc.p), hq, log_n, A, 0);
+  d2h(out, dout.p, bytes);
+}
+
+static void shim_ntt(bool inverse, uint64_t* a, int k, int n, const uint64_t* tw_mont,
+                     const uint64_t* ninv_mont, const uint64_t* q) {
+  if (k == 0) return;
+  const int log_n = ilog2_exact(n);
+  if (log_n < 2) throw HegpuError{HEGPU_E_ARG, "n too small for the NTT"};
+  std::vector<PrimeConst> pc(k);
+  std::vector<uint64_t> tw((size_t)k * 4 * n, 0);
+  for (int i = 0; i < k; ++i) {
+    const uint64_t qi = q[i];
+    if (qi < 3 || qi >= (1ull << 62) || (qi & 1) == 0)
+      throw HegpuError{HEGPU_E_ARG, "moduli must be odd and < 2^62"};
+    const uint64_t rinv = h_inv(h_rmod(qi), qi);  // Montgomery -> natural
+    uint64_t* t = tw.data() + (size_t)i * 4 * n + (inverse ? 2 * (size_t)n : 0);
+    for (int j = 0; j < n; ++j) {
+      const uint64_t w = h_mulmod(tw_mont[(size_t)i * n + j] % qi, rinv, qi);
+      t[j] = w;
+      t[n + j] = h_shoup(w, qi);
+    }
+    pc[i] = make_prime_const(qi, log_n, inverse ? t[1] : 1);
+    if (inverse) {
+      pc[i].ninv = h_mulmod(ninv_mont[i] % qi, rinv, qi);
+      pc[i].ninv_sh = h_shoup(pc[i].ninv, qi);
+      pc[i].ilast = h_mulmod(t[1], pc[i].ninv, qi);
+      pc[i].ilast_sh = h_shoup(pc[i].ilast, qi);
+    }
+  }
+  const size_t bytes = (size_t)k * n * 8;
+  DevBuf dpc(pc.size() * sizeof(PrimeConst)), dtw(tw.size() * 8), da(bytes);
+  h2d(dpc.p, pc.data(), pc.size() * sizeof(PrimeConst));
+  h2d(dtw.p, tw.data(), tw.size() * 8);
+  h2d(da.p, a, bytes);
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  std::vector<int32_t> sel = range_primes(0, k);
+  add_seg(S, da.u64(), 0, da.u64(), 0, 1, k, sel.data());
+  launch_ntt(static_cast<PrimeConst*>(dpc.p), dtw.u64(), log_n, inverse, S, nullptr, 0);
+  d2h(a, da.p, bytes);
+}
+
+}  // namespace hegpu
+
+// ============================================================================
+// C ABI
+// ============================================================================
+using namespace hegpu;
+
+struct hegpu_ring {
+  Ring* r;
+};
+
+#define HEGPU_TRY(...)                          \
+  try {                                         \
+    __VA_ARGS__;                                \
+    return HEGPU_OK;                            \
+  } catch (const HegpuError& e) {               \
+    set_error(e.msg);                           \
+    return e.code;                              \
+  } catch (const std::bad_alloc&) {             \
+    set_error("host out of memory");            \
+    return HEGPU_E_NOMEM;                       \
+  } catch (const std::exception& e) {           \
+    set_error(e.what());                        \
+    return HEGPU_E_ARG;                         \
+  }
+
+static Ring& RR(hegpu_ring_t r) {
+  if (!r || !r->r) throw HegpuError{HEGPU_E_ARG, "null ring handle"};
+  return *r->r;
+}
+static inline cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* hegpu_version(void) { return "hegpu 0.1 (sm_100a)"; }
+const char* hegpu_last_error(void) { return g_last_error.c_str(); }
+int hegpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+long long hegpu_launch_count(void) { return g_launches.load(); }
+
+int hegpu_bench_modmul_peak(int iters, double* modmul_per_s) {
+  HEGPU_TRY(*modmul_per_s = bench_modmul_peak(iters))
+}
+
+int hegpu_profile_enable(int on) {
+  HEGPU_TRY({
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    g_prof_on.store(on != 0);
+  })
+}
+
+int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* modmuls,
+                       int n_classes) {
+  HEGPU_TRY({
+    check_cuda(cudaDeviceSynchronize(), "profile sync");
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (int c = 0; c < n_classes; ++c) {
+      ms[c] = 0;
+      counts[c] = 0;
+      bytes[c] = 0;
+      modmuls[c] = 0;
+    }
+    for (auto& r : g_prof) {
+      float t = 0;
+      check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "event time");
+      if (r.cls < n_classes) {
+        ms[r.cls] += t;
+        counts[r.cls] += 1;
+        bytes[r.cls] += r.bytes;
+        modmuls[r.cls] += r.modmuls;
+      }
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+  })
+}
+
+int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
+                      int n_special, hegpu_ring_t* out) {
+  HEGPU_TRY({
+    if (!out) throw HegpuError{HEGPU_E_ARG, "null output"};
+    Ring* r = create_ring(log_n, chain, n_chain, special, n_special);
+    *out = new hegpu_ring{r};
+  })
+}
+
+int hegpu_ring_destroy(hegpu_ring_t ring) {
+  HEGPU_TRY({
+    if (ring) {
+      delete ring->r;
+      delete ring;
+    }
+  })
+}
+
+int hegpu_ring_get_tables(hegpu_ring_t ring, int p, uint64_t* host_out4n) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (p < 0 || p >= R.n_primes) throw HegpuError{HEGPU_E_ARG, "prime index out of range"};
+    d2h(host_out4n, R.dtw + (size_t)p * 4 * R.n, (size_t)4 * R.n * 8);
+  })
+}
+
+int hegpu_ntt(hegpu_ring_t ring, int inverse, const uint64_t* in, int64_t in_stride,
+              uint64_t* out, int64_t out_stride, int n_polys, int k, const int32_t* primes,
+              void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    for (int l = 0; l < k; ++l)
+      if (primes[l] >= R.n_primes) throw HegpuError{HEGPU_E_ARG, "prime index out of range"};
+    ntt_simple(R, inverse != 0, in, in_stride, out, out_stride, n_polys, k, primes, S_(stream));
+  })
+}
+
+int hegpu_elementwise(hegpu_ring_t ring, int op, const uint64_t* a, int64_t a_stride,
+                      const uint64_t* b, int64_t b_stride, uint64_t* out, int64_t out_stride,
+                      int n_polys, int k, const int32_t* primes, const uint64_t* consts,
+                      void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    EwArgs A{op, a, a_stride, b, b_stride, out, out_stride, n_polys, k, primes, consts};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, S_(stream));
+  })
+}
+
+int hegpu_lift_signed(hegpu_ring_t ring, const int64_t* src, int64_t src_stride, uint64_t* out,
+                      int64_t out_stride, int n_polys, int k, const int32_t* primes,
+                      void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    launch_lift_signed(R.dpc, R.log_n, src, src_stride, out, out_stride, n_polys, k, primes,
+                       S_(stream));
+  })
+}
+
+int hegpu_lift_centered(hegpu_ring_t ring, const uint64_t* src, int64_t src_stride,
+                        int src_prime, uint64_t* out, int64_t out_stride, int n_polys, int k,
+                        const int32_t* primes, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (src_prime < 0 || src_prime >= R.n_primes) throw HegpuError{HEGPU_E_ARG, "bad src prime"};
+    launch_lift_centered(R.dpc, R.log_n, src, src_stride, R.primes[src_prime], out, out_stride,
+                         n_polys, k, primes, S_(stream));
+  })
+}
+
+int hegpu_automorphism(hegpu_ring_t ring, int eval_form, uint64_t g, const uint64_t* in,
+                       int64_t in_stride, uint64_t* out, int64_t out_stride, int n_polys, int k,
+                       const int32_t* primes, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (in == out) throw HegpuError{HEGPU_E_ARG, "automorphism cannot run in place"};
+    launch_automorphism(R.dpc, R.log_n, eval_form != 0, g, in, in_stride, out, out_stride,
+                        n_polys, k, primes, S_(stream));
+  })
+}
+
+int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int64_t a_stride,
+                 const uint64_t* b0, const uint64_t* b1, int64_t b_stride, uint64_t* d0,
+                 uint64_t* d1, uint64_t* d2, int64_t d_stride, int n_polys, int k,
+                 void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    TensorParams T;
+    T.a0 = a0;
+    T.a1 = a1;
+    T.b0 = b0;
+    T.b1 = b1;
+    T.d0 = d0;
+    T.d1 = d1;
+    T.d2 = d2;
+    T.as = a_stride;
+    T.bs = b_stride;
+    T.ds = d_stride;
+    T.k = k;
+    launch_tensor(R.dpc, R.log_n, T, n_polys, S_(stream));
+  })
+}
+
+int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d, int64_t d_stride,
+                   int n_batch, const uint64_t* const* key_b, const uint64_t* const* key_a,
+                   int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t out_stride,
+                   void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    ks_apply_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, out_b, out_a,
+                  out_stride, S_(stream));
+  })
+}
+
+int hegpu_rescale(hegpu_ring_t ring, int level, const uint64_t* in, int64_t in_stride,
+                  uint64_t* out, int64_t out_stride, int n_polys, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    rescale_impl(R, level, in, in_stride, out, out_stride, n_polys, S_(stream));
+  })
+}
+
+int hegpu_mod_raise(hegpu_ring_t ring, const uint64_t* in, int64_t in_stride, uint64_t* out,
+                    int64_t out_stride, int n_polys, int to_level, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    mod_raise_impl(R, in, in_stride, out, out_stride, n_polys, to_level, S_(stream));
+  })
+}
+
+int hegpu_encrypt_combine(hegpu_ring_t ring, const uint64_t* v, const uint64_t* e0,
+                          const uint64_t* e1, const uint64_t* m, const uint64_t* pk_b,
+                          const uint64_t* pk_a, uint64_t* c0, uint64_t* c1, int k,
+                          void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    EncParams E;
+    E.v = v;
+    E.e0 = e0;
+    E.e1 = e1;
+    E.m = m;
+    E.pb = pk_b;
+    E.pa = pk_a;
+    E.c0 = c0;
+    E.c1 = c1;
+    launch_encrypt(R.dpc, R.log_n, E, k, S_(stream));
+  })
+}
+
+int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct_c1_off,
+                   const uint64_t* const* pt_ptrs, int n_terms, uint64_t* out,
+                   int64_t out_c1_off, int k, int accumulate, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    launch_diag_mac(R.dpc, R.log_n, ct_ptrs, ct_c1_off, pt_ptrs, n_terms, out, out_c1_off, k,
+                    accumulate, S_(stream));
+  })
+}
+
+// --- host-array kernel table -----------------------------------------------
+
+int hegpu_k_ntt_forward_inplace(uint64_t* a, int k, int n, const uint64_t* psi_rev,
+                                const uint64_t* q, const uint64_t* qinv) {
+  (void)qinv;
+  HEGPU_TRY(shim_ntt(false, a, k, n, psi_rev, nullptr, q))
+}
+
+int hegpu_k_ntt_inverse_inplace(uint64_t* a, int k, int n, const uint64_t* ipsi_rev,
+                                const uint64_t* ninv, const uint64_t* q, const uint64_t* qinv) {
+  (void)qinv;
+  HEGPU_TRY(shim_ntt(true, a, k, n, ipsi_rev, ninv, q))
+}
+
+int hegpu_k_elementwise_mont(const uint64_t* a, const uint64_t* b, uint64_t* out, int k, int n,
+                             const uint64_t* q, const uint64_t* qinv) {
+  (void)qinv;
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_MONT, a, b, out, k, n, q, nullptr))
+}
+
+int hegpu_k_elementwise_mulmod(const uint64_t* a, const uint64_t* b, uint64_t* out, int k,
+                               int n, const uint64_t* q, const uint64_t* qinv,
+                               const uint64_t* r2) {
+  (void)qinv;
+  (void)r2;
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_MUL, a, b, out, k, n, q, nullptr))
+}
+
+int hegpu_k_rowwise_mont(const uint64_t* a, const uint64_t* c, uint64_t* out, int k, int n,
+                         const uint64_t* q, const uint64_t* qinv) {
+  (void)qinv;
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_ROWMONT, a, nullptr, out, k, n, q, c))
+}
+
+int hegpu_k_addmod_rows(const uint64_t* a, const uint64_t* b, uint64_t* out, int k, int n,
+                        const uint64_t* q) {
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_ADD, a, b, out, k, n, q, nullptr))
+}
+
+int hegpu_k_submod_rows(const uint64_t* a, const uint64_t* b, uint64_t* out, int k, int n,
+                        const uint64_t* q) {
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_SUB, a, b, out, k, n, q, nullptr))
+}
+
+int hegpu_k_fma_inplace(uint64_t* acc, const uint64_t* a, const uint64_t* b, int k, int n,
+                        const uint64_t* q, const uint64_t* qinv, const uint64_t* r2) {
+  (void)qinv;
+  (void)r2;
+  HEGPU_TRY(shim_elementwise(HEGPU_OP_FMA, a, b, acc, k, n, q, nullptr))
+}
+
+int hegpu_k_fma_gather_inplace(uint64_t* acc, const uint64_t* a, const uint64_t* key,
+                               int key_rows, const int64_t* rows, int k, int n,
+                               const uint64_t* q, const uint64_t* qinv, const uint64_t* r2) {
+  (void)qinv;
+  (void)r2;
+  HEGPU_TRY({
+    std::vector<uint64_t> gathered((size_t)k * n);
+    for (int i = 0; i < k; ++i) {
+      if (rows[i] < 0 || rows[i] >= key_rows) throw HegpuError{HEGPU_E_ARG, "key row out of range"};
+      std::memcpy(gathered.data() + (size_t)i * n, key + (size_t)rows[i] * n, (size_t)n * 8);
+    }
+    shim_elementwise(HEGPU_OP_FMA, a, gathered.data(), acc, k, n, q, nullptr);
+  })
+}
+
+int hegpu_k_base_convert(const uint64_t* hat, int l, int n, const uint64_t* punc, int kt,
+                         const uint64_t* q_to, const uint64_t* qinv_to, uint64_t* out) {
+  (void)qinv_to;
+  HEGPU_TRY({
+    if (kt == 0 || n == 0) return HEGPU_OK;
+    const int log_n = ilog2_exact(n);
+    if (l > 32) throw HegpuError{HEGPU_E_ARG, "too many source rows"};
+    auto pc = shim_consts(q_to, kt, log_n);
+    DevBuf dpc(pc.size() * sizeof(PrimeConst)), dh((size_t)std::max(l, 1) * n * 8),
+        dp((size_t)std::max(l * kt, 1) * 8), dout((size_t)kt * n * 8);
+    h2d(dpc.p, pc.data(), pc.size() * sizeof(PrimeConst));
+    if (l) h2d(dh.p, hat, (size_t)l * n * 8);
+    if (l) h2d(dp.p, punc, (size_t)l * kt * 8);
+    ConvParams C;
+    C.n_jobs = 1;
+    C.n_polys = 1;
+    C.log_n = log_n;
+    C.pc = static_cast<PrimeConst*>(dpc.p);
+    ConvJob& J = C.job[0];
+    J.src = dh.u64();
+    J.src_stride = 0;
+    J.dst = dout.u64();
+    J.dst_stride = 0;
+    J.n_src = l;
+    J.n_dst = kt;
+    J.inv = nullptr;
+    J.inv_sh = nullptr;
+    J.punc = dp.u64();
+    J.punc_ld = kt;
+    for (int i = 0; i < l; ++i) C.src_sel[0][i] = 0;  // hat rows are used as given
+    for (int t = 0; t < kt; ++t) C.dst_sel[0][t] = (uint8_t)t;
+    launch_conv(C, 0);
+    d2h(out, dout.p, (size_t)kt * n * 8);
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Host-side ring context and internal launch API of libhegpu.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "hegpu.h"
+
+namespace hegpu {
+
+// Device constants for hybrid key switching at one (level, alpha), derived
+// from BaseConverter (keys.py:19-49) and _p_inv_consts (keys.py:264-275).
+struct KsLevel {
+  int level = 0, alpha = 0, beta = 0, n_ext = 0, K = 0;
+  uint64_t* dmem = nullptr;
+  // ModUp: for chain limb i <= level (digit j = i / alpha)
+  const uint64_t* mu_inv = nullptr;     // (Q_j/q_i)^-1 mod q_i, natural   [level+1]
+  const uint64_t* mu_inv_sh = nullptr;  // Shoup companions                 [level+1]
+  const uint64_t* mu_punc = nullptr;    // (Q_j/q_i mod p_t) R mod p_t      [level+1][n_ext]
+  // ModDown: specials -> chain 0..level
+  const uint64_t* md_inv = nullptr;     // [K]
+  const uint64_t* md_inv_sh = nullptr;  // [K]
+  const uint64_t* md_punc = nullptr;    // [K][level+1]
+  std::vector<uint64_t> pinv, pinv_sh;  // P^-1 mod q_t, t <= level (host, kernel params)
+  std::vector<int> dst_prime_of_digit;  // flattened [beta][n_ext] compact dst -> global prime
+};
+
+struct Ring {
+  int log_n = 0, n = 0, n_chain = 0, n_special = 0, n_primes = 0;
+  int device = 0;
+  std::vector<uint64_t> primes;  // chain then special
+  std::vector<PrimeConst> hpc;
+  PrimeConst* dpc = nullptr;
+  uint64_t* dtw = nullptr;  // [n_primes][4][N]: psi, psi_sh, ipsi, ipsi_sh
+  std::mutex mu;
+  std::map<std::pair<int, int>, std::unique_ptr<KsLevel>> ks;
+  // rescale constants: level -> (q_level^-1 mod q_i, shoup) for i < level
+  std::map<int, std::pair<std::vector<uint64_t>, std::vector<uint64_t>>> rescale;
+
+  ~Ring();
+  const KsLevel& ks_level(int level, int alpha);
+  const std::pair<std::vector<uint64_t>, std::vector<uint64_t>>& rescale_consts(int level);
+  int special_prime(int i) const { return n_chain + i; }
+};
+
+// --- host 128-bit helpers -------------------------------------------------
+inline uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t q) {
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % q);
+}
+inline uint64_t h_powmod(uint64_t b, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  b %= q;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, b, q);
+    b = h_mulmod(b, b, q);
+    e >>= 1;
+  }
+  return r;
+}
+inline uint64_t h_inv(uint64_t a, uint64_t q) { return h_powmod(a, q - 2, q); }  // q prime
+inline uint64_t h_shoup(uint64_t w, uint64_t q) {
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(w) << 64) / q);
+}
+inline uint64_t h_rmod(uint64_t q) {  // 2^64 mod q
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) % q);
+}
+PrimeConst make_prime_const(uint64_t q, int log_n, uint64_t ipsi1);
+
+// --- error state ------------------------------------------------------------
+void set_error(const std::string& msg);
+struct HegpuError {
+  int code;
+  std::string msg;
+};
+void check_cuda(cudaError_t e, const char* what);  // throws HegpuError
+
+// --- launch accounting / profiling ------------------------------------------
+// Every kernel launch bumps a global counter; when profiling is enabled the
+// launch is bracketed by CUDA events on its stream and the device time is
+// accumulated per kernel class (read back by hegpu_profile_read).
+enum ProfClass {
+  PROF_NTT = 0,
+  PROF_ELEMENTWISE,
+  PROF_LIFT,
+  PROF_AUTOMORPHISM,
+  PROF_TENSOR,
+  PROF_CONV,
+  PROF_KS_IP,
+  PROF_DIAG_MAC,
+  PROF_ENCRYPT,
+  PROF_NUM_CLASSES
+};
+// bytes / modmuls: ALGORITHMIC traffic and modular multiplications of the
+// launch (each input read once, each output written once).
+struct ProfScope {
+  int slot = -1;
+  cudaStream_t st;
+  ProfScope(int cls, cudaStream_t s, double bytes = 0, double modmuls = 0);
+  ~ProfScope();
+};
+
+// --- launchers (stream-ordered; throw HegpuError on failure) ----------------
+struct NttEpilogue {
+  bool enabled = false;
+  uint64_t c[kMaxPrimes];
+  uint64_t csh[kMaxPrimes];
+};
+
+// NTT over a set of segments.  For the forward transform with an epilogue,
+// seg.eout receives (seg.other - NTT(x)) * c[limb] and seg.out is scratch.
+void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inverse,
+                SegSet& S, const NttEpilogue* epi, cudaStream_t st);
+
+struct EwArgs {
+  int op;
+  const uint64_t* a;
+  int64_t as;
+  const uint64_t* b;
+  int64_t bs;
+  uint64_t* o;
+  int64_t os;
+  int n_polys, k;
+  const int32_t* primes;
+  const uint64_t* consts;  // host, k entries
+};
+void launch_elementwise(const PrimeConst* dpc, const std::vector<uint64_t>& hq, int log_n,
+                        const EwArgs& A, cudaStream_t st);
+
+void launch_lift_signed(const PrimeConst* dpc, int log_n, const int64_t* src, int64_t ss,
+                        uint64_t* out, int64_t os, int n_polys, int k, const int32_t* primes,
+                        cudaStream_t st);
+void launch_lift_centered(const PrimeConst* dpc, int log_n, const uint64_t* src, int64_t ss,
+                          uint64_t src_q, uint64_t* out, int64_t os, int n_polys, int k,
+                          const int32_t* primes, cudaStream_t st);
+
+struct ConvJob {
+  const uint64_t* src;
+  int64_t src_stride;
+  uint64_t* dst;
+  int64_t dst_stride;
+  int n_src, n_dst;
+  const uint64_t* inv;     // [n_src] natural
+  const uint64_t* inv_sh;  // [n_src]
+  const uint64_t* punc;    // [n_src] rows, row stride punc_ld, Montgomery form
+  int punc_ld;
+};
+struct ConvParams {
+  int n_jobs;
+  int n_polys;
+  int log_n;
+  const PrimeConst* pc;
+  ConvJob job[kMaxSeg];
+  uint8_t src_sel[kMaxSeg][kMaxPrimes];
+  uint8_t dst_sel[kMaxSeg][kMaxPrimes];
+};
+void launch_conv(ConvParams& P, cudaStream_t st);
+
+struct TensorParams {
+  const uint64_t *a0, *a1, *b0, *b1;
+  uint64_t *d0, *d1, *d2;
+  int64_t as, bs, ds;
+  int k, log_n;
+  const PrimeConst* pc;
+};
+
+struct EncParams {
+  const uint64_t *v, *e0, *e1, *m, *pb, *pa;
+  uint64_t *c0, *c1;
+  int log_n;
+  const PrimeConst* pc;
+};
+
+constexpr int kMaxDigits = 16;
+struct IpParams {
+  const uint64_t* d;  // eval-form input, (level+1) limbs per poly
+  int64_t ds;
+  const uint64_t* ext;  // [b][j][row][N] converted rows (compact per digit)
+  int64_t ext_sb, ext_sj;
+  const uint64_t* kb[kMaxDigits];
+  const uint64_t* ka[kMaxDigits];
+  uint64_t* acc;  // [b][2][n_ext][N]
+  int64_t acc_sb;
+  int level, alpha, beta, n_ext, n_chain, key_sp_row0, n_batch, log_n;
+  const PrimeConst* pc;
+};
+
+void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint64_t g,
+                         const uint64_t* in, int64_t is, uint64_t* out, int64_t os, int n_polys,
+                         int k, const int32_t* primes, cudaStream_t st);
+void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int n_polys,
+                   cudaStream_t st);
+void launch_encrypt(const PrimeConst* dpc, int log_n, const EncParams& E0, int k,
+                    cudaStream_t st);
+void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct,
+                     int64_t ct_c1_off, const uint64_t* const* pt, int n_terms, uint64_t* out,
+                     int64_t out_c1_off, int k, int accumulate, cudaStream_t st);
+void launch_ks_ip(IpParams& P, cudaStream_t st);
+double bench_modmul_peak(int iters);
+
+}  // namespace hegpu

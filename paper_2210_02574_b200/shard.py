@@ -1,0 +1,111 @@
+"""Minibatch sharding across GPUs for encrypted training.
+
+One process per GPU.  Each minibatch's ciphertexts are split contiguously
+across ranks; every rank computes and locally sums its gradients, then the
+level-1 gradient ciphertext is combined with one modular all-reduce: an NCCL
+(or gloo) int64 SUM of residues followed by one `mod q` pass.  It is exact
+when world_size * (q-1) < 2^64 for every prime q of the chain (checked;
+true for 8 ranks and primes < 2^61): integer addition wraps modulo 2^64, so
+the reduced value equals the reference's fixed-order modular sum
+(logreg.py:382-384) bit for bit.
+The two refreshes per minibatch (w and u) run on different ranks and are
+broadcast back, so they overlap when world_size > 1.
+"""
+
+import numpy as np
+
+from . import _dev
+from . import _lib
+
+
+def world():
+    """(rank, world_size) of the default process group, (0, 1) if none."""
+    try:
+        import torch.distributed as dist
+    except Exception:
+        return 0, 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard_range(n_items, rank, world_size):
+    """Contiguous [lo, hi) share of n_items for `rank` (balanced, order-preserving)."""
+    base, extra = divmod(n_items, world_size)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def refresh_owner(role, world_size):
+    """Rank that refreshes the weight (role 0) or momentum (role 1) ciphertext."""
+    return 0 if world_size == 1 else role % world_size
+
+
+def check_allreduce_exact(primes, world_size):
+    """The wrapping int64 sum is exact iff world_size*(q-1) < 2^64 for all q."""
+    return all(world_size * (int(q) - 1) < (1 << 64) for q in primes)
+
+
+def modular_sum_host(residue_arrays, primes):
+    """Host statement of the all-reduce contract (used by the CPU tests):
+    wrapping uint64 sum over ranks, then mod q per limb."""
+    acc = np.zeros_like(residue_arrays[0], dtype=np.uint64)
+    for a in residue_arrays:
+        acc = acc + np.asarray(a, dtype=np.uint64)  # wraps mod 2^64
+    q = np.asarray(primes, dtype=np.uint64).reshape((-1,) + (1,) * (acc.ndim - 1))
+    return acc % q
+
+
+def allreduce_ciphertext(ct):
+    """In-place modular all-reduce of an (unbatched) ciphertext over all ranks."""
+    import torch.distributed as dist
+
+    rank, ws = world()
+    if ws == 1:
+        return ct
+    params = ct.params
+    k = ct.level + 1
+    if not check_allreduce_exact(params.ring.moduli_chain[:k], ws):
+        raise ValueError("world size too large for an exact wrapping all-reduce")
+    from .ckks import ops
+
+    grp = ops._pair_group(ct)
+    if grp is None:
+        ct = ct.copy()
+        grp = ops._pair_group(ct)
+    base = ct.c0.data
+    n = params.ring_degree
+    flat = base.as_strided((2, k, n), (k * n, n, 1))
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+    p, cnt, s = grp
+    _lib.call(
+        "hegpu_elementwise", params.ring.device(), _lib.OP_REDUCE, p, s, None, 0, p, s, cnt, k,
+        _dev.chain_primes(k).ctypes.data, None, _dev.stream(),
+    )
+    return ct
+
+
+def broadcast_ciphertext(ct, src, template):
+    """Broadcast a ciphertext from rank `src`; other ranks pass a same-shaped template."""
+    import torch.distributed as dist
+
+    rank, ws = world()
+    if ws == 1:
+        return ct
+    from .ckks import ops
+
+    holder = ct if rank == src else template.copy()
+    grp = ops._pair_group(holder)
+    if grp is None:
+        holder = holder.copy()
+    k = holder.level + 1
+    n = holder.params.ring_degree
+    flat = holder.c0.data.as_strided((2, k, n), (k * n, n, 1))
+    dist.broadcast(flat, src=src)
+    meta = [holder.scale, int(holder.insecure_provenance)]
+    obj = [meta]
+    dist.broadcast_object_list(obj, src=src)
+    holder.scale = float(obj[0][0])
+    holder.insecure_provenance = bool(obj[0][1])
+    return holder

@@ -1,0 +1,237 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Outputs (committed): tests/golden/*.npz and tests/golden/digests.json.  Small
+cases store full arrays; large ones store SHA-256 digests of the little-endian
+limb bytes plus the seeds that recreate their inputs.  Nothing in the GPU tests
+or the bench reads /root/reference; they read these files.
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+
+from hebert import _kernels, bootstrap as bs, ckks, logreg, minimax, ring  # noqa: E402
+from hebert.ckks import keys as K, ops  # noqa: E402
+
+
+def sha(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr, dtype="<u8").tobytes()).hexdigest()
+
+
+def ct_digest(ct):
+    return {"c0": sha(ct.c0.limbs), "c1": sha(ct.c1.limbs), "level": ct.level,
+            "scale": float(ct.scale).hex()}
+
+
+def load_preset(name):
+    path = os.path.join(REPO, "paper_2210_02574_b200", "presets", f"{name}.preset")
+    with open(path) as fh:
+        return ckks.CkksParams.from_config_text(fh.read())
+
+
+def kernels_fixture():
+    rng = np.random.default_rng(11)
+    n = 64
+    primes = ring.generate_ntt_primes(61, 2, n)
+    q = np.array(primes, dtype=np.uint64)
+    qinv = np.array([(-pow(int(p), -1, 1 << 64)) % (1 << 64) for p in primes], dtype=np.uint64)
+    r2 = np.array([(1 << 128) % int(p) for p in primes], dtype=np.uint64)
+    a = np.stack([rng.integers(0, p, n, dtype=np.uint64) for p in primes])
+    b = np.stack([rng.integers(0, p, n, dtype=np.uint64) for p in primes])
+    a[:, 0] = 0
+    b[:, 1] = 0
+    a[:, 2] = q - 1
+    b[:, 2] = q - 1
+    c = np.array([rng.integers(0, p) for p in primes], dtype=np.uint64)
+    p3 = ring.RingParams("k64", n, tuple(primes))
+    st = p3.stacked(tuple(primes))
+    hat = np.stack([rng.integers(0, p, n, dtype=np.uint64) for p in primes])
+    # convert hat (rows under prime 0/1) into the 2 target primes
+    punc = np.array([[rng.integers(0, p) for p in primes] for _ in range(2)], dtype=np.uint64)
+    key = np.stack([rng.integers(0, primes[i % 2], n, dtype=np.uint64) for i in range(5)])
+    rows = np.array([3, 0], dtype=np.int64)
+    key[3] %= q[0]
+    key[0] %= q[1]
+    out = dict(q=q, qinv=qinv, r2=r2, a=a, b=b, c=c, hat=hat, punc=punc, key=key, rows=rows,
+               psi_rev=st.psi_rev, ipsi_rev=st.ipsi_rev, ninv=st.ninv1)
+    out["mulmod"] = _kernels.elementwise_mulmod(a, b, q, qinv, r2)
+    out["mont"] = _kernels.elementwise_mont(a, b, q, qinv)
+    out["rowwise"] = _kernels.rowwise_mont(a, c, q, qinv)
+    out["add"] = _kernels.addmod_rows(a, b, q)
+    out["sub"] = _kernels.submod_rows(a, b, q)
+    out["bconv"] = _kernels.base_convert(hat, punc, q, qinv)
+    acc = a.copy()
+    out["fma"] = _kernels.fma_inplace(acc, b, a, q, qinv, r2).copy()
+    acc = b.copy()
+    out["fma_gather"] = _kernels.fma_gather_inplace(acc, a, key, rows, q, qinv, r2).copy()
+    f = a.copy()
+    out["ntt_fwd"] = _kernels.ntt_forward_inplace(f, st.psi_rev, q, qinv).copy()
+    g = a.copy()
+    out["ntt_inv"] = _kernels.ntt_inverse_inplace(g, st.ipsi_rev, st.ninv1, q, qinv).copy()
+    np.savez_compressed(os.path.join(HERE, "kernels_n64.npz"), **out)
+
+
+def ring_fixture():
+    n = 64
+    primes = tuple(ring.generate_ntt_primes(40, 3, n))
+    p = ring.RingParams("r64", n, primes)
+    rng = np.random.default_rng(2)
+    x = ring.sample_poly(p, "uniform", 2, rng)
+    y = ring.sample_poly(p, "uniform", 2, rng)
+    xe, ye = ring.to_eval(x), ring.to_eval(y)
+    out = dict(primes=np.array(primes, dtype=np.uint64), x=x.limbs, y=y.limbs, x_eval=xe.limbs,
+               y_eval=ye.limbs, prod=ring.poly_mul(xe, ye).limbs,
+               prod_coeff=ring.to_coeff(ring.poly_mul(xe, ye)).limbs)
+    exps, pos = ring._eval_exponent_map(p)
+    out["exps"] = exps
+    for g in (3, 5, 127, 2 * n - 1):
+        out[f"auto_eval_{g}"] = ring.poly_automorphism_eval(xe, g).limbs
+        out[f"auto_coeff_{g}"] = ring.poly_automorphism(x, g).limbs
+    signed = np.random.default_rng(3).integers(-(1 << 61), 1 << 61, size=n)
+    out["signed"] = signed
+    out["lifted"] = ring.limbs_from_signed(signed, primes)
+    np.savez_compressed(os.path.join(HERE, "ring_n64.npz"), **out)
+
+
+def scheme_digests(params, name, steps, seed=7, conj=True, full=True):
+    t0 = time.time()
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=seed, include_conjugation=conj)
+    d = {"keygen_seconds": time.time() - t0, "rotation_steps": list(keys.rotation_steps)}
+    d["secret_ext"] = sha(keys.secret_ext)
+    d["pk_b"] = sha(keys.public_key[0].limbs)
+    d["pk_a"] = sha(keys.public_key[1].limbs)
+    d["relin_b"] = [sha(x) for x in keys.relin_key.digits_b]
+    d["relin_a"] = [sha(x) for x in keys.relin_key.digits_a]
+    d["rot"] = {str(s): [sha(x) for x in keys.rotation_keys[s].digits_b]
+                + [sha(x) for x in keys.rotation_keys[s].digits_a] for s in keys.rotation_steps}
+    if conj:
+        d["conj"] = [sha(x) for x in keys.conj_key.digits_b] + [sha(x) for x in keys.conj_key.digits_a]
+    L = params.max_level
+    # NTT of a seeded uniform poly at the top level
+    up = ring.sample_poly(params.ring, "uniform", L, np.random.default_rng(1000))
+    d["ntt_fwd"] = sha(ring.to_eval(up).limbs)
+    d["ntt_inv"] = sha(ring.ntt_transform(ring.RnsPoly(params.ring, up.limbs.copy(), ring.EVAL, L),
+                                          "inverse").limbs)
+    # key switch of a seeded uniform eval-form d at several levels
+    d["ks"] = {}
+    for lvl in sorted({L, max(1, L // 2), 1}):
+        dp = ring.sample_poly(params.ring, "uniform", lvl, np.random.default_rng(2000 + lvl))
+        dp = ring.RnsPoly(params.ring, dp.limbs, ring.EVAL, lvl)
+        kb, ka = K.ks_apply(keys, keys.relin_key, dp)
+        d["ks"][str(lvl)] = [sha(kb.limbs), sha(ka.limbs)]
+    rng = np.random.default_rng(5)
+    slots = params.slot_count
+    u = rng.uniform(-1, 1, slots)
+    v = rng.uniform(-1, 1, slots)
+    cu = ckks.encrypt_vector(params, u, keys, rng_seed=1)
+    cv = ckks.encrypt_vector(params, v, keys, rng_seed=2)
+    d["enc_u"] = ct_digest(cu)
+    d["enc_v"] = ct_digest(cv)
+    c3 = ckks.encrypt(ckks.encode(params, u[:768], 3), keys, rng_seed=3)
+    d["enc_l3"] = ct_digest(c3)
+    prod = ckks.mult(cu, cv, keys)
+    d["mult"] = ct_digest(prod)
+    d["mult_dec"] = ckks.decrypt_vector(prod, keys)[:64].tolist()
+    d["add"] = ct_digest(ckks.add(cu, cv))
+    d["sub"] = ct_digest(ckks.sub(cu, cv))
+    d["rescale"] = ct_digest(ckks.rescale(ops.mult_plain(cu, 0.5, rescale_after=False)))
+    d["mult_plain_vec"] = ct_digest(ckks.mult_plain(cu, v))
+    d["add_plain_const"] = ct_digest(ckks.add_plain(cu, 0.25))
+    d["mod_down"] = ct_digest(ckks.mod_down(cu, max(1, L // 2)))
+    d["add_aligned"] = ct_digest(ckks.add(prod, ckks.mod_down(cv, prod.level - 1)))
+    if full:
+        for s in steps:
+            d[f"rot_{s}"] = ct_digest(ckks.rotate(cu, s, keys))
+        d["rot_3"] = ct_digest(ckks.rotate(cu, 3, keys))
+        if conj:
+            d["conj_ct"] = ct_digest(ckks.conjugate(cu, keys))
+        d["dec_u"] = ckks.decrypt_vector(cu, keys)[:64].tolist()
+    return d, keys
+
+
+def desk_extra(params, keys, d):
+    path = os.path.join(REPO, "paper_2210_02574_b200", "approximants", "sigmoid_deg15.txt")
+    sig = minimax.import_text(open(path).read())
+    pts = np.linspace(-12, 12, params.slot_count)
+    ct = ckks.encrypt_vector(params, pts, keys, rng_seed=9)
+    out = ckks.eval_poly_bsgs(ct, sig, keys)
+    d["sigmoid_bsgs"] = ct_digest(out)
+    d["sigmoid_dec"] = ckks.decrypt_vector(out, keys)[:64].tolist()
+
+
+def boot_fixture():
+    params = ckks.get_preset("desk-boot")
+    ctx = bs.build_context(params, n_slots=64)
+    steps = sorted(set(list(ckks.default_rotation_steps(params)) + ctx.required_rotation_steps()))
+    t0 = time.time()
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=11)
+    tk = time.time() - t0
+    v = np.random.default_rng(1002).uniform(-1, 1, 64)
+    ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=21)
+    raised = bs._mod_raise(ct)
+    t0 = time.time()
+    out = bs.bootstrap(ct, ctx, keys)
+    tb = time.time() - t0
+    dec = ckks.decrypt_vector(out, keys)
+    res = {"steps": steps, "keygen_seconds": tk, "bootstrap_seconds": tb,
+           "enc": ct_digest(ct), "mod_raise": ct_digest(raised), "out_level": out.level,
+           "out_scale": float(out.scale).hex(), "err": float(np.max(np.abs(dec[:64] - v))),
+           "sine_coeffs": [float(c).hex() for c in ctx.evalmod_poly.cheb_coeffs]}
+    np.savez_compressed(os.path.join(HERE, "boot_desk64.npz"), v=v, dec=dec)
+    return res
+
+
+def logreg_fixture():
+    params = ckks.get_preset("desk")
+    keys = ckks.keygen(params, rng_seed=7)
+    path = os.path.join(REPO, "paper_2210_02574_b200", "approximants", "sigmoid_deg15.txt")
+    sig = minimax.import_text(open(path).read())
+    rng = np.random.default_rng(0)
+    X = rng.uniform(-1, 1, (256, 16))
+    w = rng.normal(size=16)
+    y = (X @ w > 0).astype(np.int64)
+    layout = logreg.make_layout(params, 16)
+    pairs = logreg.pack_batch(X, y, layout, params, keys)
+    cfg = logreg.TrainConfig(1.0, 0.9, 128, 2)
+    model, _ = logreg.train(pairs, 256, cfg, params, keys, sig,
+                            bs.DebugRefresher(keys, enabled=True), layout=layout)
+    got = logreg.decrypted_weights(model, keys)
+    shadow = logreg.shadow_train(X, y, cfg, sig, layout=layout)
+    np.savez_compressed(os.path.join(HERE, "logreg_desk.npz"), X=X, y=y, ref_weights=got,
+                        shadow_weights=shadow.weights)
+
+
+def main():
+    t0 = time.time()
+    kernels_fixture()
+    ring_fixture()
+    digests = {}
+    desk = ckks.get_preset("desk")
+    d, keys = scheme_digests(desk, "desk", [1, -1, 2, 4])
+    desk_extra(desk, keys, d)
+    digests["desk"] = d
+    for name in ("p14", "p16"):
+        params = load_preset(name)
+        digests[name], _ = scheme_digests(params, name, [1], conj=False, full=(name == "p14"))
+        print(name, "done", time.time() - t0, file=sys.stderr)
+    digests["boot_desk64"] = boot_fixture()
+    logreg_fixture()
+    with open(os.path.join(HERE, "digests.json"), "w") as fh:
+        json.dump(digests, fh, indent=1, sort_keys=True)
+    print("golden fixtures written in %.1fs" % (time.time() - t0), file=sys.stderr)
+
+
+if __name__ == "__main__":
+    main()

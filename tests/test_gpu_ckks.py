@@ -1,0 +1,239 @@
+"""GPU parity for the CKKS layer: keygen, seeded encryption, key switching,
+products, rotations, rescale -- limbs bit-exact against digests of the
+reference's own outputs -- plus the reference's tolerance tests
+(T/test_ckks.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import preset_text
+
+pytestmark = pytest.mark.gpu
+
+from oracle.scheme import sha  # noqa: E402  (digest helper only)
+from paper_2210_02574_b200 import ckks, minimax, ring  # noqa: E402
+from paper_2210_02574_b200.ckks import keys as K, ops  # noqa: E402
+from paper_2210_02574_b200.errors import (  # noqa: E402
+    CryptoError,
+    MissingRotationKeyError,
+    OutOfLevelsError,
+    ScaleMismatchError,
+)
+
+
+def params_for(name):
+    if name == "desk":
+        return ckks.get_preset("desk")
+    return ckks.CkksParams.from_config_text(preset_text(name))
+
+
+def ct_digest(ct):
+    return {"c0": sha(ct.c0.limbs), "c1": sha(ct.c1.limbs), "level": ct.level,
+            "scale": float(ct.scale).hex()}
+
+
+_KEYS = {}
+
+
+def keyset(name, d):
+    if name not in _KEYS:
+        params = params_for(name)
+        _KEYS[name] = (params, ckks.keygen(params, rotation_steps=d["rotation_steps"], rng_seed=7,
+                                           include_conjugation="conj" in d))
+    return _KEYS[name]
+
+
+@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+def test_keygen_bit_exact(name, digests):
+    d = digests[name]
+    params, keys = keyset(name, d)
+    assert sha(keys.secret_ext) == d["secret_ext"]
+    assert sha(keys.public_key[0].limbs) == d["pk_b"]
+    assert sha(keys.public_key[1].limbs) == d["pk_a"]
+    assert [sha(x) for x in keys.relin_key.digits_b] == d["relin_b"]
+    assert [sha(x) for x in keys.relin_key.digits_a] == d["relin_a"]
+    for s, hs in d["rot"].items():
+        k = keys.rotation_keys[int(s)]
+        assert [sha(x) for x in k.digits_b] + [sha(x) for x in k.digits_a] == hs
+    if "conj" in d:
+        c = keys.conj_key
+        assert [sha(x) for x in c.digits_b] + [sha(x) for x in c.digits_a] == d["conj"]
+
+
+@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+def test_key_switch_bit_exact(name, digests):
+    d = digests[name]
+    params, keys = keyset(name, d)
+    for lvl, want in d["ks"].items():
+        lvl = int(lvl)
+        dp = ring.sample_poly(params.ring, "uniform", lvl, np.random.default_rng(2000 + lvl))
+        dp = ring.RnsPoly(params.ring, dp.limbs, ring.EVAL, lvl)
+        kb, ka = K.ks_apply(keys, keys.relin_key, dp)
+        assert [sha(kb.limbs), sha(ka.limbs)] == want, f"level {lvl}"
+
+
+@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+def test_ciphertext_ops_bit_exact(name, digests):
+    d = digests[name]
+    params, keys = keyset(name, d)
+    L = params.max_level
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, params.slot_count)
+    v = rng.uniform(-1, 1, params.slot_count)
+    cu = ckks.encrypt_vector(params, u, keys, rng_seed=1)
+    cv = ckks.encrypt_vector(params, v, keys, rng_seed=2)
+    assert ct_digest(cu) == d["enc_u"]
+    assert ct_digest(cv) == d["enc_v"]
+    c3 = ckks.encrypt(ckks.encode(params, u[:768], 3), keys, rng_seed=3)
+    assert ct_digest(c3) == d["enc_l3"]
+    prod = ckks.mult(cu, cv, keys)
+    assert ct_digest(prod) == d["mult"]
+    assert np.array_equal(ckks.decrypt_vector(prod, keys)[:64], np.array(d["mult_dec"]))
+    assert ct_digest(ckks.add(cu, cv)) == d["add"]
+    assert ct_digest(ckks.sub(cu, cv)) == d["sub"]
+    assert ct_digest(ckks.rescale(ops.mult_plain(cu, 0.5, rescale_after=False))) == d["rescale"]
+    assert ct_digest(ckks.mult_plain(cu, v)) == d["mult_plain_vec"]
+    assert ct_digest(ckks.add_plain(cu, 0.25)) == d["add_plain_const"]
+    assert ct_digest(ckks.mod_down(cu, max(1, L // 2))) == d["mod_down"]
+    assert ct_digest(ckks.add(prod, ckks.mod_down(cv, prod.level - 1))) == d["add_aligned"]
+    if "rot_3" in d:
+        for s in d["rotation_steps"]:
+            assert ct_digest(ckks.rotate(cu, s, keys)) == d[f"rot_{s}"]
+        assert ct_digest(ckks.rotate(cu, 3, keys)) == d["rot_3"]
+        assert np.array_equal(ckks.decrypt_vector(cu, keys)[:64], np.array(d["dec_u"]))
+    if "conj_ct" in d:
+        assert ct_digest(ckks.conjugate(cu, keys)) == d["conj_ct"]
+
+
+def test_sigmoid_bsgs_bit_exact(digests, sigmoid15):
+    d = digests["desk"]
+    params, keys = keyset("desk", d)
+    pts = np.linspace(-12, 12, params.slot_count)
+    ct = ckks.encrypt_vector(params, pts, keys, rng_seed=9)
+    out = ckks.eval_poly_bsgs(ct, sigmoid15, keys)
+    assert ct_digest(out) == d["sigmoid_bsgs"]
+    assert np.array_equal(ckks.decrypt_vector(out, keys)[:64], np.array(d["sigmoid_dec"]))
+
+
+def test_batched_key_switch_equals_single(digests):
+    """B ciphertext components through one key switch stream the key once and
+    give the same limbs as B separate switches."""
+    params, keys = keyset("desk", digests["desk"])
+    lvl = params.max_level
+    polys = [ring.sample_poly(params.ring, "uniform", lvl, np.random.default_rng(50 + i))
+             for i in range(4)]
+    batch = ring.RnsPoly(params.ring, np.stack([p.limbs for p in polys]), ring.EVAL, lvl)
+    kb, ka = K.ks_apply(keys, keys.relin_key, batch)
+    for i, p in enumerate(polys):
+        sb, sa = K.ks_apply(keys, keys.relin_key, ring.RnsPoly(params.ring, p.limbs, ring.EVAL, lvl))
+        assert np.array_equal(kb.limbs[i], sb.limbs)
+        assert np.array_equal(ka.limbs[i], sa.limbs)
+
+
+def test_batched_ciphertext_pipeline(digests):
+    """mult / rotate / rescale on a stacked batch equal the per-ciphertext results."""
+    params, keys = keyset("desk", digests["desk"])
+    rng = np.random.default_rng(77)
+    cts = [ckks.encrypt_vector(params, rng.uniform(-1, 1, params.slot_count), keys, rng_seed=i)
+           for i in range(3)]
+    w = ckks.encrypt_vector(params, rng.uniform(-1, 1, params.slot_count), keys, rng_seed=10)
+    batch = ops.stack(cts)
+    got = ckks.rotate(ckks.mult(batch, w, keys), 1, keys)
+    for i, c in enumerate(cts):
+        want = ckks.rotate(ckks.mult(c, w, keys), 1, keys)
+        assert np.array_equal(got[i].c0.limbs, want.c0.limbs)
+        assert np.array_equal(got[i].c1.limbs, want.c1.limbs)
+        assert got.scale == want.scale
+
+
+# ---- reference tolerance tests (T/test_ckks.py) ----------------------------
+
+
+@pytest.fixture(scope="module")
+def desk_keys(digests):
+    return keyset("desk", digests["desk"])
+
+
+def test_encode_decode(desk_keys):
+    params, _ = desk_keys
+    rng = np.random.default_rng(12)
+    v = rng.uniform(-1, 1, 768)
+    pt = ckks.encode(params, v, 3)
+    out = ckks.decode_real(pt)
+    assert np.max(np.abs(out[:768] - v)) < 1e-4
+    assert np.max(np.abs(out[768:])) < 1e-4
+    with pytest.raises(CryptoError):
+        ckks.encode(params, v[:16], 0, scale=2.0 ** 80)
+
+
+def test_add_mult_rotate_tolerances(desk_keys):
+    params, keys = desk_keys
+    rng = np.random.default_rng(12)
+    for _ in range(5):
+        u = rng.uniform(-1, 1, params.slot_count)
+        v = rng.uniform(-1, 1, params.slot_count)
+        cu = ckks.encrypt_vector(params, u, keys)
+        cv = ckks.encrypt_vector(params, v, keys)
+        assert np.max(np.abs(ckks.decrypt_vector(ckks.add(cu, cv), keys) - (u + v))) < 1e-3
+        prod = ckks.mult(cu, cv, keys)
+        assert np.max(np.abs(ckks.decrypt_vector(prod, keys) - u * v)) < 1e-2
+        assert prod.level == cu.level - 1
+    u = rng.uniform(-1, 1, params.slot_count)
+    ct = ckks.encrypt_vector(params, u, keys)
+    back = ckks.rotate(ckks.rotate(ct, 1, keys), -1, keys)
+    assert np.max(np.abs(ckks.decrypt_vector(back, keys) - u)) < 1e-3
+    five = ckks.decrypt_vector(ckks.rotate(ct, 5, keys), keys)
+    assert np.max(np.abs(five - np.roll(u, -5))) < 1e-3
+    conj = ckks.decrypt_vector(ckks.conjugate(ct, keys), keys)
+    assert np.max(np.abs(conj - u)) < 1e-3
+
+
+def test_squaring_chain_and_levels(desk_keys):
+    params, keys = desk_keys
+    ct = ckks.encrypt_vector(params, np.full(params.slot_count, 0.9), keys)
+    for _ in range(params.max_level - 1):
+        ct = ckks.square(ct, keys)
+    want = 0.9 ** (2 ** (params.max_level - 1))
+    assert np.max(np.abs(ckks.decrypt_vector(ct, keys) - want)) < 1e-2
+    low = ckks.mod_down(ckks.encrypt_vector(params, np.ones(8), keys), 0)
+    with pytest.raises(OutOfLevelsError, match="bootstrap"):
+        ckks.mult(low, low, keys)
+    with pytest.raises(OutOfLevelsError):
+        ckks.rescale(low)
+
+
+def test_scale_mismatch_and_missing_key(desk_keys):
+    params, keys = desk_keys
+    rng = np.random.default_rng(3)
+    v = rng.uniform(-1, 1, 16)
+    a = ckks.encrypt(ckks.encode(params, v, 2, scale=2.0 ** 40), keys)
+    b = ckks.encrypt(ckks.encode(params, v, 2, scale=2.0 ** 41), keys)
+    with pytest.raises(ScaleMismatchError):
+        ckks.add(a, b)
+    limited = ckks.keygen(params, rotation_steps=[], rng_seed=1, include_conjugation=False)
+    ct = ckks.encrypt_vector(params, v, limited)
+    with pytest.raises(MissingRotationKeyError):
+        ckks.rotate(ct, 3, limited)
+
+
+def test_poly_eval_depth(desk_keys, sigmoid15):
+    params, keys = desk_keys
+    pts = np.array([-12.0, -6.0, 0.0, 6.0, 12.0])
+    ct = ckks.encrypt_vector(params, pts, keys)
+    out = ckks.eval_poly_bsgs(ct, sigmoid15, keys)
+    got = ckks.decrypt_vector(out, keys, 5)
+    assert np.max(np.abs(got - minimax.eval_cheb(sigmoid15, pts))) < 1e-2
+    assert ct.level - out.level == ckks.bsgs_depth(15)
+    lin = minimax.remez_fit("linear", (-1, 1), 1)
+    v = np.random.default_rng(4).uniform(-1, 1, params.slot_count)
+    got = ckks.decrypt_vector(ckks.eval_poly_bsgs(ckks.encrypt_vector(params, v, keys), lin, keys),
+                              keys)
+    assert np.max(np.abs(got - v)) < 1e-3
+
+
+def test_serialization_roundtrip(desk_keys):
+    params, keys = desk_keys
+    ct = ckks.encrypt_vector(params, np.random.default_rng(1).uniform(-1, 1, 32), keys)
+    blob = ckks.serialize_ciphertext(ct)
+    assert ckks.serialize_ciphertext(ckks.deserialize_ciphertext(blob, params)) == blob
+    assert len(blob) == ckks.size_report(params, ct.level)

@@ -1,0 +1,132 @@
+"""GPU parity: the kernel table and ring layer vs the reference's golden
+vectors (bit-exact) and the reference ring tests (T/test_ring.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_npz, preset_text
+
+pytestmark = pytest.mark.gpu
+
+from paper_2210_02574_b200 import _kernels, ring  # noqa: E402
+from paper_2210_02574_b200.errors import CryptoError, FormMismatchError, LevelMismatchError  # noqa: E402
+
+
+def test_kernel_table_bit_exact():
+    g = golden_npz("kernels_n64.npz")
+    q, qinv, r2 = g["q"], g["qinv"], g["r2"]
+    a, b = g["a"], g["b"]
+    assert np.array_equal(_kernels.elementwise_mulmod(a, b, q, qinv, r2), g["mulmod"])
+    assert np.array_equal(_kernels.elementwise_mont(a, b, q, qinv), g["mont"])
+    assert np.array_equal(_kernels.rowwise_mont(a, g["c"], q, qinv), g["rowwise"])
+    assert np.array_equal(_kernels.addmod_rows(a, b, q), g["add"])
+    assert np.array_equal(_kernels.submod_rows(a, b, q), g["sub"])
+    assert np.array_equal(_kernels.base_convert(g["hat"], g["punc"], q, qinv), g["bconv"])
+    acc = a.copy()
+    assert np.array_equal(_kernels.fma_inplace(acc, b, a, q, qinv, r2), g["fma"])
+    acc = b.copy()
+    out = _kernels.fma_gather_inplace(acc, a, g["key"], g["rows"], q, qinv, r2)
+    assert out is acc and np.array_equal(out, g["fma_gather"])
+    f = a.copy()
+    assert np.array_equal(_kernels.ntt_forward_inplace(f, g["psi_rev"], q, qinv), g["ntt_fwd"])
+    assert np.array_equal(f, g["ntt_fwd"])  # in place
+    f = a.copy()
+    assert np.array_equal(_kernels.ntt_inverse_inplace(f, g["ipsi_rev"], g["ninv"], q, qinv),
+                          g["ntt_inv"])
+
+
+def test_ring_ops_bit_exact():
+    g = golden_npz("ring_n64.npz")
+    primes = tuple(int(x) for x in g["primes"])
+    p = ring.RingParams("r64", 64, primes)
+    x = ring.RnsPoly(p, g["x"], ring.COEFF, 2)
+    y = ring.RnsPoly(p, g["y"], ring.COEFF, 2)
+    xe, ye = ring.to_eval(x), ring.to_eval(y)
+    assert np.array_equal(xe.limbs, g["x_eval"])
+    assert np.array_equal(ring.poly_mul(xe, ye).limbs, g["prod"])
+    assert np.array_equal(ring.to_coeff(ring.poly_mul(xe, ye)).limbs, g["prod_coeff"])
+    for gg in (3, 5, 127):
+        assert np.array_equal(ring.poly_automorphism_eval(xe, gg).limbs, g[f"auto_eval_{gg}"])
+        assert np.array_equal(ring.poly_automorphism(x, gg).limbs, g[f"auto_coeff_{gg}"])
+    assert np.array_equal(ring.poly_from_signed(p, g["signed"], 2).limbs, g["lifted"])
+    assert np.array_equal(ring._eval_exponent_map(p)[0], g["exps"])
+
+
+@pytest.mark.parametrize("name", ["p14", "p16"])
+def test_full_chain_ntt_digest(name, digests):
+    from oracle.scheme import sha
+    from paper_2210_02574_b200.ckks import CkksParams
+
+    params = CkksParams.from_config_text(preset_text(name))
+    L = params.max_level
+    up = ring.sample_poly(params.ring, "uniform", L, np.random.default_rng(1000))
+    assert sha(ring.to_eval(up).limbs) == digests[name]["ntt_fwd"]
+    inv = ring.ntt_transform(ring.RnsPoly(params.ring, up.limbs, ring.EVAL, L), "inverse")
+    assert sha(inv.limbs) == digests[name]["ntt_inv"]
+
+
+@pytest.mark.parametrize("n", [16, 1024, 1 << 13, 1 << 15, 1 << 17])
+def test_ntt_roundtrip_and_oracle(n):
+    """Every supported size vs the oracle (reference T/test_ring.py:29-42)."""
+    from oracle import scheme as S
+
+    primes = tuple(ring.generate_ntt_primes(60, 1, n) + ring.generate_ntt_primes(40, 2, n))
+    p = ring.RingParams("rt", n, primes)
+    a = ring.sample_poly(p, "uniform", 2, np.random.default_rng(1))
+    fwd = ring.ntt_transform(a, "forward")
+    op = S.Params(n, primes, (), 2.0 ** 40, 1, None, 3.2)
+    assert np.array_equal(fwd.limbs, S.ntt_fwd(op, a.limbs, primes))
+    back = ring.ntt_transform(fwd, "inverse")
+    assert np.array_equal(a.limbs, back.limbs)
+
+
+def test_constant_and_wraparound():
+    p = ring.RingParams("t16", 16, (97,))
+    c = ring.poly_from_signed(p, [5] + [0] * 15, 0)
+    assert set(ring.to_eval(c).limbs[0].tolist()) == {5}
+    half = ring.to_eval(ring.poly_from_signed(p, [0] * 8 + [1] + [0] * 7, 0))
+    assert ring.to_coeff(ring.poly_mul(half, half)).limbs[0].tolist() == [96] + [0] * 15
+    z = ring.zero_poly(p, 0, form=ring.COEFF)
+    assert not ring.ntt_transform(z, "forward").limbs.any()
+
+
+def test_errors():
+    p = ring.RingParams("lm", 16, tuple(ring.generate_ntt_primes(30, 2, 16)))
+    rng = np.random.default_rng(4)
+    a = ring.to_eval(ring.sample_poly(p, "uniform", 1, rng))
+    b = ring.to_eval(ring.sample_poly(p, "uniform", 0, rng))
+    with pytest.raises(LevelMismatchError):
+        ring.poly_mul(a, b)
+    with pytest.raises(FormMismatchError):
+        ring.ntt_transform(a, "forward")
+    with pytest.raises(CryptoError):
+        ring.sample_poly(p, "discrete_gaussian", 0, rng, sigma=0)
+
+
+def test_sampling_statistics():
+    p = ring.RingParams("s13", 1 << 13, tuple(ring.generate_ntt_primes(40, 1, 1 << 13)))
+    s = ring.sample_poly(p, "ternary", 0, np.random.default_rng(6))
+    q = p.moduli_chain[0]
+    vals = s.limbs[0]
+    assert set(np.unique(vals)) <= {0, 1, q - 1}
+    g = ring.sample_poly(p, "discrete_gaussian", 0, np.random.default_rng(7), sigma=3.2)
+    v = g.limbs[0].astype(np.int64)
+    v = np.where(v > q // 2, v - q, v)
+    assert abs(v.std() - 3.2) < 0.32
+    h = ring.sample_poly(p, "ternary", 0, np.random.default_rng(8), hamming_weight=64)
+    assert int(np.sum(h.limbs[0] != 0)) == 64
+
+
+def test_batched_ops_equal_single():
+    """A (B, k, N) batch through one launch equals B separate calls."""
+    primes = tuple(ring.generate_ntt_primes(40, 3, 1024))
+    p = ring.RingParams("cc", 1024, primes)
+    rng = np.random.default_rng(13)
+    polys = [ring.to_eval(ring.sample_poly(p, "uniform", 2, rng)) for _ in range(5)]
+    batch = ring.RnsPoly(p, np.stack([x.limbs for x in polys]), ring.EVAL, 2)
+    other = polys[0]
+    prod = ring.poly_mul(batch, other)
+    coeff = ring.to_coeff(batch)
+    for i, x in enumerate(polys):
+        assert np.array_equal(prod.limbs[i], ring.poly_mul(x, other).limbs)
+        assert np.array_equal(coeff.limbs[i], ring.to_coeff(x).limbs)
