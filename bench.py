@@ -284,7 +284,135 @@ class BootstrapWorkload:
                 "diag_cache_gib": round(self.ctx.diag_cache_bytes() / 2 ** 30, 2)}
 
 
-WORKLOADS = {"ks": KsWorkload, "bootstrap": BootstrapWorkload}
+def logreg_rotation_steps(layout):
+    """Rotation steps of the gradient pipeline (logreg.py:202-229)."""
+    steps = set()
+    sh = 1
+    while sh < layout.padded_dim:
+        steps.update((sh, -sh))
+        sh <<= 1
+    sh = layout.padded_dim
+    while sh < layout.padded_dim * layout.rows_per_ct:
+        steps.add(sh)
+        sh <<= 1
+    return steps
+
+
+class TrainWorkload:
+    """cfg4 (SST-2-sized synthetic 768-d embeddings, P16): one minibatch of the
+    encrypted Nesterov trainer = 16 ciphertexts x 32 rows (batch 512), the
+    batched gradient, the modular gradient sum, the update and the
+    sparse-1024 bootstrap refresh of w and u.  Data ciphertexts are at the
+    refresher's output level (the reference excludes the ingest refresh from
+    epoch time, logreg.py:337-339)."""
+
+    metric = "encrypted LR train samples/sec"
+    unit = "samples/s"
+    higher = True
+    batch_rows = 512
+    n_pool = 4  # distinct minibatches cycled through
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg, minimax, shard
+        from paper_2210_02574_b200.ckks import ops
+        from tests.conftest import make_separable
+
+        self.params = params = p16()
+        self.sig = minimax.load_approximant("sigmoid_deg15")
+        self.layout = logreg.make_layout(params, 768)
+        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True)
+        steps = sorted(set(self.ctx.required_rotation_steps()) | logreg_rotation_steps(self.layout))
+        t0 = time.time()
+        self.keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
+        self.keygen_s = time.time() - t0
+        self.refresher = bs.BootstrapRefresher(self.ctx, self.keys)
+        self.cfg = logreg.TrainConfig(1.0, 0.9, self.batch_rows, 1)
+        rows_per_ct = self.layout.rows_per_ct
+        cts = self.batch_rows // rows_per_ct
+        lo, hi = shard.shard_range(cts, rank, world)
+        self.local = hi - lo
+        X, y = make_separable(np.random.default_rng(100), self.batch_rows * self.n_pool, dim=768,
+                              margin=0.5)
+        self.X, self.y = X, y
+        top = self.ctx.output_level
+        self.pool_dev = []
+        for b in range(self.n_pool):
+            xs, ys = [], []
+            for c in range(lo, hi):
+                r0 = b * self.batch_rows + c * rows_per_ct
+                xr, yr = X[r0 : r0 + rows_per_ct], y[r0 : r0 + rows_per_ct]
+                xs.append(ckks.encrypt(ckks.encode(params, logreg._pack_slots(xr, self.layout), top),
+                                       self.keys, rng_seed=10_000 + b * 100 + c))
+                ys.append(ckks.encrypt(
+                    ckks.encode(params, logreg._pack_label_slots(yr, self.layout), 3), self.keys,
+                    rng_seed=20_000 + b * 100 + c))
+            self.pool_dev.append((ops.stack(xs), ops.stack(ys)))
+        # pinned host copies of each minibatch's ciphertexts (the e2e leg uploads them)
+        self.host_x = [torch.stack([xb.c0.data, xb.c1.data], dim=1).cpu().pin_memory()
+                       for xb, _ in self.pool_dev]
+        self.host_y = [torch.stack([yb.c0.data, yb.c1.data], dim=1).cpu().pin_memory()
+                       for _, yb in self.pool_dev]
+        self.w = logreg._zeros_ct(params, self.keys, top)
+        self.u = logreg._zeros_ct(params, self.keys, top)
+        self.it = 0
+        self.units = self.batch_rows
+        self.h2d = (self.host_x[0].numel() + self.host_y[0].numel()) * 8
+        self.d2h = 0
+        self.config = {
+            "workload": "cfg4 encrypted-LR training minibatch (SST-2-shaped synthetic 768-d)",
+            "preset": "p16", "N": params.ring_degree, "batch_rows": self.batch_rows,
+            "ciphertexts_per_minibatch": cts, "rows_per_ct": rows_per_ct,
+            "refresh": "sparse-1024 bootstrap of w and u", "rotation_keys": len(steps),
+            "parallelism": f"minibatch sharded over {world} GPU(s)",
+            "l2": "keys (>14 GiB) and diagonals (36 GiB) exceed L2"}
+
+    def step(self):
+        from paper_2210_02574_b200 import logreg
+
+        xb, yb = self.pool_dev[self.it % self.n_pool]
+        self.it += 1
+        self.w, self.u = logreg.train_minibatch(
+            self.w, self.u, xb, yb, self.batch_rows, self.cfg, self.keys, self.sig, self.layout,
+            self.refresher, local_shard=True)
+        return self.w
+
+    def e2e_step(self):
+        from paper_2210_02574_b200 import logreg
+        from paper_2210_02574_b200.ckks import ops
+
+        i = self.it % self.n_pool
+        self.it += 1
+        xt = self.host_x[i].to("cuda", non_blocking=True)
+        yt = self.host_y[i].to("cuda", non_blocking=True)
+        x0, y0 = self.pool_dev[i]
+        xb = ops._ct(xt, x0.level, x0.scale, x0.slot_count, self.params)
+        yb = ops._ct(yt, y0.level, y0.scale, y0.slot_count, self.params)
+        self.w, self.u = logreg.train_minibatch(
+            self.w, self.u, xb, yb, self.batch_rows, self.cfg, self.keys, self.sig, self.layout,
+            self.refresher, local_shard=True)
+        wh = self.w.c0.data.to("cpu", non_blocking=False)
+        self.d2h = wh.numel() * 8 * 2
+        wh1 = self.w.c1.data.to("cpu")
+        return wh, wh1
+
+    def check(self):
+        from paper_2210_02574_b200 import ckks, logreg
+
+        w = ckks.decrypt_vector(self.w, self.keys)[: self.layout.padded_dim]
+        # replay the same minibatch sequence in the plaintext shadow trainer
+        n_done = self.it
+        order = [i % self.n_pool for i in range(n_done)]
+        Xs = np.concatenate([self.X[b * self.batch_rows:(b + 1) * self.batch_rows] for b in order])
+        ys = np.concatenate([self.y[b * self.batch_rows:(b + 1) * self.batch_rows] for b in order])
+        sh = logreg.shadow_train(Xs, ys, self.cfg, self.sig, layout=self.layout)
+        return {"weights_vs_shadow_max_abs": float(np.max(np.abs(w - sh.weights[0]))),
+                "minibatches_applied": n_done, "keygen_s": round(self.keygen_s, 1),
+                "diag_cache_gib": round(self.ctx.diag_cache_bytes() / 2 ** 30, 2)}
+
+
+WORKLOADS = {"train": TrainWorkload, "ks": KsWorkload, "bootstrap": BootstrapWorkload}
 
 
 # ---------------------------------------------------------------------------

@@ -176,14 +176,17 @@ int hegpu_encrypt_combine(hegpu_ring_t ring, const uint64_t* v, const uint64_t* 
                           void* stream);
 
 /* Plaintext-diagonal multiply-accumulate for the BSGS linear transforms
- * (_apply_diag_transform, bootstrap.py:200-247): for each of n_terms terms t,
- * out += pt[t] * ct[t] over both ciphertext components, where ct[t] is a
- * ciphertext (c0 at ct_ptrs[t], c1 at ct_ptrs[t] + ct_c1_off) and pt[t] a
- * plaintext poly; k chain limbs.  out c1 at out + out_c1_off.  accumulate=0
- * overwrites out.  Host arrays of device pointers. */
+ * (_apply_diag_transform, bootstrap.py:200-247): for each of n_terms terms t
+ * and each of n_batch ciphertexts b,
+ *   out_b.c0 (+)= pt[t] * ct[t]_b.c0,   out_b.c1 (+)= pt[t] * ct[t]_b.c1,
+ * where ct[t]_b.c0 is at ct_ptrs[t] + b*ct_bstride, c1 at +ct_c1_off, and
+ * out_b.c0 at out + b*out_bstride, c1 at +out_c1_off; k chain limbs.  Each
+ * plaintext diagonal is read once per batch.  accumulate=0 overwrites out.
+ * ct_ptrs / pt_ptrs are host arrays of device pointers. */
 int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct_c1_off,
-                   const uint64_t* const* pt_ptrs, int n_terms, uint64_t* out,
-                   int64_t out_c1_off, int k, int accumulate, void* stream);
+                   int64_t ct_bstride, const uint64_t* const* pt_ptrs, int n_terms,
+                   int n_batch, uint64_t* out, int64_t out_c1_off, int64_t out_bstride, int k,
+                   int accumulate, void* stream);
 
 /* -------------------------------------------------------------------------
  * host-array kernel table: drop-in for hebert._kernels (_kernels.py:319-328)

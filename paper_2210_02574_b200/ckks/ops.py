@@ -19,6 +19,7 @@ import numpy as np
 
 from .. import _dev
 from .. import _lib
+from .. import _stats
 from .. import ring as rg
 from ..errors import CryptoError, LevelMismatchError, OutOfLevelsError, ScaleMismatchError
 from . import keys as keysmod
@@ -292,6 +293,7 @@ def mod_down(ct, target_level):
 
 
 def _rescale_polys(params, level, in_ptr, in_stride, out_ptr, out_stride, cnt):
+    _stats.count("rescale_poly", level, cnt)
     _lib.call(
         "hegpu_rescale", params.ring.device(), level, in_ptr, in_stride, out_ptr, out_stride, cnt,
         _dev.stream(),

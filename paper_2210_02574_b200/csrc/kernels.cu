@@ -375,74 +375,117 @@ void launch_encrypt(const PrimeConst* dpc, int log_n, const EncParams& E0, int k
 // plaintext-diagonal multiply-accumulate (bootstrap.py:222-241)
 // ---------------------------------------------------------------------------
 
-constexpr int kMaxDiagTerms = 32;
+constexpr int kMaxDiagTerms = 64;
+constexpr int kDiagMaxB = 4;
 struct DiagParams {
   const uint64_t* ct[kMaxDiagTerms];
   const uint64_t* pt[kMaxDiagTerms];
   int n_terms;
+  int n_batch;        // ciphertexts per term (<= kDiagMaxB per launch)
   int64_t ct_c1_off;
+  int64_t ct_bstride;  // batch stride of the term ciphertexts
   uint64_t* out;
   int64_t out_c1_off;
+  int64_t out_bstride;
   int k, log_n;
   int accumulate;
   const PrimeConst* pc;
 };
 
-// out_c{0,1} (+)= sum_t pt[t] * ct[t].c{0,1}, one 128-bit accumulator per
-// component, one REDC pair per output.
+// out_b.c{0,1} (+)= sum_t pt[t] * ct[t]_b.c{0,1}.  Each thread owns two
+// adjacent coefficients (128-bit loads) of one limb; the plaintext diagonal
+// is loaded once and applied to every ciphertext of the batch; products are
+// accumulated in 128 bits and reduced once per output (one REDC + R^2 fix).
+template <int NB>
 __global__ void __launch_bounds__(kEwThreads) k_diag_mac(const __grid_constant__ DiagParams P) {
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
-  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
   if (x >= N) return;
   const PrimeConst pc = P.pc[limb];
   const size_t l = (size_t)limb * N + x;
-  Acc128 a0, a1;
-  a0.zero();
-  a1.zero();
+  Acc128 a[NB][4];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[b][c].zero();
+#pragma unroll 2
   for (int t = 0; t < P.n_terms; ++t) {
-    const uint64_t p = P.pt[t][l];
-    a0.mac(P.ct[t][l], p, pc.q);
-    a1.mac(P.ct[t][P.ct_c1_off + l], p, pc.q);
+    const ulonglong2 p = __ldg(reinterpret_cast<const ulonglong2*>(P.pt[t] + l));
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const uint64_t* base = P.ct[t] + b * P.ct_bstride + l;
+      const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(base));
+      const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(base + P.ct_c1_off));
+      a[b][0].mac(v0.x, p.x, pc.q);
+      a[b][1].mac(v0.y, p.y, pc.q);
+      a[b][2].mac(v1.x, p.x, pc.q);
+      a[b][3].mac(v1.y, p.y, pc.q);
+    }
   }
-  uint64_t r0 = mont_mul(redc128(a0.hi, a0.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
-  uint64_t r1 = mont_mul(redc128(a1.hi, a1.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
-  if (P.accumulate) {
-    r0 = add_mod(r0, P.out[l], pc.q);
-    r1 = add_mod(r1, P.out[P.out_c1_off + l], pc.q);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    uint64_t r[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      r[c] = mont_mul(redc128(a[b][c].hi, a[b][c].lo, pc.q, pc.qinv_neg), pc.r2, pc.q,
+                      pc.qinv_neg);
+    uint64_t* o0 = P.out + b * P.out_bstride + l;
+    uint64_t* o1 = o0 + P.out_c1_off;
+    if (P.accumulate) {
+      const ulonglong2 p0 = *reinterpret_cast<const ulonglong2*>(o0);
+      const ulonglong2 p1 = *reinterpret_cast<const ulonglong2*>(o1);
+      r[0] = add_mod(r[0], p0.x, pc.q);
+      r[1] = add_mod(r[1], p0.y, pc.q);
+      r[2] = add_mod(r[2], p1.x, pc.q);
+      r[3] = add_mod(r[3], p1.y, pc.q);
+    }
+    *reinterpret_cast<ulonglong2*>(o0) = make_ulonglong2(r[0], r[1]);
+    *reinterpret_cast<ulonglong2*>(o1) = make_ulonglong2(r[2], r[3]);
   }
-  P.out[l] = r0;
-  P.out[P.out_c1_off + l] = r1;
 }
 
 void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct,
-                     int64_t ct_c1_off, const uint64_t* const* pt, int n_terms, uint64_t* out,
-                     int64_t out_c1_off, int k, int accumulate, cudaStream_t st) {
-  int done = 0;
-  bool acc = accumulate != 0;
-  if (n_terms == 0 && !acc) throw HegpuError{HEGPU_E_ARG, "diag_mac with no terms"};
-  while (done < n_terms) {
-    DiagParams P;
-    P.n_terms = n_terms - done < kMaxDiagTerms ? n_terms - done : kMaxDiagTerms;
-    for (int t = 0; t < P.n_terms; ++t) {
-      P.ct[t] = ct[done + t];
-      P.pt[t] = pt[done + t];
+                     int64_t ct_c1_off, int64_t ct_bstride, const uint64_t* const* pt,
+                     int n_terms, int n_batch, uint64_t* out, int64_t out_c1_off,
+                     int64_t out_bstride, int k, int accumulate, cudaStream_t st) {
+  if (n_terms == 0 && !accumulate) throw HegpuError{HEGPU_E_ARG, "diag_mac with no terms"};
+  if (n_batch < 1) throw HegpuError{HEGPU_E_ARG, "diag_mac needs n_batch >= 1"};
+  for (int b0 = 0; b0 < n_batch; b0 += kDiagMaxB) {
+    const int nb = n_batch - b0 < kDiagMaxB ? n_batch - b0 : kDiagMaxB;
+    int done = 0;
+    bool acc = accumulate != 0;
+    while (done < n_terms) {
+      DiagParams P;
+      P.n_terms = n_terms - done < kMaxDiagTerms ? n_terms - done : kMaxDiagTerms;
+      for (int t = 0; t < P.n_terms; ++t) {
+        P.ct[t] = ct[done + t] + b0 * ct_bstride;
+        P.pt[t] = pt[done + t];
+      }
+      P.n_batch = nb;
+      P.ct_c1_off = ct_c1_off;
+      P.ct_bstride = ct_bstride;
+      P.out = out + b0 * out_bstride;
+      P.out_c1_off = out_c1_off;
+      P.out_bstride = out_bstride;
+      P.k = k;
+      P.log_n = log_n;
+      P.accumulate = acc ? 1 : 0;
+      P.pc = dpc;
+      dim3 grid(((1 << log_n) / 2 + kEwThreads - 1) / kEwThreads, k);
+      ProfScope ps(PROF_DIAG_MAC, st,
+                   (double)k * (1 << log_n) * 8.0 * (P.n_terms * (1.0 + 2.0 * nb) + (acc ? 4 : 2) * nb),
+                   (double)k * (1 << log_n) * nb * (2.0 * P.n_terms + 4));
+      switch (nb) {
+        case 1: k_diag_mac<1><<<grid, kEwThreads, 0, st>>>(P); break;
+        case 2: k_diag_mac<2><<<grid, kEwThreads, 0, st>>>(P); break;
+        case 3: k_diag_mac<3><<<grid, kEwThreads, 0, st>>>(P); break;
+        default: k_diag_mac<4><<<grid, kEwThreads, 0, st>>>(P); break;
+      }
+      check_cuda(cudaGetLastError(), "diag_mac launch");
+      done += P.n_terms;
+      acc = true;
     }
-    P.ct_c1_off = ct_c1_off;
-    P.out = out;
-    P.out_c1_off = out_c1_off;
-    P.k = k;
-    P.log_n = log_n;
-    P.accumulate = acc ? 1 : 0;
-    P.pc = dpc;
-    dim3 grid(((1 << log_n) + kEwThreads - 1) / kEwThreads, k);
-    ProfScope ps(PROF_DIAG_MAC, st,
-                 (double)k * (1 << log_n) * 8.0 * (3.0 * P.n_terms + (acc ? 4 : 2)),
-                 (double)k * (1 << log_n) * (2.0 * P.n_terms + 4));
-    k_diag_mac<<<grid, kEwThreads, 0, st>>>(P);
-    check_cuda(cudaGetLastError(), "diag_mac launch");
-    done += P.n_terms;
-    acc = true;
   }
 }
 

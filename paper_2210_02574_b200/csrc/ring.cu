@@ -865,13 +865,14 @@ int hegpu_encrypt_combine(hegpu_ring_t ring, const uint64_t* v, const uint64_t* 
 }
 
 int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct_c1_off,
-                   const uint64_t* const* pt_ptrs, int n_terms, uint64_t* out,
-                   int64_t out_c1_off, int k, int accumulate, void* stream) {
+                   int64_t ct_bstride, const uint64_t* const* pt_ptrs, int n_terms,
+                   int n_batch, uint64_t* out, int64_t out_c1_off, int64_t out_bstride, int k,
+                   int accumulate, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
-    launch_diag_mac(R.dpc, R.log_n, ct_ptrs, ct_c1_off, pt_ptrs, n_terms, out, out_c1_off, k,
-                    accumulate, S_(stream));
+    launch_diag_mac(R.dpc, R.log_n, ct_ptrs, ct_c1_off, ct_bstride, pt_ptrs, n_terms, n_batch,
+                    out, out_c1_off, out_bstride, k, accumulate, S_(stream));
   })
 }
 

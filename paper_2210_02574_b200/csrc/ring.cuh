@@ -196,8 +196,9 @@ void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int
 void launch_encrypt(const PrimeConst* dpc, int log_n, const EncParams& E0, int k,
                     cudaStream_t st);
 void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct,
-                     int64_t ct_c1_off, const uint64_t* const* pt, int n_terms, uint64_t* out,
-                     int64_t out_c1_off, int k, int accumulate, cudaStream_t st);
+                     int64_t ct_c1_off, int64_t ct_bstride, const uint64_t* const* pt,
+                     int n_terms, int n_batch, uint64_t* out, int64_t out_c1_off,
+                     int64_t out_bstride, int k, int accumulate, cudaStream_t st);
 void launch_ks_ip(IpParams& P, cudaStream_t st);
 double bench_modmul_peak(int iters);
 

@@ -227,6 +227,9 @@ def main():
         digests[name], _ = scheme_digests(params, name, [1], conj=False, full=(name == "p14"))
         print(name, "done", time.time() - t0, file=sys.stderr)
     digests["boot_desk64"] = boot_fixture()
+    ref_sig = os.path.join(os.path.dirname(minimax.__file__), "approximants", "sigmoid_deg15.txt")
+    digests["sigmoid_ref"] = [float(c).hex() for c in
+                              minimax.import_text(open(ref_sig).read()).cheb_coeffs]
     logreg_fixture()
     with open(os.path.join(HERE, "digests.json"), "w") as fh:
         json.dump(digests, fh, indent=1, sort_keys=True)

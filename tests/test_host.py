@@ -1,0 +1,148 @@
+"""Host-side logic of the engine (no GPU): presets and params hash, digit
+groups, minimax fits vs the reference's coefficients, packing layouts, the
+plaintext shadow trainer vs the reference's, sharding arithmetic."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_npz, preset_text
+from paper_2210_02574_b200 import logreg, minimax, ring, shard
+from paper_2210_02574_b200.ckks import params as P
+from paper_2210_02574_b200.errors import ApproximationError, CryptoError, DataError
+
+
+def test_preset_hashes_match_survey():
+    assert P.get_preset("p14").params_hash().hex()[:16] == "19ccb5aaa2a93e75"
+    assert P.get_preset("p16").params_hash().hex()[:16] == "6d2a5cc54b140f43"
+    p16 = P.get_preset("p16")
+    assert p16.max_level == 21 and p16.digit_size == 6 and len(p16.ring.special_moduli) == 5
+    assert p16.digit_groups(21) == [list(range(0, 6)), list(range(6, 12)), list(range(12, 18)),
+                                    list(range(18, 22))]
+    assert p16.digit_groups(13)[-1] == [12, 13]
+
+
+def test_builtin_presets_roundtrip(tmp_path, monkeypatch):
+    for name in P.PRESET_NAMES:
+        params = P.get_preset(name)
+        assert params.slot_count == params.ring_degree // 2
+        back = P.CkksParams.from_config_text(params.to_config_text())
+        assert back == params and back.params_hash() == params.params_hash()
+    desk = P.get_preset("desk")
+    custom = desk.to_config_text().replace("security insecure-test-only",
+                                           "security custom-flavor")
+    (tmp_path / "desk.preset").write_text(custom)
+    monkeypatch.setenv("HEBERT_PRESET_DIR", str(tmp_path))
+    assert P.get_preset("desk").security_preset_name == "custom-flavor"
+    with pytest.raises(CryptoError, match="unknown preset"):
+        P.get_preset("made-up")
+
+
+def test_ring_params_validation():
+    with pytest.raises(CryptoError):
+        ring.RingParams("bad", 24, (97,))
+    with pytest.raises(CryptoError):
+        ring.RingParams("bad", 16, (91,))
+    with pytest.raises(CryptoError):
+        ring.RingParams("bad", 16, (17,))
+    with pytest.raises(CryptoError):
+        ring.RingParams("bad", 16, (97, 97))
+    primes = ring.generate_ntt_primes(40, 4, 1 << 13)
+    assert all(q % (1 << 14) == 1 and q.bit_length() == 40 for q in primes)
+    p = ring.RingParams("cfg", 32, tuple(ring.generate_ntt_primes(30, 2, 32)),
+                        tuple(ring.generate_ntt_primes(31, 1, 32)))
+    assert ring.RingParams.from_config_text(p.to_config_text()) == p
+
+
+def test_host_tables_match_reference_formula():
+    g = golden_npz("kernels_n64.npz")
+    primes = [int(q) for q in g["q"]]
+    p = ring.RingParams("k64", 64, tuple(primes))
+    st = p.stacked(tuple(primes))
+    assert np.array_equal(st.psi_rev, g["psi_rev"])
+    assert np.array_equal(st.ipsi_rev, g["ipsi_rev"])
+    assert np.array_equal(st.ninv1, g["ninv"])
+
+
+def test_sigmoid_fit_bit_identical_to_reference(digests):
+    ref = np.array([float.fromhex(c) for c in digests["sigmoid_ref"]])
+    poly = minimax.remez_fit("sigmoid", (-12, 12), 15)
+    assert np.array_equal(poly.cheb_coeffs, ref)
+    assert abs(poly.certified_max_error - 0.00614) <= 0.05 * 0.00614
+    assert minimax.equioscillation_check(poly, "sigmoid")
+    shipped = minimax.load_approximant("sigmoid_deg15")
+    assert np.array_equal(shipped.cheb_coeffs, ref)
+    assert minimax.import_text(minimax.export_text(shipped)).cheb_coeffs.tolist() == ref.tolist()
+
+
+def test_sine_fit_matches_reference(digests):
+    ref = np.array([float.fromhex(c) for c in digests["boot_desk64"]["sine_coeffs"]])
+    poly = minimax.remez_fit("sine2pi", (-14.5, 14.5), 119)
+    assert np.max(np.abs(poly.cheb_coeffs - ref)) < 1e-12
+
+
+def test_minimax_contract():
+    assert minimax.remez_fit("linear", (-3, 5), 1).certified_max_error <= 1e-12
+    with pytest.raises(ApproximationError):
+        minimax.remez_fit("sigmoid", (-1, 1), 0)
+    odd = minimax.remez_fit("sine2pi", (-5.5, 5.5), 47)
+    assert odd.degree == 47 and minimax.equioscillation_check(odd, "sine2pi")
+    a = minimax.remez_fit("sigmoid", (-6, 6), 7)
+    b = minimax.remez_fit("sigmoid", (-6, 6), 7)
+    assert np.array_equal(a.cheb_coeffs, b.cheb_coeffs)
+    xs = np.linspace(-8, 8, 257)
+    poly = minimax.remez_fit("sigmoid", (-8, 8), 15)
+    mono = minimax.to_monomial(poly)
+    assert np.max(np.abs(minimax.eval_cheb(poly, xs) - np.polynomial.polynomial.polyval(xs, mono))) < 1e-10
+
+
+def test_layout_and_config():
+    params = P.get_preset("p16")
+    lay = logreg.make_layout(params, 768)
+    assert (lay.padded_dim, lay.rows_per_ct, lay.bias_index) == (1024, 32, 768)
+    assert logreg.make_layout(params, 1024).rows_per_ct == 16
+    with pytest.raises(DataError):
+        logreg.PackingLayout(768, 768, 1, 1024)
+    with pytest.raises(DataError):
+        logreg.TrainConfig(momentum_gamma=1.0)
+    slots = logreg._pack_slots(np.ones((2, 768)), lay)
+    assert slots[768] == 1.0 and slots[1024 + 768] == 1.0 and slots[769] == 0.0
+    assert logreg.iteration_depth(minimax.load_approximant("sigmoid_deg15")) == 8
+
+
+def test_shadow_trainer_matches_reference(sigmoid15):
+    g = golden_npz("logreg_desk.npz")
+    layout = logreg.make_layout(P.get_preset("desk"), 16)
+    cfg = logreg.TrainConfig(1.0, 0.9, 128, 2)
+    sh = logreg.shadow_train(g["X"], g["y"], cfg, sigmoid15, layout=layout)
+    assert np.array_equal(sh.weights, g["shadow_weights"])
+
+
+def test_batches_and_threshold():
+    assert list(logreg._batches(5, 32, 150, 64)) == [([0, 1], 64), ([2, 3], 64), ([4], 22)]
+    scores = np.array([0.1, 0.4, 0.6, 0.9])
+    assert logreg.tune_threshold(scores, np.array([0, 0, 1, 1])) == pytest.approx(0.5)
+
+
+@pytest.mark.parametrize("n,world", [(16, 1), (16, 2), (16, 8), (3, 8), (17, 4)])
+def test_shard_ranges_partition(n, world):
+    seen = []
+    for r in range(world):
+        lo, hi = shard.shard_range(n, r, world)
+        seen.extend(range(lo, hi))
+    assert seen == list(range(n))
+    sizes = [shard.shard_range(n, r, world)[1] - shard.shard_range(n, r, world)[0]
+             for r in range(world)]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_wrapping_allreduce_contract():
+    """NCCL int64 SUM wraps mod 2^64; one mod-q pass gives the modular sum."""
+    primes = P.get_preset("p16").ring.moduli_chain[:3] + (2 ** 61 - 1,)
+    assert shard.check_allreduce_exact(primes, 8)
+    rng = np.random.default_rng(0)
+    ranks = [np.stack([rng.integers(0, q, 64, dtype=np.uint64) for q in primes])
+             for _ in range(8)]
+    got = shard.modular_sum_host(ranks, primes)
+    want = np.stack([sum(r[i].astype(object) for r in ranks) % q for i, q in enumerate(primes)])
+    assert got.astype(object).tolist() == want.tolist()
+    assert shard.refresh_owner(0, 1) == 0 and shard.refresh_owner(1, 2) == 1
