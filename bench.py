@@ -317,7 +317,7 @@ class TrainWorkload:
 
         from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg, minimax, shard
         from paper_2210_02574_b200.ckks import ops
-        from tests.conftest import make_separable
+        from paper_2210_02574_b200.synth import make_separable
 
         self.params = params = p16()
         self.sig = minimax.load_approximant("sigmoid_deg15")

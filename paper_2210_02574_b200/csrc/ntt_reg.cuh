@@ -1,0 +1,156 @@
+// Register-resident radix NTT passes (sm_100a), used for N >= 2^12.
+//
+// Same decomposition as ntt.cu (forward: column pass over the first a stages,
+// block pass over the rest; inverse reversed), but each S-point sub-transform
+// (S = 2^LOGS in {64..512}) is owned by ONE warp: every lane keeps E = S/32
+// elements in registers and runs log2(E) butterfly stages per round without
+// any barrier; between rounds the warp re-distributes its elements through a
+// warp-private shared-memory buffer (__syncwarp only).  The element index j
+// of (lane, e) in a round whose register window starts at bit `lo` is
+//     j = (lane & (2^lo - 1)) | (e << lo) | ((lane >> lo) << (lo + log2 E)),
+// so a butterfly at distance t = 2^p pairs registers e and e + 2^(p - lo).
+// Twiddle indices are the reference's psi_rev[m + i] / ipsi_rev[h + i]
+// (hebert/_kernels.py:152-203) expressed in global stage/group terms, so the
+// output is bit-identical to the CT/GS transforms.
+#pragma once
+#include "common.cuh"
+
+namespace hegpu {
+
+template <int LOGS>
+struct RegShape {
+  static constexpr int S = 1 << LOGS;
+  static constexpr int EB = LOGS - 5;  // log2(elements per lane)
+  static constexpr int E = 1 << EB;
+  static constexpr int ROUNDS = (LOGS + EB - 1) / EB;
+  static constexpr int PAD_S = S + S / 16;  // warp buffer with 1 pad word per 16
+};
+
+__device__ __forceinline__ int reg_j(int lane, int e, int lo, int eb) {
+  return (lane & ((1 << lo) - 1)) | (e << lo) | ((lane >> lo) << (lo + eb));
+}
+__device__ __forceinline__ int padi(int j) { return j + (j >> 4); }
+
+// Forward CT butterflies on register window [lo, lo+EB) for bit positions
+// p = phi down to plo (t = 2^p within the sub-transform).  Twiddle index of
+// the butterfly whose lower element is j at local stage st (t = 2^(LOGS-1-st))
+// is tw_base(st) + (j >> (p + 1)), tw_base(st) = (1 << (g0 + st)) + (blk << st).
+template <int LOGS>
+__device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
+                                          int phi, int plo, int g0, int blk,
+                                          const uint64_t* __restrict__ w,
+                                          const uint64_t* __restrict__ wsh, uint64_t q) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  const uint64_t q2 = q << 1;
+#pragma unroll
+  for (int p = LOGS - 1; p >= 0; --p) {
+    if (p > phi || p < plo) continue;
+    const int st = LOGS - 1 - p;
+    const int d = 1 << (p - lo);
+    const int base = (1 << (g0 + st)) + (blk << st);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & d) continue;
+      const int j = reg_j(lane, e, lo, EB);
+      const int ti = base + (j >> (p + 1));
+      uint64_t u = x[e];
+      u = u >= q2 ? u - q2 : u;
+      const uint64_t v = shoup_lazy(x[e + d], __ldg(w + ti), __ldg(wsh + ti), q);
+      x[e] = u + v;
+      x[e + d] = u - v + q2;
+    }
+  }
+}
+
+// Inverse GS butterflies for bit positions p = plo up to phi.  Twiddle index
+// is hbase(p) + (blk << (LOGS - p - 1)) + (j >> (p + 1)) with
+// hbase(p) = N >> (gshift + p + 1), gshift the global bit offset of this pass.
+// When `last_n` the final stage (global t = N/2) folds in N^-1.
+template <int LOGS>
+__device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
+                                          int plo, int phi, int log_n, int gshift, int blk,
+                                          const uint64_t* __restrict__ w,
+                                          const uint64_t* __restrict__ wsh,
+                                          const PrimeConst& pc) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  const uint64_t q = pc.q, q2 = q << 1;
+#pragma unroll
+  for (int p = 0; p < LOGS; ++p) {
+    if (p < plo || p > phi) continue;
+    const int d = 1 << (p - lo);
+    const bool last = (gshift + p == log_n - 1);
+    const int base = (1 << (log_n - gshift - p - 1)) + (blk << (LOGS - p - 1));
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & d) continue;
+      const uint64_t a = x[e], b = x[e + d];
+      uint64_t s = a + b;
+      s = s >= q2 ? s - q2 : s;
+      const uint64_t df = a - b + q2;
+      if (!last) {
+        const int j = reg_j(lane, e, lo, EB);
+        const int ti = base + (j >> (p + 1));
+        x[e] = s;
+        x[e + d] = shoup_lazy(df, __ldg(w + ti), __ldg(wsh + ti), q);
+      } else {
+        x[e] = shoup(s, pc.ninv, pc.ninv_sh, q);
+        x[e + d] = shoup(df, pc.ilast, pc.ilast_sh, q);
+      }
+    }
+  }
+}
+
+// Re-distribute the warp's elements from window lo_from to window lo_to.
+template <int LOGS>
+__device__ __forceinline__ void reg_shuffle(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+                                            int lane, int lo_from, int lo_to) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  if (lo_from == lo_to) return;
+#pragma unroll
+  for (int e = 0; e < E; ++e) buf[padi(reg_j(lane, e, lo_from, EB))] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = buf[padi(reg_j(lane, e, lo_to, EB))];
+  __syncwarp();
+}
+
+// Full S-point forward sub-transform in registers; input layout window
+// lo_in, output layout window lo_out.
+template <int LOGS>
+__device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+                                        int lane, int lo_in, int lo_out, int g0, int blk,
+                                        const uint64_t* w, const uint64_t* wsh, uint64_t q) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int phi = LOGS - 1 - r * EB;
+    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
+    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
+    cur = lo;
+    fwd_round<LOGS>(x, lane, lo, phi, plo, g0, blk, w, wsh, q);
+  }
+  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+}
+
+template <int LOGS>
+__device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+                                        int lane, int lo_in, int lo_out, int log_n, int gshift,
+                                        int blk, const uint64_t* w, const uint64_t* wsh,
+                                        const PrimeConst& pc) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int plo = r * EB;
+    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
+    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
+    cur = lo;
+    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, w, wsh, pc);
+  }
+  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+}
+
+}  // namespace hegpu
