@@ -214,7 +214,9 @@ class KsWorkload:
         from oracle import scheme as S
 
         p = S.Params.from_text(self.params.to_config_text())
-        keys = S.keygen(p, [], 7, conj=False)
+        if getattr(self, "_okeys", None) is None:
+            self._okeys = S.keygen(p, [], 7, conj=False)
+        keys = self._okeys
         rng = np.random.default_rng(1000)
         L = p.max_level
         d = np.stack([rng.integers(0, q, size=p.n, dtype=np.uint64) for q in p.chain])
@@ -226,6 +228,25 @@ class KsWorkload:
         S.ks_apply(p, keys.relin, d, L)
         sec = time.perf_counter() - t0
         return 1.0 / sec, "1 ciphertext: 2x(22-limb NTT + iNTT) + 1 top-level KS (N=2^16)"
+
+
+def cost_model_sample(params, histogram, units, unit_kind):
+    """Reference CPU time of one step from the oracle cost model (bounded sample)."""
+    from oracle.costmodel import OracleCostModel, histogram_levels
+
+    t0 = time.perf_counter()
+    model = OracleCostModel(params.to_config_text())
+    ks_levels, other = histogram_levels(histogram)
+    model.sample(ks_levels, other)
+    sec = model.seconds(histogram)
+    n_ks = sum(v for k, v in histogram.items() if k.startswith("ks@"))
+    n_enc = sum(v for k, v in histogram.items() if k.startswith("encode@"))
+    sample = (f"oracle (C/OpenMP, all host cores) timed KS at levels {ks_levels} and "
+              f"encode/rescale/pt-mult at levels {other} ({time.perf_counter() - t0:.1f}s of "
+              f"CPU sampling), weighted by the step's reference op histogram ({n_ks} KS, "
+              f"{n_enc} encodes): modelled {sec:.1f} s per step")
+    value = units / sec if unit_kind == "rate" else sec * 1e3
+    return value, sample
 
 
 class BootstrapWorkload:
@@ -274,6 +295,9 @@ class BootstrapWorkload:
         self.d2h = out.c0.data.numel() * 16
         host = out.c0.data.cpu()
         return host
+
+    def oracle_sample(self):
+        return cost_model_sample(self.params, self.histogram, 1, "ms")
 
     def check(self):
         from paper_2210_02574_b200 import ckks
@@ -397,6 +421,9 @@ class TrainWorkload:
         wh1 = self.w.c1.data.to("cpu")
         return wh, wh1
 
+    def oracle_sample(self):
+        return cost_model_sample(self.params, self.histogram, self.units, "rate")
+
     def check(self):
         from paper_2210_02574_b200 import ckks, logreg
 
@@ -459,11 +486,21 @@ def run_ours(args):
     wl.e2e_step()
     e2e_ms = max_over_ranks(timed(wl.e2e_step, max(1, args.steps // 2), world), world) / max(
         1, args.steps // 2)
-    # per-kernel-class profile of one step (separate pass, not the timed one)
+    # per-kernel-class profile + reference op histogram of one step (separate
+    # pass, not the timed one)
+    from paper_2210_02574_b200 import _stats
+
+    _stats.enable(True)
     _lib.profile_enable(True)
     wl.step()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
+    wl.histogram = _stats.snapshot()
+    _stats.enable(False)
+    os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+    if rank == 0 and wl.histogram:
+        with open(os.path.join(REPO, "gpurun_out", f"op_histogram_{args.config}.json"), "w") as fh:
+            json.dump(wl.histogram, fh, indent=1, sort_keys=True)
     extra = wl.check() if hasattr(wl, "check") else {}
     if rank != 0:
         return
@@ -502,6 +539,9 @@ def run_ours(args):
             "frac": round(dp["modmuls"] / (dp["ms"] / 1e3) / int_peak, 4)
             if (dp["ms"] and int_peak) else None},
         "kernel_profile_ms": {c: round(p["ms"], 3) for c, p in prof.items() if p["launches"]},
+        "kernel_profile_gbs": {c: round(p["bytes"] / p["ms"] / 1e6, 1)
+                               for c, p in prof.items() if p["launches"] and p["ms"]},
+        "kernel_profile_launches": {c: p["launches"] for c, p in prof.items() if p["launches"]},
         "clocks": clk.summary(),
     }
     line.update(extra)
@@ -530,12 +570,20 @@ def run_reference(args):
         return
     wl = WORKLOADS[args.config]()
 
-    class _P:  # parameters only; no GPU on this path
-        pass
+    from oracle.costmodel import load_histogram
 
-    from paper_2210_02574_b200.ckks import params as P
+    class _Preset:  # the preset file text only: nothing of the engine runs on this arm
+        def __init__(self, path):
+            with open(path) as fh:
+                self.text = fh.read()
 
-    wl.params = P.get_preset("p16")
+        def to_config_text(self):
+            return self.text
+
+    wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", "p16.preset"))
+    if args.config in ("train", "bootstrap"):
+        wl.histogram = load_histogram(args.config)
+        wl.units = TrainWorkload.batch_rows if args.config == "train" else 1
     vals = []
     for i in range(args.warmup + args.steps):
         v, sample = wl.oracle_sample()

@@ -188,6 +188,19 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
                    int n_batch, uint64_t* out, int64_t out_c1_off, int64_t out_bstride, int k,
                    int accumulate, void* stream);
 
+/* All-giants BSGS multiply-accumulate (one launch per linear transform):
+ * for every giant g < n_giants and batch element b < n_batch,
+ *   out[g]_b.c{0,1} = sum_{t < n_terms} pt[idx[g][t]] * baby[t]_b.c{0,1}
+ * with baby[t]_b.c0 at babies[t] + b*bstride, c1 at +c1_off (host array of
+ * n_terms <= 64 device pointers); diagonal i at pt_base + i*pt_stride;
+ * pt_idx a DEVICE int32 array [n_giants][n_terms] (-1 = zero diagonal);
+ * out[g]_b.c0 at out + g*out_gstride + b*bstride, c1 at +c1_off.  Every
+ * diagonal, baby and output crosses HBM once. */
+int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
+               int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
+               const int32_t* pt_idx, int n_giants, uint64_t* out, int64_t out_gstride, int k,
+               void* stream);
+
 /* -------------------------------------------------------------------------
  * host-array kernel table: drop-in for hebert._kernels (_kernels.py:319-328)
  * shapes are (k, n) row-major uint64; vectors are length k

@@ -497,32 +497,86 @@ void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct
 
 constexpr int kMaxConvSrc = 32;
 
+// 128-bit accumulation without reduction; fold() keeps T < q 2^64 (call it
+// at least every second product of two < 2^62 x < q factors).
+struct Acc2 {
+  uint64_t hi, lo;
+  __device__ __forceinline__ void zero() { hi = lo = 0; }
+  __device__ __forceinline__ void add(uint64_t a, uint64_t b) {
+    const uint64_t plo = a * b;
+    const uint64_t phi = __umul64hi(a, b);
+    const uint64_t nlo = lo + plo;
+    hi = hi + phi + (nlo < lo);
+    lo = nlo;
+  }
+  __device__ __forceinline__ void fold(uint64_t q) { hi = hi >= q ? hi - q : hi; }
+};
+
+// Two adjacent coefficients per thread; the job's conversion matrix and the
+// destination moduli are staged in shared memory; NS = compile-time bound on
+// the job's source-limb count (loops fully unrolled, predicated on n_src).
+template <int NS>
 __global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ ConvParams P) {
+  __shared__ uint64_t s_punc[NS * kMaxPrimes];
+  __shared__ uint64_t s_q[kMaxPrimes], s_qi[kMaxPrimes];
   const int N = 1 << P.log_n;
   const int j = blockIdx.y;
   const int poly = blockIdx.z;
-  const int x = blockIdx.x * kEwThreads + threadIdx.x;
-  if (x >= N) return;
   const ConvJob& J = P.job[j];
-  uint64_t hat[kMaxConvSrc];
+  const int ns = J.n_src, nd = J.n_dst;
+  for (int e = threadIdx.x; e < ns * nd; e += blockDim.x) {
+    const int i = e / nd, t = e - i * nd;
+    s_punc[i * kMaxPrimes + t] = J.punc[(size_t)i * J.punc_ld + t];
+  }
+  for (int t = threadIdx.x; t < nd; t += blockDim.x) {
+    const PrimeConst pc = P.pc[P.dst_sel[j][t]];
+    s_q[t] = pc.q;
+    s_qi[t] = pc.qinv_neg;
+  }
+  __syncthreads();
+  const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
+  if (x >= N) return;
+  uint64_t h0[NS], h1[NS];
   const uint64_t* src = J.src + poly * J.src_stride + x;
 #pragma unroll
-  for (int i = 0; i < kMaxConvSrc; ++i) {
-    if (i < J.n_src) {
-      const uint64_t q = P.pc[P.src_sel[j][i]].q;
-      const uint64_t v = src[(size_t)i * N];
-      hat[i] = J.inv ? shoup(v, J.inv[i], J.inv_sh[i], q) : v;
+  for (int i = 0; i < NS; ++i) {
+    if (i < ns) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + (size_t)i * N);
+      if (J.inv) {
+        const uint64_t q = P.pc[P.src_sel[j][i]].q;
+        const uint64_t w = J.inv[i], wsh = J.inv_sh[i];
+        h0[i] = shoup(v.x, w, wsh, q);
+        h1[i] = shoup(v.y, w, wsh, q);
+      } else {
+        h0[i] = v.x;
+        h1[i] = v.y;
+      }
+    } else {
+      h0[i] = h1[i] = 0;
     }
   }
   uint64_t* dst = J.dst + poly * J.dst_stride + x;
-  for (int t = 0; t < J.n_dst; ++t) {
-    const PrimeConst pc = P.pc[P.dst_sel[j][t]];
-    Acc128 acc;
-    acc.zero();
+  for (int t = 0; t < nd; ++t) {
+    const uint64_t q = s_q[t], qi = s_qi[t];
+    Acc2 a0, a1;
+    a0.zero();
+    a1.zero();
 #pragma unroll
-    for (int i = 0; i < kMaxConvSrc; ++i)
-      if (i < J.n_src) acc.mac(hat[i], J.punc[(size_t)i * J.punc_ld + t], pc.q);
-    dst[(size_t)t * N] = redc128(acc.hi, acc.lo, pc.q, pc.qinv_neg);
+    for (int i = 0; i < NS; ++i) {
+      if (i < ns) {
+        const uint64_t c = s_punc[i * kMaxPrimes + t];
+        a0.add(h0[i], c);
+        a1.add(h1[i], c);
+        if (i & 1) {
+          a0.fold(q);
+          a1.fold(q);
+        }
+      }
+    }
+    a0.fold(q);
+    a1.fold(q);
+    *reinterpret_cast<ulonglong2*>(dst + (size_t)t * N) =
+        make_ulonglong2(redc128(a0.hi, a0.lo, q, qi), redc128(a1.hi, a1.lo, q, qi));
   }
 }
 
@@ -537,8 +591,16 @@ void launch_conv(ConvParams& P, cudaStream_t st) {
     cm += (double)P.n_polys * (1 << P.log_n) *
           ((double)P.job[j].n_src * P.job[j].n_dst + P.job[j].n_src);
   }
+  int ns = 1;
+  for (int j = 0; j < P.n_jobs; ++j) ns = P.job[j].n_src > ns ? P.job[j].n_src : ns;
+  grid.x = ((1 << P.log_n) / 2 + kEwThreads - 1) / kEwThreads;
   ProfScope ps(PROF_CONV, st, cb, cm);
-  k_conv<<<grid, kEwThreads, 0, st>>>(P);
+  if (ns <= 2) k_conv<2><<<grid, kEwThreads, 0, st>>>(P);
+  else if (ns <= 4) k_conv<4><<<grid, kEwThreads, 0, st>>>(P);
+  else if (ns <= 6) k_conv<6><<<grid, kEwThreads, 0, st>>>(P);
+  else if (ns <= 8) k_conv<8><<<grid, kEwThreads, 0, st>>>(P);
+  else if (ns <= 12) k_conv<12><<<grid, kEwThreads, 0, st>>>(P);
+  else k_conv<kMaxConvSrc><<<grid, kEwThreads, 0, st>>>(P);
   check_cuda(cudaGetLastError(), "conv launch");
 }
 
@@ -550,54 +612,79 @@ void launch_conv(ConvParams& P, cudaStream_t st) {
 
 
 
+// Two adjacent coefficients per thread (128-bit loads); BETA = compile-time
+// bound on the digit count, predicated on P.beta.
+template <int BETA>
 __global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ IpParams P) {
   const int N = 1 << P.log_n;
   const int r = blockIdx.y;
-  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
   if (x >= N) return;
   const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
   const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
   const PrimeConst pc = P.pc[prime];
-  uint64_t kb[kMaxDigits], ka[kMaxDigits];
+  ulonglong2 kb[BETA], ka[BETA];
 #pragma unroll
-  for (int j = 0; j < kMaxDigits; ++j) {
+  for (int j = 0; j < BETA; ++j) {
     if (j < P.beta) {
-      kb[j] = P.kb[j][(size_t)krow * N + x];
-      ka[j] = P.ka[j][(size_t)krow * N + x];
+      kb[j] = __ldg(reinterpret_cast<const ulonglong2*>(P.kb[j] + (size_t)krow * N + x));
+      ka[j] = __ldg(reinterpret_cast<const ulonglong2*>(P.ka[j] + (size_t)krow * N + x));
     }
   }
   for (int b = 0; b < P.n_batch; ++b) {
-    Acc128 ab, aa;
-    ab.zero();
-    aa.zero();
+    Acc2 b0, b1, a0, a1;
+    b0.zero();
+    b1.zero();
+    a0.zero();
+    a1.zero();
 #pragma unroll
-    for (int j = 0; j < kMaxDigits; ++j) {
+    for (int j = 0; j < BETA; ++j) {
       if (j < P.beta) {
         const int g0 = j * P.alpha;
         const int g1 = min(g0 + P.alpha, P.level + 1);
-        uint64_t v;
+        const uint64_t* src;
         if (r >= g0 && r < g1)
-          v = P.d[b * P.ds + (size_t)r * N + x];
+          src = P.d + b * P.ds + (size_t)r * N + x;
         else
-          v = P.ext[b * P.ext_sb + j * P.ext_sj + (size_t)(r < g0 ? r : r - (g1 - g0)) * N + x];
-        ab.mac(v, kb[j], pc.q);
-        aa.mac(v, ka[j], pc.q);
+          src = P.ext + b * P.ext_sb + j * P.ext_sj + (size_t)(r < g0 ? r : r - (g1 - g0)) * N + x;
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(src));
+        b0.add(v.x, kb[j].x);
+        b1.add(v.y, kb[j].y);
+        a0.add(v.x, ka[j].x);
+        a1.add(v.y, ka[j].y);
+        if (j & 1) {
+          b0.fold(pc.q);
+          b1.fold(pc.q);
+          a0.fold(pc.q);
+          a1.fold(pc.q);
+        }
       }
     }
+    b0.fold(pc.q);
+    b1.fold(pc.q);
+    a0.fold(pc.q);
+    a1.fold(pc.q);
     uint64_t* o = P.acc + b * P.acc_sb + (size_t)r * N + x;
-    o[0] = mont_mul(redc128(ab.hi, ab.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
-    o[(size_t)P.n_ext * N] =
-        mont_mul(redc128(aa.hi, aa.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+    const uint64_t q = pc.q, qn = pc.qinv_neg, r2 = pc.r2;
+    *reinterpret_cast<ulonglong2*>(o) =
+        make_ulonglong2(mont_mul(redc128(b0.hi, b0.lo, q, qn), r2, q, qn),
+                        mont_mul(redc128(b1.hi, b1.lo, q, qn), r2, q, qn));
+    *reinterpret_cast<ulonglong2*>(o + (size_t)P.n_ext * N) =
+        make_ulonglong2(mont_mul(redc128(a0.hi, a0.lo, q, qn), r2, q, qn),
+                        mont_mul(redc128(a1.hi, a1.lo, q, qn), r2, q, qn));
   }
 }
 
 void launch_ks_ip(IpParams& P, cudaStream_t st) {
   if (P.beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
-  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext);
+  dim3 grid(((1 << P.log_n) / 2 + kEwThreads - 1) / kEwThreads, P.n_ext);
   const double ipn = (double)(1 << P.log_n) * P.n_ext;
   ProfScope ps(PROF_KS_IP, st, ipn * 8.0 * (2.0 * P.beta + P.n_batch * (P.beta + 2.0)),
                ipn * P.n_batch * (2.0 * P.beta + 4));
-  k_ks_ip<<<grid, kEwThreads, 0, st>>>(P);
+  if (P.beta <= 2) k_ks_ip<2><<<grid, kEwThreads, 0, st>>>(P);
+  else if (P.beta <= 4) k_ks_ip<4><<<grid, kEwThreads, 0, st>>>(P);
+  else if (P.beta <= 8) k_ks_ip<8><<<grid, kEwThreads, 0, st>>>(P);
+  else k_ks_ip<kMaxDigits><<<grid, kEwThreads, 0, st>>>(P);
   check_cuda(cudaGetLastError(), "ks inner product launch");
 }
 
@@ -650,6 +737,168 @@ double bench_modmul_peak(int iters) {
   cudaEventDestroy(b);
   cudaFree(sink);
   return (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+}
+
+}  // namespace hegpu
+
+namespace hegpu {
+
+// ---------------------------------------------------------------------------
+// All-giants BSGS multiply-accumulate (the linear transforms of bootstrapping,
+// bootstrap.py:200-247): for every giant g and batch element b
+//   out[g]_b.c{0,1} = sum_t pt[idx[g][t]] * baby[t]_b.c{0,1}.
+// A CTA owns 32 coefficients of one limb: it stages those coefficients of
+// every baby ciphertext in shared memory once, then each thread accumulates
+// GPT giants for one coefficient.  HBM traffic is the minimum: every plaintext
+// diagonal, every baby and every output is touched exactly once (the per-giant
+// formulation re-reads all babies once per giant).
+// ---------------------------------------------------------------------------
+constexpr int kBsgsTX = 32;
+constexpr int kBsgsMaxTerms = 64;
+constexpr int kBsgsGroups = kEwThreads / kBsgsTX;  // 8 giant groups per CTA
+
+struct BsgsParams {
+  const uint64_t* baby[kBsgsMaxTerms];
+  int n_terms, n_giants, n_batch, log_n;
+  int64_t c1_off, bstride;          // baby / output component and batch strides
+  const uint64_t* pt_base;
+  int64_t pt_stride;                // elements between diagonals
+  const int32_t* pt_idx;            // device [n_giants][n_terms], -1 = zero diagonal
+  uint64_t* out;
+  int64_t out_gstride;              // elements between giants' outputs
+  const PrimeConst* pc;
+};
+
+template <int NB, int GPT>
+__global__ void __launch_bounds__(kEwThreads) k_bsgs(const __grid_constant__ BsgsParams P) {
+  extern __shared__ uint64_t sm[];  // [n_terms][NB][2][TX]
+  const int N = 1 << P.log_n;
+  const int limb = blockIdx.y;
+  const int x0 = blockIdx.x * kBsgsTX;
+  const PrimeConst pc = P.pc[limb];
+  const int per_term = NB * 2 * kBsgsTX;
+  for (int e = threadIdx.x; e < P.n_terms * per_term; e += blockDim.x) {
+    const int t = e / per_term;
+    const int rem = e - t * per_term;
+    const int b = rem / (2 * kBsgsTX);
+    const int c = (rem / kBsgsTX) & 1;
+    const int xi = rem % kBsgsTX;
+    sm[e] = P.baby[t][b * P.bstride + c * P.c1_off + (size_t)limb * N + x0 + xi];
+  }
+  __syncthreads();
+  const int xi = threadIdx.x % kBsgsTX;
+  const int grp = threadIdx.x / kBsgsTX;
+  Acc2 acc[GPT][NB][2];
+#pragma unroll
+  for (int gg = 0; gg < GPT; ++gg)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      acc[gg][b][0].zero();
+      acc[gg][b][1].zero();
+    }
+  const size_t coef = (size_t)limb * N + x0 + xi;
+  for (int t = 0; t < P.n_terms; ++t) {
+    uint64_t bv[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      bv[b][0] = sm[t * per_term + b * 2 * kBsgsTX + xi];
+      bv[b][1] = sm[t * per_term + b * 2 * kBsgsTX + kBsgsTX + xi];
+    }
+#pragma unroll
+    for (int gg = 0; gg < GPT; ++gg) {
+      const int g = grp * GPT + gg;
+      if (g < P.n_giants) {
+        const int idx = __ldg(P.pt_idx + g * P.n_terms + t);
+        if (idx >= 0) {
+          const uint64_t p = __ldg(P.pt_base + (size_t)idx * P.pt_stride + coef);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            acc[gg][b][0].add(bv[b][0], p);
+            acc[gg][b][1].add(bv[b][1], p);
+          }
+        }
+      }
+    }
+    if (t & 1) {
+#pragma unroll
+      for (int gg = 0; gg < GPT; ++gg)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          acc[gg][b][0].fold(pc.q);
+          acc[gg][b][1].fold(pc.q);
+        }
+    }
+  }
+#pragma unroll
+  for (int gg = 0; gg < GPT; ++gg) {
+    const int g = grp * GPT + gg;
+    if (g >= P.n_giants) continue;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        Acc2 a = acc[gg][b][c];
+        a.fold(pc.q);
+        P.out[g * P.out_gstride + b * P.bstride + c * P.c1_off + coef] =
+            mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+      }
+    }
+  }
+}
+
+template <int NB>
+static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
+  const int gpt_need = (P.n_giants + kBsgsGroups - 1) / kBsgsGroups;
+  dim3 grid((1 << P.log_n) / kBsgsTX, k);
+  const size_t smem = (size_t)P.n_terms * NB * 2 * kBsgsTX * 8;
+  static bool attr = false;
+  if (!attr) {
+    const int mx = 200 * 1024;
+    cudaFuncSetAttribute(k_bsgs<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_bsgs<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_bsgs<NB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr = true;
+  }
+  if (gpt_need <= 1) k_bsgs<NB, 1><<<grid, kEwThreads, smem, st>>>(P);
+  else if (gpt_need <= 2) k_bsgs<NB, 2><<<grid, kEwThreads, smem, st>>>(P);
+  else k_bsgs<NB, 4><<<grid, kEwThreads, smem, st>>>(P);
+}
+
+void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
+                 int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
+                 int64_t pt_stride, const int32_t* pt_idx, int n_giants, uint64_t* out,
+                 int64_t out_gstride, int k, cudaStream_t st) {
+  if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
+  if ((1 << log_n) % kBsgsTX) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
+  const int max_giants = kBsgsGroups * 4;
+  for (int b0 = 0; b0 < n_batch; b0 += 2) {
+    const int nb = n_batch - b0 < 2 ? n_batch - b0 : 2;
+    for (int g0 = 0; g0 < n_giants; g0 += max_giants) {
+      BsgsParams P;
+      for (int t = 0; t < n_terms; ++t) P.baby[t] = babies[t] + b0 * bstride;
+      P.n_terms = n_terms;
+      P.n_giants = n_giants - g0 < max_giants ? n_giants - g0 : max_giants;
+      P.n_batch = nb;
+      P.log_n = log_n;
+      P.c1_off = c1_off;
+      P.bstride = bstride;
+      P.pt_base = pt_base;
+      P.pt_stride = pt_stride;
+      P.pt_idx = pt_idx + (size_t)g0 * n_terms;
+      P.out = out + (size_t)g0 * out_gstride + b0 * bstride;
+      P.out_gstride = out_gstride;
+      P.pc = dpc;
+      const double el = (double)k * (1 << log_n);
+      ProfScope ps(PROF_DIAG_MAC, st,
+                   el * 8.0 * ((double)P.n_giants * n_terms + 2.0 * nb * (n_terms + P.n_giants)),
+                   el * 2.0 * nb * ((double)P.n_giants * n_terms + P.n_giants));
+      if (nb == 1)
+        launch_bsgs_nb<1>(P, k, st);
+      else
+        launch_bsgs_nb<2>(P, k, st);
+      check_cuda(cudaGetLastError(), "bsgs launch");
+    }
+  }
 }
 
 }  // namespace hegpu

@@ -19,6 +19,7 @@
 // N = 2^16 is 16 tiles, so every launch has (16 x limbs x polys) CTAs.
 // Intermediate values stay in Harvey lazy ranges ([0,4q) forward, [0,2q)
 // inverse); outputs are fully reduced.
+#include "ntt_reg.cuh"
 #include "ring.cuh"
 
 namespace hegpu {
@@ -199,6 +200,168 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
   }
 }
 
+// ---------------------------------------------------------------------------
+// register-radix passes (N >= 2^12): one warp per S-point sub-transform
+// ---------------------------------------------------------------------------
+
+constexpr int kRegWarps = 8;
+
+template <int LOGS, bool INV>
+__global__ void __launch_bounds__(256) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+  using Sh = RegShape<LOGS>;
+  constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
+  constexpr int TS = kRegWarps + 1;  // padded tile row (conflict-free column reads)
+  extern __shared__ uint64_t sm[];
+  const int log_n = P.log_n, N = 1 << log_n, C = N >> LOGS;
+  const int row = blockIdx.y;
+  const int s = find_seg(P.S, row);
+  const Seg& sg = P.S.seg[s];
+  const int rr = row - sg.row_start;
+  const int poly = rr / sg.k, limb = rr - poly * sg.k;
+  const int prime = P.S.sel[s][limb];
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
+  const uint64_t* wsh = w + N;
+  const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
+                            : (sg.in + poly * sg.in_stride + (size_t)limb * N);
+  uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
+  uint64_t* tile = sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
+  const int c0 = blockIdx.x * kRegWarps;
+  for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+    const int r = e / kRegWarps, c = e % kRegWarps;
+    tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+  }
+  __syncthreads();
+  constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
+  uint64_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
+  if (!INV)
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, w, wsh, pc.q);
+  else
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, w, wsh, pc);
+#pragma unroll
+  for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+    const int r = e / kRegWarps, c = e % kRegWarps;
+    dst[c0 + c + (size_t)C * r] = tile[r * TS + c];
+  }
+}
+
+template <int LOGS, bool INV>
+__global__ void __launch_bounds__(256) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+  using Sh = RegShape<LOGS>;
+  constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
+  extern __shared__ uint64_t sm[];
+  const int log_n = P.log_n, N = 1 << log_n, a = log_n - LOGS;
+  const int row = blockIdx.y;
+  const int s = find_seg(P.S, row);
+  const Seg& sg = P.S.seg[s];
+  const int rr = row - sg.row_start;
+  const int poly = rr / sg.k, limb = rr - poly * sg.k;
+  const int prime = P.S.sel[s][limb];
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t q = pc.q, q2 = q << 1;
+  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
+  const uint64_t* wsh = w + N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * kRegWarps + warp;
+  const size_t off = (size_t)limb * N + (size_t)blk * S;
+  const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + off)
+                            : (sg.out + poly * sg.out_stride + off);
+  uint64_t* dst = sg.out + poly * sg.out_stride + off;
+  uint64_t* wbuf = sm + warp * Sh::PAD_S;
+  constexpr int LO_S = LOGS - EB;
+  uint64_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
+  if (!INV) {
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, a, blk, w, wsh, q);
+    if (P.epi) {
+      const uint64_t* other = sg.other + poly * sg.other_stride + off;
+      uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
+      const uint64_t cc = P.c[limb], ccsh = P.csh[limb];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        uint64_t y = x[e];
+        y = y >= q2 ? y - q2 : y;
+        y = y >= q ? y - q : y;
+        eout[lane + 32 * e] = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
+      }
+      return;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      uint64_t y = x[e];
+      y = y >= q2 ? y - q2 : y;
+      dst[lane + 32 * e] = y >= q ? y - q : y;
+    }
+  } else {
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, w, wsh, pc);
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
+  }
+}
+
+template <int LOGS>
+static void launch_cols_r(bool inverse, const NttParams& P, int n_rows, int log_n,
+                          cudaStream_t st) {
+  const int C = (1 << log_n) >> LOGS;
+  dim3 grid(C / kRegWarps, n_rows);
+  const size_t smem = ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8;
+  static bool attr_set = false;  // opt in to > 48 KiB dynamic shared memory once
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    attr_set = true;
+  }
+  if (inverse)
+    k_ntt_cols_r<LOGS, true><<<grid, 32 * kRegWarps, smem, st>>>(P);
+  else
+    k_ntt_cols_r<LOGS, false><<<grid, 32 * kRegWarps, smem, st>>>(P);
+}
+
+template <int LOGS>
+static void launch_blocks_r(bool inverse, const NttParams& P, int n_rows, int log_n,
+                            cudaStream_t st) {
+  const int R = (1 << log_n) >> LOGS;
+  dim3 grid(R / kRegWarps, n_rows);
+  const size_t smem = (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8;
+  if (inverse)
+    k_ntt_blocks_r<LOGS, true><<<grid, 32 * kRegWarps, smem, st>>>(P);
+  else
+    k_ntt_blocks_r<LOGS, false><<<grid, 32 * kRegWarps, smem, st>>>(P);
+}
+
+static void cols_r(int logs, bool inverse, const NttParams& P, int n_rows, int log_n,
+                   cudaStream_t st) {
+  switch (logs) {
+    case 6: launch_cols_r<6>(inverse, P, n_rows, log_n, st); break;
+    case 7: launch_cols_r<7>(inverse, P, n_rows, log_n, st); break;
+    case 8: launch_cols_r<8>(inverse, P, n_rows, log_n, st); break;
+    case 9: launch_cols_r<9>(inverse, P, n_rows, log_n, st); break;
+    default: throw HegpuError{HEGPU_E_ARG, "unsupported NTT column size"};
+  }
+}
+
+static void blocks_r(int logs, bool inverse, const NttParams& P, int n_rows, int log_n,
+                     cudaStream_t st) {
+  switch (logs) {
+    case 6: launch_blocks_r<6>(inverse, P, n_rows, log_n, st); break;
+    case 7: launch_blocks_r<7>(inverse, P, n_rows, log_n, st); break;
+    case 8: launch_blocks_r<8>(inverse, P, n_rows, log_n, st); break;
+    case 9: launch_blocks_r<9>(inverse, P, n_rows, log_n, st); break;
+    default: throw HegpuError{HEGPU_E_ARG, "unsupported NTT block size"};
+  }
+}
+
 static inline bool P_epi_guard(const NttEpilogue* e) { return e && e->enabled; }
 
 static inline int ilog2(int x) {
@@ -244,6 +407,27 @@ void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inve
   const double mm_b = rows * nn / 2 * (log_n - a) + ((P_epi_guard(epi)) ? rows * nn : 0.0);
   pa.tile_log = ilog2(cpb);
   pb.tile_log = ilog2(bpc);
+  if (log_n >= 12) {
+    const int logs_b = log_n - a;
+    if (!inverse) {
+      pa.epi = 0;
+      {
+        ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
+        cols_r(a, false, pa, S.n_rows, log_n, st);
+      }
+      ProfScope ps(PROF_NTT, st, bytes_pass * (P_epi_guard(epi) ? 1.5 : 1.0), mm_b);
+      blocks_r(logs_b, false, pb, S.n_rows, log_n, st);
+    } else {
+      {
+        ProfScope ps(PROF_NTT, st, bytes_pass, rows * nn / 2 * (log_n - a));
+        blocks_r(logs_b, true, pb, S.n_rows, log_n, st);
+      }
+      ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
+      cols_r(a, true, pa, S.n_rows, log_n, st);
+    }
+    check_cuda(cudaGetLastError(), "ntt launch");
+    return;
+  }
   if (!inverse) {
     pa.epi = 0;
     {

@@ -876,6 +876,18 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
   })
 }
 
+int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
+               int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
+               const int32_t* pt_idx, int n_giants, uint64_t* out, int64_t out_gstride, int k,
+               void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    launch_bsgs(R.dpc, R.log_n, babies, n_terms, c1_off, bstride, n_batch, pt_base, pt_stride,
+                pt_idx, n_giants, out, out_gstride, k, S_(stream));
+  })
+}
+
 // --- host-array kernel table -----------------------------------------------
 
 int hegpu_k_ntt_forward_inplace(uint64_t* a, int k, int n, const uint64_t* psi_rev,

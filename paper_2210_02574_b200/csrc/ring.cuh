@@ -201,5 +201,9 @@ void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct
                      int64_t out_bstride, int k, int accumulate, cudaStream_t st);
 void launch_ks_ip(IpParams& P, cudaStream_t st);
 double bench_modmul_peak(int iters);
+void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
+                 int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
+                 int64_t pt_stride, const int32_t* pt_idx, int n_giants, uint64_t* out,
+                 int64_t out_gstride, int k, cudaStream_t st);
 
 }  // namespace hegpu
