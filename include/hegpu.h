@@ -156,6 +156,20 @@ int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
                    const uint64_t* const* key_a, int n_digits, uint64_t* out_b,
                    uint64_t* out_a, int64_t out_stride, void* stream);
 
+/* Hoisted rotations of one (batched) ciphertext by n_rot Galois elements
+ * (the bootstrap baby steps, bootstrap.py:214-217): ModUp of c1 once, then
+ * per rotation r a digit permutation, the inner product with rotation key r
+ * (key_b/key_a: host arrays of n_rot*n_digits device pointers, rotation-major)
+ * and ModDown; outs[r] (host array of device pointers) receives the packed
+ * rotated ciphertexts (c0 at outs[r] + b*cs, c1 at +c1_off).  Input c0 at
+ * c + b*cs, c1 at c + b*cs + c1_off.  Decrypts like the unhoisted rotation;
+ * limbs are not bit-identical to it (the digit lift commutes with the
+ * automorphism only up to a multiple of the digit modulus). */
+int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
+                     int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
+                     const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                     uint64_t* const* outs, void* stream);
+
 /* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
  * limbs (eval form), out gets `level` limbs.  in may equal out. */
 int hegpu_rescale(hegpu_ring_t ring, int level, const uint64_t* in, int64_t in_stride,

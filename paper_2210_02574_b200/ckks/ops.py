@@ -593,6 +593,54 @@ def rotate(ct, step, keyset):
     return ct
 
 
+def rotate_hoisted(ct, steps, keyset):
+    """Rotations of one (batched) ciphertext by several keyed steps sharing
+    one ModUp of c1 (hoisting).  Each output decrypts like `rotate(ct, s)`;
+    its limbs are not bit-identical to it (see hegpu_ks_hoisted), so the
+    public `rotate` keeps the reference's per-rotation key switch.  Used for
+    the bootstrap's baby steps.  Step 0 returns ct itself."""
+    import ctypes
+
+    params = ct.params
+    n = params.ring_degree
+    k = ct.level + 1
+    out = {}
+    todo = []
+    for s in steps:
+        s = int(s) % ct.slot_count
+        if s == 0:
+            out[0] = ct
+        elif s in keyset.rotation_keys or s - ct.slot_count in keyset.rotation_keys:
+            todo.append(s)
+        else:
+            out[s] = rotate(ct, s, keyset)
+    if not todo:
+        return [out[int(s) % ct.slot_count] for s in steps]
+    src = ct if _pair_group(ct) is not None else ct.copy()
+    cnt = 1 if src.batch is None else src.batch
+    keys = [keysmod.rotation_key_for(keyset, s if s in keyset.rotation_keys else s - ct.slot_count)
+            for s in todo]
+    dnum = keys[0].dnum
+    gal = np.array([keysmod.galois_exponent_for_step(params, s) % (2 * n) for s in todo],
+                   dtype=np.uint64)
+    kb = (ctypes.c_void_p * (len(todo) * dnum))(
+        *[kk.b[j].data_ptr() for kk in keys for j in range(dnum)])
+    ka = (ctypes.c_void_p * (len(todo) * dnum))(
+        *[kk.a[j].data_ptr() for kk in keys for j in range(dnum)])
+    outs = [_packed(params, _lead(ct), ct.level) for _ in todo]
+    optr = (ctypes.c_void_p * len(todo))(*[o.data_ptr() for o in outs])
+    for _ in todo:
+        _stats.count("ks", ct.level, cnt)
+    _lib.call(
+        "hegpu_ks_hoisted", params.ring.device(), ct.level, params.digit_size,
+        src.c0.data.data_ptr(), 2 * k * n, k * n, cnt, len(todo), gal.ctypes.data, kb, ka, dnum,
+        optr, _dev.stream(),
+    )
+    for s, o in zip(todo, outs):
+        out[s] = _ct(o, ct.level, ct.scale, ct.slot_count, params, ct.insecure_provenance)
+    return [out[int(s) % ct.slot_count] for s in steps]
+
+
 def conjugate(ct, keyset):
     if keyset.conj_key is None:
         raise CryptoError("key set has no conjugation key")

@@ -348,23 +348,14 @@ static void ntt_simple(Ring& R, bool inverse, const uint64_t* in, int64_t is, ui
 
 // --- hybrid key switching (keys.py:278-339) --------------------------------
 
-static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds, int B,
-                          const uint64_t* const* key_b, const uint64_t* const* key_a,
-                          int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t os,
-                          cudaStream_t st) {
-  if (B <= 0) return;
-  const KsLevel& L = R.ks_level(level, alpha);
-  const int k = level + 1, K = R.n_special, n_ext = L.n_ext, beta = L.beta;
+// ModUp (keys.py:290-313): d (B eval-form polys of level+1 limbs) -> the
+// converted rows of every digit, NTT'd, in the compact layout
+// ext[b][j][t][N] (t < n_ext - |group j|).  dcoeff: B*(level+1)*N scratch.
+static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, int B,
+                     uint64_t* dcoeff, uint64_t* ext, cudaStream_t st) {
+  const int level = L.level, alpha = L.alpha;
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
-  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
-  if (beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many digits"};
-  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
-  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
-  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
-  uint64_t* dcoeff = ws.u64();
-  uint64_t* ext = dcoeff + sz_dc;
-  uint64_t* acc = ext + sz_ext;
-  uint64_t* corr = acc + sz_acc;
   const std::vector<int32_t> chain = range_primes(0, k);
   // 1. d -> coefficient form
   ntt_simple(R, true, d, ds, dcoeff, (int64_t)k * N, B, k, chain.data(), st);
@@ -406,6 +397,20 @@ static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int6
     launch_conv(C, st);
     launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
   }
+}
+
+// Key inner product (keys.py:316-323) and ModDown (keys.py:325-338).  d / ext
+// are the digit sources (own rows from d, converted rows from ext).
+static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
+                      const uint64_t* ext, int B, const uint64_t* const* key_b,
+                      const uint64_t* const* key_a, uint64_t* acc, uint64_t* corr,
+                      uint64_t* out_b, int64_t os_b, uint64_t* out_a, int64_t os_a,
+                      cudaStream_t st) {
+  const int level = L.level, alpha = L.alpha;
+  const int k = level + 1, K = R.n_special, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  const size_t sz_corr = (size_t)B * 2 * k * N;
+  const std::vector<int32_t> chain = range_primes(0, k);
   // 4. inner product with the key digits
   IpParams P;
   P.d = d;
@@ -465,11 +470,11 @@ static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int6
   S.seg[0].other = acc;
   S.seg[0].other_stride = (int64_t)2 * n_ext * N;
   S.seg[0].eout = out_b;
-  S.seg[0].eout_stride = os;
+  S.seg[0].eout_stride = os_b;
   S.seg[1].other = acc + (size_t)n_ext * N;
   S.seg[1].other_stride = (int64_t)2 * n_ext * N;
   S.seg[1].eout = out_a;
-  S.seg[1].eout_stride = os;
+  S.seg[1].eout_stride = os_a;
   NttEpilogue E;
   E.enabled = true;
   for (int t = 0; t < k; ++t) {
@@ -477,6 +482,76 @@ static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int6
     E.csh[t] = L.pinv_sh[t];
   }
   launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+}
+
+
+static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds, int B,
+                          const uint64_t* const* key_b, const uint64_t* const* key_a,
+                          int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t os,
+                          cudaStream_t st) {
+  if (B <= 0) return;
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many digits"};
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  ks_modup(R, L, d, ds, B, dcoeff, ext, st);
+  ks_ipdown(R, L, d, ds, ext, B, key_b, key_a, acc, corr, out_b, os, out_a, os, st);
+}
+
+// Hoisted rotations (bootstrap baby steps): ModUp of c1 once, then per
+// rotation r: permute the digits by X -> X^g[r] (eval-form slot gather),
+// inner product with rotation key r, ModDown, and c0' = sigma(c0) + b.
+// sigma commutes with the RNS digit decomposition up to the usual
+// fast-conversion error (a multiple of the digit modulus), so each output
+// decrypts exactly like the unhoisted rotation; limbs differ from it.
+// c: B packed ciphertexts at `level` (c0 at c + b*cs, c1 at +c1_off);
+// outs[r]: packed output ciphertexts with the same layout.
+static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, int64_t cs,
+                            int64_t c1_off, int B, int n_rot, const uint64_t* galois,
+                            const uint64_t* const* key_b, const uint64_t* const* key_a,
+                            int n_digits, uint64_t* const* outs, cudaStream_t st) {
+  if (B <= 0 || n_rot <= 0) return;
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  const size_t sz_kb = (size_t)B * k * N;
+  Scratch ws((sz_dc + 2 * sz_ext + sz_acc + sz_corr + 2 * sz_kb) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* extp = ext + sz_ext;
+  uint64_t* acc = extp + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  uint64_t* dp = corr + sz_corr;
+  uint64_t* kb = dp + sz_kb;
+  const uint64_t* c1 = c + c1_off;
+  ks_modup(R, L, c1, cs, B, dcoeff, ext, st);
+  const std::vector<int32_t> chain = range_primes(0, k);
+  const std::vector<int32_t> rows = range_primes(0, n_ext);
+  for (int r = 0; r < n_rot; ++r) {
+    launch_automorphism(R.dpc, R.log_n, true, galois[r], c1, cs, dp, (int64_t)k * N, B, k,
+                        chain.data(), st);
+    launch_automorphism(R.dpc, R.log_n, true, galois[r], ext, (int64_t)n_ext * N, extp,
+                        (int64_t)n_ext * N, B * beta, n_ext, rows.data(), st);
+    uint64_t* out = outs[r];
+    ks_ipdown(R, L, dp, (int64_t)k * N, extp, B, key_b + (size_t)r * n_digits,
+              key_a + (size_t)r * n_digits, acc, corr, kb, (int64_t)k * N, out + c1_off, cs,
+              st);
+    // c0' = sigma(c0) + kb
+    launch_automorphism(R.dpc, R.log_n, true, galois[r], c, cs, out, cs, B, k, chain.data(), st);
+    EwArgs A{HEGPU_OP_ADD, out, cs, kb, (int64_t)k * N, out, cs, B, k, chain.data(), nullptr};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
+  }
 }
 
 // --- rescale (ops.py:164-189) and ModRaise (bootstrap.py:260-275) ----------
@@ -825,6 +900,17 @@ int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d, i
     Ring& R = RR(ring);
     ks_apply_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, out_b, out_a,
                   out_stride, S_(stream));
+  })
+}
+
+int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
+                     int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
+                     const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                     uint64_t* const* outs, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    ks_hoisted_impl(R, level, alpha, c, cs, c1_off, n_batch, n_rot, galois, key_b, key_a,
+                    n_digits, outs, S_(stream));
   })
 }
 

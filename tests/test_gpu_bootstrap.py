@@ -111,3 +111,23 @@ def test_debug_refresh_flags():
         bs.debug_refresh(ct, keys.public_only(), enabled=True)
     with pytest.raises(InsecureDebugError):
         bs.DebugRefresher(keys)
+
+
+def test_hoisted_rotations_decrypt_like_rotate(boot):
+    """Hoisted baby-step rotations (one shared ModUp) decrypt to the same
+    slots as the reference's per-rotation key switch."""
+    from paper_2210_02574_b200.ckks import ops
+
+    params, ctx, keys, _ = boot
+    v = np.random.default_rng(8).uniform(-1, 1, params.slot_count)
+    ct = ckks.encrypt_vector(params, v, keys, rng_seed=3)
+    steps = [0, 1, 2, 3, 5]
+    hoisted = ops.rotate_hoisted(ct, steps, keys)
+    for s, h in zip(steps, hoisted):
+        want = ckks.decrypt_vector(ckks.rotate(ct, s, keys), keys)
+        got = ckks.decrypt_vector(h, keys)
+        assert np.max(np.abs(got - want)) < 1e-6
+        assert np.max(np.abs(got - np.roll(v, -s))) < 1e-3
+    batch = ops.stack([ct, ckks.encrypt_vector(params, -v, keys, rng_seed=4)])
+    hb = ops.rotate_hoisted(batch, [1, 2], keys)
+    assert np.max(np.abs(ckks.decrypt_vector(hb[1][1], keys) - np.roll(-v, -2))) < 1e-3
