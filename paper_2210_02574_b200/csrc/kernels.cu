@@ -753,9 +753,7 @@ namespace hegpu {
 // diagonal, every baby and every output is touched exactly once (the per-giant
 // formulation re-reads all babies once per giant).
 // ---------------------------------------------------------------------------
-constexpr int kBsgsTX = 32;
 constexpr int kBsgsMaxTerms = 64;
-constexpr int kBsgsGroups = kEwThreads / kBsgsTX;  // 8 giant groups per CTA
 
 struct BsgsParams {
   const uint64_t* baby[kBsgsMaxTerms];
@@ -769,78 +767,108 @@ struct BsgsParams {
   const PrimeConst* pc;
 };
 
+// CTA = 16 warps over a 64-coefficient tile of one limb (2 coefficients per
+// lane, 128-bit loads).  The tile of every baby is staged in shared memory
+// once; warp w accumulates giants w, w+16, ... (GPT of them); the giant x term
+// index table is staged too.  The term loop is unrolled by 2 so each lane
+// keeps 2*GPT independent 16-byte diagonal loads in flight.
+constexpr int kBsgsWarps = 16;
+constexpr int kBsgsTile = 64;
+
 template <int NB, int GPT>
-__global__ void __launch_bounds__(kEwThreads) k_bsgs(const __grid_constant__ BsgsParams P) {
-  extern __shared__ uint64_t sm[];  // [n_terms][NB][2][TX]
+__global__ void __launch_bounds__(kBsgsWarps * 32) k_bsgs(const __grid_constant__ BsgsParams P) {
+  extern __shared__ uint64_t sm[];  // babies [n_terms][NB][2][64], then idx [n_giants][n_terms]
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
-  const int x0 = blockIdx.x * kBsgsTX;
+  const int x0 = blockIdx.x * kBsgsTile;
   const PrimeConst pc = P.pc[limb];
-  const int per_term = NB * 2 * kBsgsTX;
-  for (int e = threadIdx.x; e < P.n_terms * per_term; e += blockDim.x) {
-    const int t = e / per_term;
-    const int rem = e - t * per_term;
-    const int b = rem / (2 * kBsgsTX);
-    const int c = (rem / kBsgsTX) & 1;
-    const int xi = rem % kBsgsTX;
-    sm[e] = P.baby[t][b * P.bstride + c * P.c1_off + (size_t)limb * N + x0 + xi];
+  constexpr int per_term = NB * 2 * kBsgsTile;
+  int32_t* s_idx = reinterpret_cast<int32_t*>(sm + (size_t)P.n_terms * per_term);
+  const int nthr = kBsgsWarps * 32;
+  for (int e = threadIdx.x; e < P.n_terms * per_term / 2; e += nthr) {
+    const int e2 = e * 2;
+    const int t = e2 / per_term;
+    const int rem = e2 - t * per_term;
+    const int b = rem / (2 * kBsgsTile);
+    const int c = (rem / kBsgsTile) & 1;
+    const int xi = rem % kBsgsTile;
+    *reinterpret_cast<ulonglong2*>(sm + e2) = __ldg(reinterpret_cast<const ulonglong2*>(
+        P.baby[t] + b * P.bstride + c * P.c1_off + (size_t)limb * N + x0 + xi));
   }
+  for (int e = threadIdx.x; e < P.n_giants * P.n_terms; e += nthr) s_idx[e] = __ldg(P.pt_idx + e);
   __syncthreads();
-  const int xi = threadIdx.x % kBsgsTX;
-  const int grp = threadIdx.x / kBsgsTX;
-  Acc2 acc[GPT][NB][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int xi = lane * 2;
+  const size_t coef = (size_t)limb * N + x0 + xi;
+  Acc2 acc[GPT][NB][2][2];
 #pragma unroll
   for (int gg = 0; gg < GPT; ++gg)
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      acc[gg][b][0].zero();
-      acc[gg][b][1].zero();
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        acc[gg][b][c][0].zero();
+        acc[gg][b][c][1].zero();
+      }
+  for (int t0 = 0; t0 < P.n_terms; t0 += 2) {
+    ulonglong2 pv[2][GPT];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int gg = 0; gg < GPT; ++gg) {
+        const int g = warp + gg * kBsgsWarps;
+        const int t = t0 + u;
+        const int idx = (g < P.n_giants && t < P.n_terms) ? s_idx[g * P.n_terms + t] : -1;
+        pv[u][gg] = idx >= 0 ? __ldg(reinterpret_cast<const ulonglong2*>(
+                                   P.pt_base + (size_t)idx * P.pt_stride + coef))
+                             : make_ulonglong2(0, 0);
+      }
     }
-  const size_t coef = (size_t)limb * N + x0 + xi;
-  for (int t = 0; t < P.n_terms; ++t) {
-    uint64_t bv[NB][2];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      bv[b][0] = sm[t * per_term + b * 2 * kBsgsTX + xi];
-      bv[b][1] = sm[t * per_term + b * 2 * kBsgsTX + kBsgsTX + xi];
-    }
+    for (int u = 0; u < 2; ++u) {
+      const int t = t0 + u;
+      if (t >= P.n_terms) break;
 #pragma unroll
-    for (int gg = 0; gg < GPT; ++gg) {
-      const int g = grp * GPT + gg;
-      if (g < P.n_giants) {
-        const int idx = __ldg(P.pt_idx + g * P.n_terms + t);
-        if (idx >= 0) {
-          const uint64_t p = __ldg(P.pt_base + (size_t)idx * P.pt_stride + coef);
+      for (int b = 0; b < NB; ++b) {
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            acc[gg][b][0].add(bv[b][0], p);
-            acc[gg][b][1].add(bv[b][1], p);
+        for (int c = 0; c < 2; ++c) {
+          const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(
+              sm + t * per_term + b * 2 * kBsgsTile + c * kBsgsTile + xi);
+#pragma unroll
+          for (int gg = 0; gg < GPT; ++gg) {
+            acc[gg][b][c][0].add(bv.x, pv[u][gg].x);
+            acc[gg][b][c][1].add(bv.y, pv[u][gg].y);
           }
         }
       }
     }
-    if (t & 1) {
 #pragma unroll
-      for (int gg = 0; gg < GPT; ++gg)
+    for (int gg = 0; gg < GPT; ++gg)
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          acc[gg][b][0].fold(pc.q);
-          acc[gg][b][1].fold(pc.q);
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          acc[gg][b][c][0].fold(pc.q);
+          acc[gg][b][c][1].fold(pc.q);
         }
-    }
   }
 #pragma unroll
   for (int gg = 0; gg < GPT; ++gg) {
-    const int g = grp * GPT + gg;
+    const int g = warp + gg * kBsgsWarps;
     if (g >= P.n_giants) continue;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        Acc2 a = acc[gg][b][c];
-        a.fold(pc.q);
-        P.out[g * P.out_gstride + b * P.bstride + c * P.c1_off + coef] =
-            mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+        uint64_t r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          Acc2 a = acc[gg][b][c][h];
+          a.fold(pc.q);
+          r[h] = mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+        }
+        *reinterpret_cast<ulonglong2*>(P.out + g * P.out_gstride + b * P.bstride +
+                                       c * P.c1_off + coef) = make_ulonglong2(r[0], r[1]);
       }
     }
   }
@@ -848,20 +876,19 @@ __global__ void __launch_bounds__(kEwThreads) k_bsgs(const __grid_constant__ Bsg
 
 template <int NB>
 static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
-  const int gpt_need = (P.n_giants + kBsgsGroups - 1) / kBsgsGroups;
-  dim3 grid((1 << P.log_n) / kBsgsTX, k);
-  const size_t smem = (size_t)P.n_terms * NB * 2 * kBsgsTX * 8;
+  const int gpt_need = (P.n_giants + kBsgsWarps - 1) / kBsgsWarps;
+  dim3 grid((1 << P.log_n) / kBsgsTile, k);
+  const size_t smem = (size_t)P.n_terms * NB * 2 * kBsgsTile * 8 +
+                      (size_t)P.n_giants * P.n_terms * 4;
   static bool attr = false;
   if (!attr) {
-    const int mx = 200 * 1024;
+    const int mx = 220 * 1024;
     cudaFuncSetAttribute(k_bsgs<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_bsgs<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_bsgs<NB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     attr = true;
   }
-  if (gpt_need <= 1) k_bsgs<NB, 1><<<grid, kEwThreads, smem, st>>>(P);
-  else if (gpt_need <= 2) k_bsgs<NB, 2><<<grid, kEwThreads, smem, st>>>(P);
-  else k_bsgs<NB, 4><<<grid, kEwThreads, smem, st>>>(P);
+  if (gpt_need <= 1) k_bsgs<NB, 1><<<grid, kBsgsWarps * 32, smem, st>>>(P);
+  else k_bsgs<NB, 2><<<grid, kBsgsWarps * 32, smem, st>>>(P);
 }
 
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
@@ -869,8 +896,8 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                  int64_t pt_stride, const int32_t* pt_idx, int n_giants, uint64_t* out,
                  int64_t out_gstride, int k, cudaStream_t st) {
   if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
-  if ((1 << log_n) % kBsgsTX) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
-  const int max_giants = kBsgsGroups * 4;
+  if ((1 << log_n) % kBsgsTile) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
+  const int max_giants = kBsgsWarps * 2;
   for (int b0 = 0; b0 < n_batch; b0 += 2) {
     const int nb = n_batch - b0 < 2 ? n_batch - b0 : 2;
     for (int g0 = 0; g0 < n_giants; g0 += max_giants) {
