@@ -78,8 +78,9 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
 int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain,
                       const uint64_t* special, int n_special, hegpu_ring_t* out);
 int hegpu_ring_destroy(hegpu_ring_t ring);
-/* Copy the device twiddle tables of global prime p to host (4 arrays of N:
- * psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup; natural form). */
+/* Copy the device twiddle tables of global prime p to host: 4N words,
+ * interleaved (psi_rev[i], shoup(psi_rev[i])) pairs for i < N, then
+ * (ipsi_rev[i], shoup(ipsi_rev[i])); natural form, bit-reversed order. */
 int hegpu_ring_get_tables(hegpu_ring_t ring, int p, uint64_t* host_out4n);
 
 /* -------------------------------------------------------------------------

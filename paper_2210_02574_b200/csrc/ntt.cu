@@ -49,8 +49,9 @@ __global__ void __launch_bounds__(256) k_ntt_cols(const __grid_constant__ NttPar
   const int prime = P.S.sel[s][limb];
   const PrimeConst pc = P.pc[prime];
   const uint64_t q = pc.q, q2 = q << 1;
-  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
-  const uint64_t* wsh = w + N;
+  // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
+  const ulonglong2* tw =
+      reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
   const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
                             : (sg.in + poly * sg.in_stride + (size_t)limb * N);
   uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(256) k_ntt_cols(const __grid_constant__ NttPar
         uint64_t x = sm[i0];
         const uint64_t y = sm[i1];
         x = x >= q2 ? x - q2 : x;
-        const uint64_t v = shoup_lazy(y, w[ti], wsh[ti], q);
+        const ulonglong2 wp = tw[ti];
+        const uint64_t v = shoup_lazy(y, wp.x, wp.y, q);
         sm[i0] = x + v;
         sm[i1] = x - v + q2;
       }
@@ -100,7 +102,8 @@ __global__ void __launch_bounds__(256) k_ntt_cols(const __grid_constant__ NttPar
         if (!last) {
           const int ti = h + grp;
           sm[i0] = sum;
-          sm[i1] = shoup_lazy(d, w[ti], wsh[ti], q);
+          const ulonglong2 wp = tw[ti];
+          sm[i1] = shoup_lazy(d, wp.x, wp.y, q);
         } else {
           sm[i0] = shoup(sum, pc.ninv, pc.ninv_sh, q);
           sm[i1] = shoup(d, pc.ilast, pc.ilast_sh, q);
@@ -129,8 +132,9 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
   const int prime = P.S.sel[s][limb];
   const PrimeConst pc = P.pc[prime];
   const uint64_t q = pc.q, q2 = q << 1;
-  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
-  const uint64_t* wsh = w + N;
+  // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
+  const ulonglong2* tw =
+      reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
   const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + (size_t)limb * N)
                             : (sg.out + poly * sg.out_stride + (size_t)limb * N);
   uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
@@ -154,7 +158,8 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
         uint64_t x = sm[i0];
         const uint64_t y = sm[i1];
         x = x >= q2 ? x - q2 : x;
-        const uint64_t v = shoup_lazy(y, w[ti], wsh[ti], q);
+        const ulonglong2 wp = tw[ti];
+        const uint64_t v = shoup_lazy(y, wp.x, wp.y, q);
         sm[i0] = x + v;
         sm[i1] = x - v + q2;
       }
@@ -192,7 +197,8 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
         uint64_t sum = x + y;
         sum = sum >= q2 ? sum - q2 : sum;
         sm[i0] = sum;
-        sm[i1] = shoup_lazy(x - y + q2, w[ti], wsh[ti], q);
+        const ulonglong2 wp = tw[ti];
+        sm[i1] = shoup_lazy(x - y + q2, wp.x, wp.y, q);
       }
       __syncthreads();
     }
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
 constexpr int kRegWarps = 8;
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   constexpr int TS = kRegWarps + 1;  // padded tile row (conflict-free column reads)
@@ -220,8 +226,9 @@ __global__ void __launch_bounds__(256) k_ntt_cols_r(const __grid_constant__ NttP
   const int poly = rr / sg.k, limb = rr - poly * sg.k;
   const int prime = P.S.sel[s][limb];
   const PrimeConst pc = P.pc[prime];
-  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
-  const uint64_t* wsh = w + N;
+  // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
+  const ulonglong2* tw =
+      reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
   const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
                             : (sg.in + poly * sg.in_stride + (size_t)limb * N);
   uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
@@ -239,9 +246,9 @@ __global__ void __launch_bounds__(256) k_ntt_cols_r(const __grid_constant__ NttP
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
   if (!INV)
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, w, wsh, pc.q);
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, tw, pc.q);
   else
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, w, wsh, pc);
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, tw, pc);
 #pragma unroll
   for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
   __syncthreads();
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(256) k_ntt_cols_r(const __grid_constant__ NttP
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
@@ -265,8 +272,9 @@ __global__ void __launch_bounds__(256) k_ntt_blocks_r(const __grid_constant__ Nt
   const int prime = P.S.sel[s][limb];
   const PrimeConst pc = P.pc[prime];
   const uint64_t q = pc.q, q2 = q << 1;
-  const uint64_t* w = P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0);
-  const uint64_t* wsh = w + N;
+  // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
+  const ulonglong2* tw =
+      reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x * kRegWarps + warp;
   const size_t off = (size_t)limb * N + (size_t)blk * S;
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(256) k_ntt_blocks_r(const __grid_constant__ Nt
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
   if (!INV) {
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, a, blk, w, wsh, q);
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, a, blk, tw, q);
     if (P.epi) {
       const uint64_t* other = sg.other + poly * sg.other_stride + off;
       uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(256) k_ntt_blocks_r(const __grid_constant__ Nt
       dst[lane + 32 * e] = y >= q ? y - q : y;
     }
   } else {
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, w, wsh, pc);
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, tw, pc);
 #pragma unroll
     for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
   }

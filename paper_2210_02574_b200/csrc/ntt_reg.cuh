@@ -38,8 +38,7 @@ __device__ __forceinline__ int padi(int j) { return j + (j >> 4); }
 template <int LOGS>
 __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
                                           int phi, int plo, int g0, int blk,
-                                          const uint64_t* __restrict__ w,
-                                          const uint64_t* __restrict__ wsh, uint64_t q) {
+                                          const ulonglong2* __restrict__ tw, uint64_t q) {
   constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
   const uint64_t q2 = q << 1;
 #pragma unroll
@@ -55,7 +54,8 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
       const int ti = base + (j >> (p + 1));
       uint64_t u = x[e];
       u = u >= q2 ? u - q2 : u;
-      const uint64_t v = shoup_lazy(x[e + d], __ldg(w + ti), __ldg(wsh + ti), q);
+      const ulonglong2 wp = __ldg(tw + ti);
+      const uint64_t v = shoup_lazy(x[e + d], wp.x, wp.y, q);
       x[e] = u + v;
       x[e + d] = u - v + q2;
     }
@@ -69,8 +69,7 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
 template <int LOGS>
 __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
                                           int plo, int phi, int log_n, int gshift, int blk,
-                                          const uint64_t* __restrict__ w,
-                                          const uint64_t* __restrict__ wsh,
+                                          const ulonglong2* __restrict__ tw,
                                           const PrimeConst& pc) {
   constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
   const uint64_t q = pc.q, q2 = q << 1;
@@ -91,7 +90,8 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
         const int j = reg_j(lane, e, lo, EB);
         const int ti = base + (j >> (p + 1));
         x[e] = s;
-        x[e + d] = shoup_lazy(df, __ldg(w + ti), __ldg(wsh + ti), q);
+        const ulonglong2 wp = __ldg(tw + ti);
+        x[e + d] = shoup_lazy(df, wp.x, wp.y, q);
       } else {
         x[e] = shoup(s, pc.ninv, pc.ninv_sh, q);
         x[e + d] = shoup(df, pc.ilast, pc.ilast_sh, q);
@@ -119,7 +119,7 @@ __device__ __forceinline__ void reg_shuffle(uint64_t (&x)[RegShape<LOGS>::E], ui
 template <int LOGS>
 __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
                                         int lane, int lo_in, int lo_out, int g0, int blk,
-                                        const uint64_t* w, const uint64_t* wsh, uint64_t q) {
+                                        const ulonglong2* tw, uint64_t q) {
   constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
   int cur = lo_in;
 #pragma unroll
@@ -129,7 +129,7 @@ __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
     const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
     reg_shuffle<LOGS>(x, buf, lane, cur, lo);
     cur = lo;
-    fwd_round<LOGS>(x, lane, lo, phi, plo, g0, blk, w, wsh, q);
+    fwd_round<LOGS>(x, lane, lo, phi, plo, g0, blk, tw, q);
   }
   reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
 }
@@ -137,8 +137,7 @@ __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
 template <int LOGS>
 __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
                                         int lane, int lo_in, int lo_out, int log_n, int gshift,
-                                        int blk, const uint64_t* w, const uint64_t* wsh,
-                                        const PrimeConst& pc) {
+                                        int blk, const ulonglong2* tw, const PrimeConst& pc) {
   constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
   int cur = lo_in;
 #pragma unroll
@@ -148,7 +147,7 @@ __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
     const int lo = plo + EB > LOGS ? LOGS - EB : plo;
     reg_shuffle<LOGS>(x, buf, lane, cur, lo);
     cur = lo;
-    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, w, wsh, pc);
+    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, pc);
   }
   reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
 }

@@ -133,7 +133,9 @@ PrimeConst make_prime_const(uint64_t q, int log_n, uint64_t ipsi1) {
   return c;
 }
 
-// Twiddles of one prime: psi_rev, shoup, ipsi_rev, shoup (natural form).
+// Twiddles of one prime, natural form, bit-reversed order, as interleaved
+// Shoup pairs: [psi_rev[i], shoup(psi_rev[i])] for i < N, then the same for
+// ipsi_rev -- one 16-byte load per butterfly.
 static void make_twiddles(uint64_t q, int log_n, uint64_t* out4n) {
   const uint64_t n = 1ull << log_n;
   const uint64_t psi = find_psi(q, 2 * n);
@@ -148,10 +150,10 @@ static void make_twiddles(uint64_t q, int log_n, uint64_t* out4n) {
   }
   for (uint64_t i = 0; i < n; ++i) {
     const uint32_t rv = brev((uint32_t)i, log_n);
-    out4n[i] = pw[rv];
-    out4n[n + i] = h_shoup(pw[rv], q);
-    out4n[2 * n + i] = ipw[rv];
-    out4n[3 * n + i] = h_shoup(ipw[rv], q);
+    out4n[2 * i] = pw[rv];
+    out4n[2 * i + 1] = h_shoup(pw[rv], q);
+    out4n[2 * n + 2 * i] = ipw[rv];
+    out4n[2 * n + 2 * i + 1] = h_shoup(ipw[rv], q);
   }
 }
 
@@ -293,7 +295,7 @@ static Ring* create_ring(int log_n, const uint64_t* chain, int n_chain, const ui
   for (size_t i = 0; i < R->primes.size(); ++i) {
     uint64_t* t = tw.data() + i * 4 * n;
     make_twiddles(R->primes[i], log_n, t);
-    R->hpc[i] = make_prime_const(R->primes[i], log_n, t[2 * n + 1]);
+    R->hpc[i] = make_prime_const(R->primes[i], log_n, t[2 * n + 2]);  // ipsi_rev[1]
   }
   check_cuda(cudaMalloc(&R->dpc, R->hpc.size() * sizeof(PrimeConst)), "alloc consts");
   check_cuda(cudaMemcpy(R->dpc, R->hpc.data(), R->hpc.size() * sizeof(PrimeConst),
@@ -674,14 +676,14 @@ static void shim_ntt(bool inverse, uint64_t* a, int k, int n, const uint64_t* tw
     uint64_t* t = tw.data() + (size_t)i * 4 * n + (inverse ? 2 * (size_t)n : 0);
     for (int j = 0; j < n; ++j) {
       const uint64_t w = h_mulmod(tw_mont[(size_t)i * n + j] % qi, rinv, qi);
-      t[j] = w;
-      t[n + j] = h_shoup(w, qi);
+      t[2 * j] = w;
+      t[2 * j + 1] = h_shoup(w, qi);
     }
-    pc[i] = make_prime_const(qi, log_n, inverse ? t[1] : 1);
+    pc[i] = make_prime_const(qi, log_n, inverse ? t[2] : 1);
     if (inverse) {
       pc[i].ninv = h_mulmod(ninv_mont[i] % qi, rinv, qi);
       pc[i].ninv_sh = h_shoup(pc[i].ninv, qi);
-      pc[i].ilast = h_mulmod(t[1], pc[i].ninv, qi);
+      pc[i].ilast = h_mulmod(t[2], pc[i].ninv, qi);
       pc[i].ilast_sh = h_shoup(pc[i].ilast, qi);
     }
   }
