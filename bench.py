@@ -391,11 +391,16 @@ class TrainWorkload:
         self.units = self.batch_rows
         self.h2d = (self.host_x[0].numel() + self.host_y[0].numel()) * 8
         self.d2h = 0
-        self.config = {
+        self.config = self.static_config(world)
+        self.config["rotation_keys"] = len(steps)
+
+    @classmethod
+    def static_config(cls, world):
+        return {
             "workload": "cfg4 encrypted-LR training minibatch (SST-2-shaped synthetic 768-d)",
-            "preset": "p16", "N": params.ring_degree, "batch_rows": self.batch_rows,
-            "ciphertexts_per_minibatch": cts, "rows_per_ct": rows_per_ct,
-            "refresh": "sparse-1024 bootstrap of w and u", "rotation_keys": len(steps),
+            "preset": "p16", "N": 65536, "batch_rows": cls.batch_rows,
+            "ciphertexts_per_minibatch": cls.batch_rows // 32, "rows_per_ct": 32,
+            "refresh": "sparse-1024 bootstrap of w and u",
             "parallelism": f"minibatch sharded over {world} GPU(s)",
             "l2": "keys (>14 GiB) and diagonals (36 GiB) exceed L2"}
 
@@ -645,7 +650,8 @@ def run_reference(args):
     line = {"metric": wl.metric, "value": round(value, 6), "unit": wl.unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": wl.higher, "impl": "reference", "data": "synthetic",
-            "config": {"workload": args.config, "preset": "p16"},
+            "config": (wl.static_config(args.gpus) if hasattr(wl, "static_config")
+                       else {"workload": args.config, "preset": "p16"}),
             "cpu_baseline": {"value": round(value, 6), "unit": wl.unit,
                              "cores": os.cpu_count(), "kind": "port", "sample": sample},
             "e2e": {"value": round(value, 6), "unit": wl.unit, "h2d_bytes_per_step": 0,

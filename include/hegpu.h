@@ -151,11 +151,14 @@ int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int6
  * key_b/key_a: host arrays of n_digits device pointers, each digit a
  * (key_rows, N) eval-form poly over chain primes then special primes
  * (key_rows = n_chain + n_special).  alpha = digit size (params.py:48-51).
- * out_b / out_a: eval-form results at `level`.  Bit-exact with the reference. */
+ * out_b / out_a: eval-form results at `level`.  accumulate bit 0 / bit 1: add
+ * the result into out_b / out_a instead of overwriting (fuses the
+ * "d0 + KS(d2).b" of mult and rotate into the ModDown epilogue).  Bit-exact
+ * with the reference. */
 int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
                    int64_t d_stride, int n_batch, const uint64_t* const* key_b,
                    const uint64_t* const* key_a, int n_digits, uint64_t* out_b,
-                   uint64_t* out_a, int64_t out_stride, void* stream);
+                   uint64_t* out_a, int64_t out_stride, int accumulate, void* stream);
 
 /* Hoisted rotations of one (batched) ciphertext by n_rot Galois elements
  * (the bootstrap baby steps, bootstrap.py:214-217): ModUp of c1 once, then
@@ -170,6 +173,20 @@ int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c,
                      int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
                      uint64_t* const* outs, void* stream);
+
+/* Giant steps of a BSGS linear transform with one lazy ModDown:
+ * out = partial[0] + sum_{g=1}^{n_giants-1} rot_g(partial[g]) where rot_g is
+ * X -> X^galois[g] followed by a key switch with key g (key_b/key_a: host
+ * arrays of n_giants*n_digits device pointers, giant-major; entries of giant
+ * 0 unused).  partials: packed (n_batch, 2, level+1, N) ciphertexts at
+ * partials + g*gstride; out: packed (n_batch, 2, level+1, N).  The inner
+ * products accumulate in the extended basis and are brought down once
+ * (bootstrap.py:243-245 rotates and adds per giant); decrypts identically,
+ * limbs differ. */
+int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
+                      int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
+                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                      uint64_t* out, void* stream);
 
 /* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
  * limbs (eval form), out gets `level` limbs.  in may equal out. */

@@ -514,26 +514,20 @@ def mult(ct1, ct2, relin_key_or_keyset, rescale_after=True):
         raise OutOfLevelsError("mult at level 0")
     params = ct1.params
     level = ct1.level
-    d = _tensor(ct1, ct2)
+    d = _tensor(ct1, ct2)  # (..., 3, k, N): d0, d1, d2
     ring = params.ring
-    d2 = rg.RnsPoly(ring, d[..., 2, :, :], rg.EVAL, level)
-    kb, ka = keysmod.ks_apply(keyset, keyset.relin_key, d2)
-    lead = tuple(d.shape[:-3])
-    out = _packed(params, lead, level)
-    res = _ct(out, level, ct1.scale * ct2.scale, ct1.slot_count, params,
-              ct1.insecure_provenance or ct2.insecure_provenance)
     k = level + 1
     n = params.ring_degree
-    # (d0, d1) + (kb, ka): both operands are (..., 2, k, N)-strided views
-    dp, cnt, _ = _dev.group(d[..., 0, :, :], k, n)
-    kp, _, _ = kb._group()
-    if cnt == 1:
-        _ew_group(params, _lib.OP_ADD, dp, k * n, kp, k * n, out.data_ptr(), k * n, 2, k)
-    else:
-        for c in range(2):
-            _ew_group(params, _lib.OP_ADD, d[..., c, :, :].data_ptr(), 3 * k * n,
-                      (kb if c == 0 else ka).data.data_ptr(), 2 * k * n,
-                      out[..., c, :, :].data_ptr(), 2 * k * n, cnt, k)
+    d2 = rg.RnsPoly(ring, d[..., 2, :, :], rg.EVAL, level)
+    # (d0, d1) += KS(d2): the ModDown epilogue accumulates in place
+    keysmod.ks_apply_into(keyset, keyset.relin_key, d2, d[..., 0, :, :].data_ptr(),
+                          d[..., 1, :, :].data_ptr(), 3 * k * n, 3)
+    res = Ciphertext(
+        rg.RnsPoly(ring, d[..., 0, :, :], rg.EVAL, level),
+        rg.RnsPoly(ring, d[..., 1, :, :], rg.EVAL, level),
+        ct1.scale * ct2.scale, ct1.slot_count, params,
+        ct1.insecure_provenance or ct2.insecure_provenance,
+    )
     return rescale(res) if rescale_after else res
 
 
@@ -562,17 +556,13 @@ def _automorph_ct(ct, g):
 
 
 def _switch_after_automorph(ct, g, key, keyset):
-    """(c0∘σ + KS(c1∘σ).b, KS(c1∘σ).a) (ops.py:374-388 / :401-416)."""
+    """(c0∘σ + KS(c1∘σ).b, KS(c1∘σ).a) (ops.py:374-388 / :401-416); the b half
+    is accumulated into c0∘σ and the a half overwrites c1∘σ in place."""
     r = _automorph_ct(ct, g)
-    kb, ka = keysmod.ks_apply(keyset, key, r.c1)
-    params = ct.params
     k = ct.level + 1
-    n = params.ring_degree
-    cnt = 1 if ct.batch is None else ct.batch
-    # c0' = c0r + kb (written into r's c0 slot), c1' = ka
-    _ew_group(params, _lib.OP_ADD, r.c0.data.data_ptr(), 2 * k * n, kb.data.data_ptr(),
-              2 * k * n, r.c0.data.data_ptr(), 2 * k * n, cnt, k)
-    r.c1.data.copy_(ka.data)
+    n = ct.params.ring_degree
+    keysmod.ks_apply_into(keyset, key, r.c1, r.c0.data.data_ptr(), r.c1.data.data_ptr(),
+                          2 * k * n, 1)
     return r
 
 

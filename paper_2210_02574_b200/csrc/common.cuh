@@ -124,6 +124,18 @@ struct Seg {
   int n_polys;
   int k;
   int row_start;  // first global (poly, limb) row of this segment
+  // fused basis-conversion prologue (forward register NTT): the input of limb
+  // t of poly p is REDC(sum_i csrc[p*csrc_stride + i*N + x] * cpunc[i*cpunc_ld + t])
+  const uint64_t* csrc;
+  int64_t csrc_stride;
+  const uint64_t* cpunc;
+  int c_nsrc;
+  int cpunc_ld;
+  int eacc;  // epilogue accumulates: eout = eout + (other - y) * c
+  // cmode 1: the prologue instead lifts one coefficient-form limb (modulus
+  // csrc_q, at csrc + p*csrc_stride) centered into every limb (rescale/ModRaise)
+  int cmode;
+  uint64_t csrc_q;
 };
 
 struct SegSet {

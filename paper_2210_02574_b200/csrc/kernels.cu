@@ -666,12 +666,18 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ Ip
     a1.fold(pc.q);
     uint64_t* o = P.acc + b * P.acc_sb + (size_t)r * N + x;
     const uint64_t q = pc.q, qn = pc.qinv_neg, r2 = pc.r2;
-    *reinterpret_cast<ulonglong2*>(o) =
-        make_ulonglong2(mont_mul(redc128(b0.hi, b0.lo, q, qn), r2, q, qn),
-                        mont_mul(redc128(b1.hi, b1.lo, q, qn), r2, q, qn));
-    *reinterpret_cast<ulonglong2*>(o + (size_t)P.n_ext * N) =
-        make_ulonglong2(mont_mul(redc128(a0.hi, a0.lo, q, qn), r2, q, qn),
-                        mont_mul(redc128(a1.hi, a1.lo, q, qn), r2, q, qn));
+    ulonglong2 vb = make_ulonglong2(mont_mul(redc128(b0.hi, b0.lo, q, qn), r2, q, qn),
+                                    mont_mul(redc128(b1.hi, b1.lo, q, qn), r2, q, qn));
+    ulonglong2 va = make_ulonglong2(mont_mul(redc128(a0.hi, a0.lo, q, qn), r2, q, qn),
+                                    mont_mul(redc128(a1.hi, a1.lo, q, qn), r2, q, qn));
+    if (P.accumulate) {
+      const ulonglong2 pb = *reinterpret_cast<const ulonglong2*>(o);
+      const ulonglong2 pa = *reinterpret_cast<const ulonglong2*>(o + (size_t)P.n_ext * N);
+      vb = make_ulonglong2(add_mod(vb.x, pb.x, q), add_mod(vb.y, pb.y, q));
+      va = make_ulonglong2(add_mod(va.x, pa.x, q), add_mod(va.y, pa.y, q));
+    }
+    *reinterpret_cast<ulonglong2*>(o) = vb;
+    *reinterpret_cast<ulonglong2*>(o + (size_t)P.n_ext * N) = va;
   }
 }
 

@@ -34,6 +34,10 @@ struct NttParams {
   int epi;
   uint64_t c[kMaxPrimes];
   uint64_t csh[kMaxPrimes];
+  // inverse with post-scale: final-stage constants per limb (sum, difference)
+  int post;
+  ulonglong2 fin_s[kMaxPrimes];
+  ulonglong2 fin_d[kMaxPrimes];
 };
 
 template <bool INV>
@@ -173,7 +177,9 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
         uint64_t y = sm[e];
         y = y >= q2 ? y - q2 : y;
         y = y >= q ? y - q : y;
-        eout[e] = shoup(other[e] + q - y, cc, ccsh, q);
+        uint64_t r = shoup(other[e] + q - y, cc, ccsh, q);
+        if (sg.eacc) r = add_mod(r, eout[e], q);
+        eout[e] = r;
       }
       return;
     }
@@ -236,9 +242,41 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
   const int c0 = blockIdx.x * kRegWarps;
-  for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
-    const int r = e / kRegWarps, c = e % kRegWarps;
-    tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+  if (!INV && sg.csrc != nullptr && sg.cmode == 1) {
+    // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
+    const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
+    const uint64_t qs = sg.csrc_q;
+    for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+      const int r = e / kRegWarps, c = e % kRegWarps;
+      const uint64_t u = __ldg(hs + c0 + c + (size_t)C * r);
+      const int64_t v = u > (qs >> 1) ? (int64_t)u - (int64_t)qs : (int64_t)u;
+      tile[r * TS + c] = signed_mod(v, pc);
+    }
+  } else if (!INV && sg.csrc != nullptr) {
+    // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
+    const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
+    const uint64_t q = pc.q;
+    for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+      const int r = e / kRegWarps, c = e % kRegWarps;
+      const size_t x = c0 + c + (size_t)C * r;
+      uint64_t hi = 0, lo = 0;
+      for (int i = 0; i < sg.c_nsrc; ++i) {
+        const uint64_t h = __ldg(hs + (size_t)i * N + x);
+        const uint64_t m = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
+        const uint64_t plo = h * m, phi = __umul64hi(h, m);
+        const uint64_t nlo = lo + plo;
+        hi = hi + phi + (nlo < lo);
+        lo = nlo;
+        if (i & 1) hi = hi >= q ? hi - q : hi;
+      }
+      hi = hi >= q ? hi - q : hi;
+      tile[r * TS + c] = redc128(hi, lo, q, pc.qinv_neg);
+    }
+  } else {
+    for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+      const int r = e / kRegWarps, c = e % kRegWarps;
+      tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+    }
   }
   __syncthreads();
   constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
@@ -248,7 +286,9 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
   if (!INV)
     fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, tw, pc.q);
   else
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, tw, pc);
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, tw, pc,
+                  P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh),
+                  P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
   for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
   __syncthreads();
@@ -297,7 +337,9 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const
         uint64_t y = x[e];
         y = y >= q2 ? y - q2 : y;
         y = y >= q ? y - q : y;
-        eout[lane + 32 * e] = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
+        uint64_t r = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
+        if (sg.eacc) r = add_mod(r, eout[lane + 32 * e], q);
+        eout[lane + 32 * e] = r;
       }
       return;
     }
@@ -308,7 +350,8 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const
       dst[lane + 32 * e] = y >= q ? y - q : y;
     }
   } else {
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, tw, pc);
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, tw, pc,
+                  make_ulonglong2(pc.ninv, pc.ninv_sh), make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
     for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
   }
@@ -396,6 +439,19 @@ void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inve
       local.csh[i] = epi->csh[i];
     }
   }
+  local.post = (epi && epi->post) ? 1 : 0;
+  if (local.post) {
+    for (int i = 0; i < kMaxPrimes; ++i) {
+      local.fin_s[i] = epi->fin_s[i];
+      local.fin_d[i] = epi->fin_d[i];
+    }
+  }
+  bool has_conv = false;
+  for (int g = 0; g < S.n_seg; ++g) has_conv |= S.seg[g].csrc != nullptr;
+  if ((has_conv || local.post) && log_n < 12)
+    throw HegpuError{HEGPU_E_ARG, "fused conversion / post-scale needs N >= 2^12"};
+  if (has_conv && inverse) throw HegpuError{HEGPU_E_ARG, "conversion prologue is forward-only"};
+  if (local.post && !inverse) throw HegpuError{HEGPU_E_ARG, "post-scale is inverse-only"};
   const int N = 1 << log_n, R = 1 << a, C = N >> a;
   const int kTile = 4096;
   int cpb = kTile / R;

@@ -65,12 +65,15 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
 // Inverse GS butterflies for bit positions p = plo up to phi.  Twiddle index
 // is hbase(p) + (blk << (LOGS - p - 1)) + (j >> (p + 1)) with
 // hbase(p) = N >> (gshift + p + 1), gshift the global bit offset of this pass.
-// When `last_n` the final stage (global t = N/2) folds in N^-1.
+// The final stage (global t = N/2) multiplies the sum by fin_s and the
+// difference by fin_d: (N^-1, ipsi_rev[1] N^-1), optionally times a per-limb
+// post-scale (the ModUp / ModDown punctured-product inverse).
 template <int LOGS>
 __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
                                           int plo, int phi, int log_n, int gshift, int blk,
                                           const ulonglong2* __restrict__ tw,
-                                          const PrimeConst& pc) {
+                                          const PrimeConst& pc, const ulonglong2 fin_s,
+                                          const ulonglong2 fin_d) {
   constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
   const uint64_t q = pc.q, q2 = q << 1;
 #pragma unroll
@@ -93,8 +96,8 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
         const ulonglong2 wp = __ldg(tw + ti);
         x[e + d] = shoup_lazy(df, wp.x, wp.y, q);
       } else {
-        x[e] = shoup(s, pc.ninv, pc.ninv_sh, q);
-        x[e + d] = shoup(df, pc.ilast, pc.ilast_sh, q);
+        x[e] = shoup(s, fin_s.x, fin_s.y, q);
+        x[e + d] = shoup(df, fin_d.x, fin_d.y, q);
       }
     }
   }
@@ -137,7 +140,8 @@ __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
 template <int LOGS>
 __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
                                         int lane, int lo_in, int lo_out, int log_n, int gshift,
-                                        int blk, const ulonglong2* tw, const PrimeConst& pc) {
+                                        int blk, const ulonglong2* tw, const PrimeConst& pc,
+                                        const ulonglong2 fin_s, const ulonglong2 fin_d) {
   constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
   int cur = lo_in;
 #pragma unroll
@@ -147,7 +151,7 @@ __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
     const int lo = plo + EB > LOGS ? LOGS - EB : plo;
     reg_shuffle<LOGS>(x, buf, lane, cur, lo);
     cur = lo;
-    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, pc);
+    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
   }
   reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
 }

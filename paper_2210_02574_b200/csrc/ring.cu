@@ -219,6 +219,14 @@ const KsLevel& Ring::ks_level(int level, int alpha) {
       md_punc[(size_t)i * k + t] = h_mulmod(prod_mod(sp, i, q), h_rmod(q), q);
     }
   }
+  auto fin = [&](int p, uint64_t sc, std::vector<ulonglong2>& fs, std::vector<ulonglong2>& fd) {
+    const uint64_t q = primes[p];
+    const uint64_t a = h_mulmod(hpc[p].ninv, sc, q), b = h_mulmod(hpc[p].ilast, sc, q);
+    fs.push_back(make_ulonglong2(a, h_shoup(a, q)));
+    fd.push_back(make_ulonglong2(b, h_shoup(b, q)));
+  };
+  for (int i = 0; i < k; ++i) fin(i, mu_inv[i], L->mu_fin_s, L->mu_fin_d);
+  for (int i = 0; i < K; ++i) fin(n_chain + i, md_inv[i], L->md_fin_s, L->md_fin_d);
   L->pinv.resize(k);
   L->pinv_sh.resize(k);
   for (int t = 0; t < k; ++t) {
@@ -320,6 +328,14 @@ static void add_seg(SegSet& S, const uint64_t* in, int64_t is, uint64_t* out, in
   g.out_stride = os;
   g.other = nullptr;
   g.eout = nullptr;
+  g.csrc = nullptr;
+  g.csrc_stride = 0;
+  g.cpunc = nullptr;
+  g.c_nsrc = 0;
+  g.cpunc_ld = 0;
+  g.eacc = 0;
+  g.cmode = 0;
+  g.csrc_q = 0;
   g.other_stride = 0;
   g.eout_stride = 0;
   g.n_polys = n_polys;
@@ -359,6 +375,46 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
   const std::vector<int32_t> chain = range_primes(0, k);
+  if (R.log_n >= 12) {
+    // fused path: INTT(d) scaled by (Q_j/q_i)^-1 gives hat_i directly; each
+    // digit's conversion runs inside the forward NTT's first pass.
+    SegSet S0;
+    S0.n_seg = 0;
+    S0.n_rows = 0;
+    add_seg(S0, d, ds, dcoeff, (int64_t)k * N, B, k, chain.data());
+    NttEpilogue E0;
+    E0.post = true;
+    for (int i = 0; i < k; ++i) {
+      E0.fin_s[i] = L.mu_fin_s[i];
+      E0.fin_d[i] = L.mu_fin_d[i];
+    }
+    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+    for (int j0 = 0; j0 < beta; j0 += kMaxSeg) {
+      const int jn = std::min(kMaxSeg, beta - j0);
+      SegSet S;
+      S.n_seg = 0;
+      S.n_rows = 0;
+      for (int jj = 0; jj < jn; ++jj) {
+        const int j = j0 + jj;
+        const int g0 = j * alpha, g1 = std::min(g0 + alpha, k), g = g1 - g0;
+        const int n_dst = n_ext - g;
+        if (n_dst <= 0) continue;
+        std::vector<int32_t> dsel(n_dst);
+        for (int t = 0; t < n_dst; ++t) dsel[t] = L.dst_prime_of_digit[(size_t)j * n_ext + t];
+        uint64_t* dst = ext + (size_t)j * n_ext * N;
+        const int64_t dsb = (int64_t)beta * n_ext * N;
+        add_seg(S, nullptr, 0, dst, dsb, B, n_dst, dsel.data());
+        Seg& sg = S.seg[S.n_seg - 1];
+        sg.csrc = dcoeff + (size_t)g0 * N;
+        sg.csrc_stride = (int64_t)k * N;
+        sg.cpunc = L.mu_punc + (size_t)g0 * n_ext;
+        sg.c_nsrc = g;
+        sg.cpunc_ld = n_ext;
+      }
+      launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    }
+    return;
+  }
   // 1. d -> coefficient form
   ntt_simple(R, true, d, ds, dcoeff, (int64_t)k * N, B, k, chain.data(), st);
   // 2. ModUp basis conversion of every digit, 3. NTT of the converted rows
@@ -401,18 +457,15 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
   }
 }
 
-// Key inner product (keys.py:316-323) and ModDown (keys.py:325-338).  d / ext
-// are the digit sources (own rows from d, converted rows from ext).
-static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
-                      const uint64_t* ext, int B, const uint64_t* const* key_b,
-                      const uint64_t* const* key_a, uint64_t* acc, uint64_t* corr,
-                      uint64_t* out_b, int64_t os_b, uint64_t* out_a, int64_t os_a,
-                      cudaStream_t st) {
+// Key inner product (keys.py:316-323): acc (+)= sum_j digit_j * key_j over
+// the extended basis.  d / ext are the digit sources (own rows from d,
+// converted rows from ext, compact layout).
+static void ks_ip(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, const uint64_t* ext,
+                  int B, const uint64_t* const* key_b, const uint64_t* const* key_a,
+                  uint64_t* acc, bool accumulate, cudaStream_t st) {
   const int level = L.level, alpha = L.alpha;
-  const int k = level + 1, K = R.n_special, n_ext = L.n_ext, beta = L.beta;
+  const int n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
-  const size_t sz_corr = (size_t)B * 2 * k * N;
-  const std::vector<int32_t> chain = range_primes(0, k);
   // 4. inner product with the key digits
   IpParams P;
   P.d = d;
@@ -435,9 +488,37 @@ static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
   P.n_batch = B;
   P.log_n = R.log_n;
   P.pc = R.dpc;
+  P.accumulate = accumulate ? 1 : 0;
   launch_ks_ip(P, st);
+}
+
+// ModDown (keys.py:325-338) of acc [b][2][n_ext][N]: (b, a) = (acc - conv(P-part))
+// * P^-1 written to (or with acc_b / acc_a added into) out_b / out_a.
+static void ks_moddown(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr, int B,
+                       uint64_t* out_b, int64_t os_b, uint64_t* out_a, int64_t os_a,
+                       cudaStream_t st, bool acc_b, bool acc_a) {
+  const int level = L.level;
+  const int k = level + 1, K = R.n_special, n_ext = L.n_ext;
+  const size_t N = R.n;
+  const size_t sz_corr = (size_t)B * 2 * k * N;
+  const std::vector<int32_t> chain = range_primes(0, k);
   // 5. ModDown: INTT(specials), convert specials -> chain, NTT, (acc - corr) P^-1
-  if (K > 0) {
+  const bool fused = R.log_n >= 12 && K > 0;
+  if (fused) {
+    const std::vector<int32_t> sp = range_primes(R.n_chain, K);
+    SegSet S0;
+    S0.n_seg = 0;
+    S0.n_rows = 0;
+    add_seg(S0, acc + (size_t)k * N, (int64_t)n_ext * N, acc + (size_t)k * N, (int64_t)n_ext * N,
+            2 * B, K, sp.data());
+    NttEpilogue E0;
+    E0.post = true;
+    for (int i = 0; i < K; ++i) {
+      E0.fin_s[i] = L.md_fin_s[i];
+      E0.fin_d[i] = L.md_fin_d[i];
+    }
+    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+  } else if (K > 0) {
     const std::vector<int32_t> sp = range_primes(R.n_chain, K);
     ntt_simple(R, true, acc + (size_t)k * N, (int64_t)n_ext * N, acc + (size_t)k * N,
                (int64_t)n_ext * N, 2 * B, K, sp.data(), st);
@@ -477,6 +558,17 @@ static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
   S.seg[1].other_stride = (int64_t)2 * n_ext * N;
   S.seg[1].eout = out_a;
   S.seg[1].eout_stride = os_a;
+  S.seg[0].eacc = acc_b ? 1 : 0;
+  S.seg[1].eacc = acc_a ? 1 : 0;
+  if (fused) {  // the specials -> chain conversion runs inside the NTT's first pass
+    for (int g = 0; g < 2; ++g) {
+      S.seg[g].csrc = acc + (size_t)g * n_ext * N + (size_t)k * N;
+      S.seg[g].csrc_stride = (int64_t)2 * n_ext * N;
+      S.seg[g].cpunc = L.md_punc;
+      S.seg[g].c_nsrc = K;
+      S.seg[g].cpunc_ld = k;
+    }
+  }
   NttEpilogue E;
   E.enabled = true;
   for (int t = 0; t < k; ++t) {
@@ -487,10 +579,19 @@ static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
 }
 
 
+static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
+                      const uint64_t* ext, int B, const uint64_t* const* key_b,
+                      const uint64_t* const* key_a, uint64_t* acc, uint64_t* corr,
+                      uint64_t* out_b, int64_t os_b, uint64_t* out_a, int64_t os_a,
+                      cudaStream_t st, bool acc_b = false, bool acc_a = false) {
+  ks_ip(R, L, d, ds, ext, B, key_b, key_a, acc, false, st);
+  ks_moddown(R, L, acc, corr, B, out_b, os_b, out_a, os_a, st, acc_b, acc_a);
+}
+
 static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds, int B,
                           const uint64_t* const* key_b, const uint64_t* const* key_a,
                           int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t os,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool acc_b = false, bool acc_a = false) {
   if (B <= 0) return;
   const KsLevel& L = R.ks_level(level, alpha);
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
@@ -505,7 +606,8 @@ static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int6
   uint64_t* acc = ext + sz_ext;
   uint64_t* corr = acc + sz_acc;
   ks_modup(R, L, d, ds, B, dcoeff, ext, st);
-  ks_ipdown(R, L, d, ds, ext, B, key_b, key_a, acc, corr, out_b, os, out_a, os, st);
+  ks_ipdown(R, L, d, ds, ext, B, key_b, key_a, acc, corr, out_b, os, out_a, os, st, acc_b,
+            acc_a);
 }
 
 // Hoisted rotations (bootstrap baby steps): ModUp of c1 once, then per
@@ -528,14 +630,13 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
   const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
   const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
   const size_t sz_kb = (size_t)B * k * N;
-  Scratch ws((sz_dc + 2 * sz_ext + sz_acc + sz_corr + 2 * sz_kb) * 8, st);
+  Scratch ws((sz_dc + 2 * sz_ext + sz_acc + sz_corr + sz_kb) * 8, st);
   uint64_t* dcoeff = ws.u64();
   uint64_t* ext = dcoeff + sz_dc;
   uint64_t* extp = ext + sz_ext;
   uint64_t* acc = extp + sz_ext;
   uint64_t* corr = acc + sz_acc;
   uint64_t* dp = corr + sz_corr;
-  uint64_t* kb = dp + sz_kb;
   const uint64_t* c1 = c + c1_off;
   ks_modup(R, L, c1, cs, B, dcoeff, ext, st);
   const std::vector<int32_t> chain = range_primes(0, k);
@@ -546,14 +647,58 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
     launch_automorphism(R.dpc, R.log_n, true, galois[r], ext, (int64_t)n_ext * N, extp,
                         (int64_t)n_ext * N, B * beta, n_ext, rows.data(), st);
     uint64_t* out = outs[r];
-    ks_ipdown(R, L, dp, (int64_t)k * N, extp, B, key_b + (size_t)r * n_digits,
-              key_a + (size_t)r * n_digits, acc, corr, kb, (int64_t)k * N, out + c1_off, cs,
-              st);
-    // c0' = sigma(c0) + kb
+    // c0' = sigma(c0) + kb: permute c0 into place, then the ModDown epilogue
+    // accumulates kb into it; c1' = ka is written directly
     launch_automorphism(R.dpc, R.log_n, true, galois[r], c, cs, out, cs, B, k, chain.data(), st);
-    EwArgs A{HEGPU_OP_ADD, out, cs, kb, (int64_t)k * N, out, cs, B, k, chain.data(), nullptr};
+    ks_ipdown(R, L, dp, (int64_t)k * N, extp, B, key_b + (size_t)r * n_digits,
+              key_a + (size_t)r * n_digits, acc, corr, out, cs, out + c1_off, cs, st,
+              /*acc_b=*/true, /*acc_a=*/false);
+  }
+}
+
+// Giant steps of a BSGS transform with one lazy ModDown (double hoisting):
+// out = partial[0] + sum_{g>0} rot_{galois[g]}(partial[g]).  Each giant's key
+// inner product accumulates in the extended basis; the sum is brought down
+// once.  Decrypts like the per-giant rotate-and-add (bootstrap.py:243-245);
+// limbs differ (ModDown is linear only up to its rounding).
+// partials: n_giants packed (B, 2, k, N) ciphertexts, giant g at
+// partials + g*gstride; out: packed (B, 2, k, N).
+static void bsgs_giants_impl(Ring& R, int level, int alpha, const uint64_t* partials,
+                             int64_t gstride, int B, int n_giants, const uint64_t* galois,
+                             const uint64_t* const* key_b, const uint64_t* const* key_a,
+                             int n_digits, uint64_t* out, cudaStream_t st) {
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  const int64_t cs = (int64_t)2 * k * N;  // packed batch stride
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  const std::vector<int32_t> chain = range_primes(0, k);
+  {  // out = partial[0]
+    EwArgs A{HEGPU_OP_COPY, partials, (int64_t)k * N, nullptr, 0, out, (int64_t)k * N, 2 * B, k,
+             chain.data(), nullptr};
     launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
   }
+  if (n_giants <= 1) return;
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  const size_t sz_tmp = (size_t)B * 2 * k * N;
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr + sz_tmp) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  uint64_t* tmp = corr + sz_corr;
+  for (int g = 1; g < n_giants; ++g) {
+    const uint64_t* part = partials + g * gstride;
+    launch_automorphism(R.dpc, R.log_n, true, galois[g], part, (int64_t)k * N, tmp,
+                        (int64_t)k * N, 2 * B, k, chain.data(), st);
+    ks_modup(R, L, tmp + (size_t)k * N, cs, B, dcoeff, ext, st);
+    ks_ip(R, L, tmp + (size_t)k * N, cs, ext, B, key_b + (size_t)g * n_digits,
+          key_a + (size_t)g * n_digits, acc, g > 1, st);
+    EwArgs A{HEGPU_OP_ADD, out, cs, tmp, cs, out, cs, B, k, chain.data(), nullptr};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);  // out.c0 += sigma(c0)
+  }
+  ks_moddown(R, L, acc, corr, B, out, cs, out + (size_t)k * N, cs, st, true, true);
 }
 
 // --- rescale (ops.py:164-189) and ModRaise (bootstrap.py:260-275) ----------
@@ -564,14 +709,16 @@ static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uin
   if (P <= 0) return;
   const size_t N = R.n;
   const auto& cs = R.rescale_consts(level);
+  const bool fused = R.log_n >= 12;
   Scratch ws((size_t)P * (1 + level) * N * 8, st);
   uint64_t* top = ws.u64();
   uint64_t* rest = top + (size_t)P * N;
   const int32_t lp = level;
   ntt_simple(R, true, in + (size_t)level * N, is, top, (int64_t)N, P, 1, &lp, st);
   const std::vector<int32_t> chain = range_primes(0, level);
-  launch_lift_centered(R.dpc, R.log_n, top, (int64_t)N, R.primes[level], rest,
-                       (int64_t)level * N, P, level, chain.data(), st);
+  if (!fused)
+    launch_lift_centered(R.dpc, R.log_n, top, (int64_t)N, R.primes[level], rest,
+                         (int64_t)level * N, P, level, chain.data(), st);
   SegSet S;
   S.n_seg = 0;
   S.n_rows = 0;
@@ -580,6 +727,12 @@ static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uin
   S.seg[0].other_stride = is;
   S.seg[0].eout = out;
   S.seg[0].eout_stride = os;
+  if (fused) {  // the centered lift of the top limb runs inside the NTT's first pass
+    S.seg[0].csrc = top;
+    S.seg[0].csrc_stride = (int64_t)N;
+    S.seg[0].cmode = 1;
+    S.seg[0].csrc_q = R.primes[level];
+  }
   NttEpilogue E;
   E.enabled = true;
   for (int i = 0; i < level; ++i) {
@@ -598,6 +751,18 @@ static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* ou
   const int32_t p0 = 0;
   ntt_simple(R, true, in, is, ws.u64(), (int64_t)N, P, 1, &p0, st);
   const std::vector<int32_t> chain = range_primes(0, to_level + 1);
+  if (R.log_n >= 12) {
+    SegSet S;
+    S.n_seg = 0;
+    S.n_rows = 0;
+    add_seg(S, nullptr, 0, out, os, P, to_level + 1, chain.data());
+    S.seg[0].csrc = ws.u64();
+    S.seg[0].csrc_stride = (int64_t)N;
+    S.seg[0].cmode = 1;
+    S.seg[0].csrc_q = R.primes[0];
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    return;
+  }
   launch_lift_centered(R.dpc, R.log_n, ws.u64(), (int64_t)N, R.primes[0], out, os, P,
                        to_level + 1, chain.data(), st);
   ntt_simple(R, false, out, os, out, os, P, to_level + 1, chain.data(), st);
@@ -897,11 +1062,11 @@ int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int6
 int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d, int64_t d_stride,
                    int n_batch, const uint64_t* const* key_b, const uint64_t* const* key_a,
                    int n_digits, uint64_t* out_b, uint64_t* out_a, int64_t out_stride,
-                   void* stream) {
+                   int accumulate, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     ks_apply_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, out_b, out_a,
-                  out_stride, S_(stream));
+                  out_stride, S_(stream), (accumulate & 1) != 0, (accumulate & 2) != 0);
   })
 }
 
@@ -913,6 +1078,17 @@ int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c,
     Ring& R = RR(ring);
     ks_hoisted_impl(R, level, alpha, c, cs, c1_off, n_batch, n_rot, galois, key_b, key_a,
                     n_digits, outs, S_(stream));
+  })
+}
+
+int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
+                      int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
+                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                      uint64_t* out, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    bsgs_giants_impl(R, level, alpha, partials, gstride, n_batch, n_giants, galois, key_b, key_a,
+                     n_digits, out, S_(stream));
   })
 }
 

@@ -26,6 +26,10 @@ struct KsLevel {
   const uint64_t* md_inv_sh = nullptr;  // [K]
   const uint64_t* md_punc = nullptr;    // [K][level+1]
   std::vector<uint64_t> pinv, pinv_sh;  // P^-1 mod q_t, t <= level (host, kernel params)
+  // final-stage constants of the post-scaled inverse NTTs that produce the
+  // conversion inputs hat_i = x_i * inv_i directly (fused ModUp / ModDown)
+  std::vector<ulonglong2> mu_fin_s, mu_fin_d;  // [level+1]
+  std::vector<ulonglong2> md_fin_s, md_fin_d;  // [K]
   std::vector<int> dst_prime_of_digit;  // flattened [beta][n_ext] compact dst -> global prime
 };
 
@@ -105,9 +109,12 @@ struct ProfScope {
 
 // --- launchers (stream-ordered; throw HegpuError on failure) ----------------
 struct NttEpilogue {
-  bool enabled = false;
+  bool enabled = false;  // forward: eout = (other - y) * c[limb]
   uint64_t c[kMaxPrimes];
   uint64_t csh[kMaxPrimes];
+  bool post = false;     // inverse: final stage scales by fin_s / fin_d (Shoup pairs)
+  ulonglong2 fin_s[kMaxPrimes];
+  ulonglong2 fin_d[kMaxPrimes];
 };
 
 // NTT over a set of segments.  For the forward transform with an epilogue,
@@ -184,6 +191,7 @@ struct IpParams {
   const uint64_t* ka[kMaxDigits];
   uint64_t* acc;  // [b][2][n_ext][N]
   int64_t acc_sb;
+  int accumulate;  // add into acc instead of overwriting (lazy ModDown)
   int level, alpha, beta, n_ext, n_chain, key_sp_row0, n_batch, log_n;
   const PrimeConst* pc;
 };
