@@ -773,128 +773,116 @@ struct BsgsParams {
   const PrimeConst* pc;
 };
 
-// CTA = 16 warps over a 64-coefficient tile of one limb (2 coefficients per
-// lane, 128-bit loads).  The tile of every baby is staged in shared memory
-// once; warp w accumulates giants w, w+16, ... (GPT of them); the giant x term
-// index table is staged too.  The term loop is unrolled by 2 so each lane
-// keeps 2*GPT independent 16-byte diagonal loads in flight.
-constexpr int kBsgsWarps = 16;
+// CTA = 32 warps over a 64-coefficient tile of one limb; warp w accumulates
+// giant w for 2 coefficients per lane (128-bit loads).  The babies' tile is
+// staged in shared memory in chunks of kBsgsChunk terms; the term loop is
+// unrolled by 4 so every lane keeps 4 independent 16-byte diagonal loads in
+// flight (64 KiB per SM) while it multiplies the previous ones.
 constexpr int kBsgsTile = 64;
+constexpr int kBsgsChunk = 16;
 
-template <int NB, int GPT>
-__global__ void __launch_bounds__(kBsgsWarps * 32) k_bsgs(const __grid_constant__ BsgsParams P) {
-  extern __shared__ uint64_t sm[];  // babies [n_terms][NB][2][64], then idx [n_giants][n_terms]
+// WARPS giants per CTA (one per warp); grid.z enumerates giant groups.
+template <int NB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ BsgsParams P) {
+  __shared__ __align__(16) uint64_t sm[kBsgsChunk * NB * 2 * kBsgsTile];
+  __shared__ int32_t s_idx[WARPS * kBsgsMaxTerms];
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
   const int x0 = blockIdx.x * kBsgsTile;
   const PrimeConst pc = P.pc[limb];
   constexpr int per_term = NB * 2 * kBsgsTile;
-  int32_t* s_idx = reinterpret_cast<int32_t*>(sm + (size_t)P.n_terms * per_term);
-  const int nthr = kBsgsWarps * 32;
-  for (int e = threadIdx.x; e < P.n_terms * per_term / 2; e += nthr) {
-    const int e2 = e * 2;
-    const int t = e2 / per_term;
-    const int rem = e2 - t * per_term;
-    const int b = rem / (2 * kBsgsTile);
-    const int c = (rem / kBsgsTile) & 1;
-    const int xi = rem % kBsgsTile;
-    *reinterpret_cast<ulonglong2*>(sm + e2) = __ldg(reinterpret_cast<const ulonglong2*>(
-        P.baby[t] + b * P.bstride + c * P.c1_off + (size_t)limb * N + x0 + xi));
-  }
-  for (int e = threadIdx.x; e < P.n_giants * P.n_terms; e += nthr) s_idx[e] = __ldg(P.pt_idx + e);
-  __syncthreads();
+  const int nthr = WARPS * 32;
+  const int g0 = blockIdx.z * WARPS;  // first giant of this CTA
+  const int ng = P.n_giants - g0 < WARPS ? P.n_giants - g0 : WARPS;
+  for (int e = threadIdx.x; e < ng * P.n_terms; e += nthr)
+    s_idx[e] = __ldg(P.pt_idx + (size_t)g0 * P.n_terms + e);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int xi = lane * 2;
   const size_t coef = (size_t)limb * N + x0 + xi;
-  Acc2 acc[GPT][NB][2][2];
+  const int g = warp;  // local giant
+  Acc2 acc[NB][2][2];
 #pragma unroll
-  for (int gg = 0; gg < GPT; ++gg)
+  for (int b = 0; b < NB; ++b)
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        acc[gg][b][c][0].zero();
-        acc[gg][b][c][1].zero();
-      }
-  for (int t0 = 0; t0 < P.n_terms; t0 += 2) {
-    ulonglong2 pv[2][GPT];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-#pragma unroll
-      for (int gg = 0; gg < GPT; ++gg) {
-        const int g = warp + gg * kBsgsWarps;
-        const int t = t0 + u;
-        const int idx = (g < P.n_giants && t < P.n_terms) ? s_idx[g * P.n_terms + t] : -1;
-        pv[u][gg] = idx >= 0 ? __ldg(reinterpret_cast<const ulonglong2*>(
-                                   P.pt_base + (size_t)idx * P.pt_stride + coef))
-                             : make_ulonglong2(0, 0);
-      }
+    for (int c = 0; c < 2; ++c) {
+      acc[b][c][0].zero();
+      acc[b][c][1].zero();
     }
+  for (int tc = 0; tc < P.n_terms; tc += kBsgsChunk) {
+    const int nt = P.n_terms - tc < kBsgsChunk ? P.n_terms - tc : kBsgsChunk;
+    __syncthreads();  // previous chunk fully consumed (and s_idx visible)
+    for (int e = threadIdx.x; e < nt * per_term / 2; e += nthr) {
+      const int e2 = e * 2;
+      const int t = e2 / per_term;
+      const int rem = e2 - t * per_term;
+      const int b = rem / (2 * kBsgsTile);
+      const int c = (rem / kBsgsTile) & 1;
+      const int xx = rem % kBsgsTile;
+      *reinterpret_cast<ulonglong2*>(sm + e2) = __ldg(reinterpret_cast<const ulonglong2*>(
+          P.baby[tc + t] + b * P.bstride + c * P.c1_off + (size_t)limb * N + x0 + xx));
+    }
+    __syncthreads();
+    if (g < ng) {
+      for (int t0 = 0; t0 < nt; t0 += 4) {
+        ulonglong2 pv[4];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int t = t0 + u;
-      if (t >= P.n_terms) break;
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u;
+          const int idx = t < nt ? s_idx[g * P.n_terms + tc + t] : -1;
+          pv[u] = idx >= 0 ? __ldg(reinterpret_cast<const ulonglong2*>(
+                                 P.pt_base + (size_t)idx * P.pt_stride + coef))
+                           : make_ulonglong2(0, 0);
+        }
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u;
+          if (t >= nt) break;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(
-              sm + t * per_term + b * 2 * kBsgsTile + c * kBsgsTile + xi);
+          for (int b = 0; b < NB; ++b) {
 #pragma unroll
-          for (int gg = 0; gg < GPT; ++gg) {
-            acc[gg][b][c][0].add(bv.x, pv[u][gg].x);
-            acc[gg][b][c][1].add(bv.y, pv[u][gg].y);
+            for (int c = 0; c < 2; ++c) {
+              const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(
+                  sm + t * per_term + b * 2 * kBsgsTile + c * kBsgsTile + xi);
+              acc[b][c][0].add(bv.x, pv[u].x);
+              acc[b][c][1].add(bv.y, pv[u].y);
+            }
+          }
+          if (u & 1) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                acc[b][c][0].fold(pc.q);
+                acc[b][c][1].fold(pc.q);
+              }
           }
         }
       }
     }
-#pragma unroll
-    for (int gg = 0; gg < GPT; ++gg)
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          acc[gg][b][c][0].fold(pc.q);
-          acc[gg][b][c][1].fold(pc.q);
-        }
   }
+  if (g >= ng) return;
 #pragma unroll
-  for (int gg = 0; gg < GPT; ++gg) {
-    const int g = warp + gg * kBsgsWarps;
-    if (g >= P.n_giants) continue;
+  for (int b = 0; b < NB; ++b) {
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
+    for (int c = 0; c < 2; ++c) {
+      uint64_t r[2];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint64_t r[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          Acc2 a = acc[gg][b][c][h];
-          a.fold(pc.q);
-          r[h] = mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
-        }
-        *reinterpret_cast<ulonglong2*>(P.out + g * P.out_gstride + b * P.bstride +
-                                       c * P.c1_off + coef) = make_ulonglong2(r[0], r[1]);
+      for (int h = 0; h < 2; ++h) {
+        Acc2 a = acc[b][c][h];
+        a.fold(pc.q);
+        r[h] = mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
       }
+      *reinterpret_cast<ulonglong2*>(P.out + (g0 + g) * P.out_gstride + b * P.bstride +
+                                     c * P.c1_off + coef) = make_ulonglong2(r[0], r[1]);
     }
   }
 }
 
 template <int NB>
 static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
-  const int gpt_need = (P.n_giants + kBsgsWarps - 1) / kBsgsWarps;
-  dim3 grid((1 << P.log_n) / kBsgsTile, k);
-  const size_t smem = (size_t)P.n_terms * NB * 2 * kBsgsTile * 8 +
-                      (size_t)P.n_giants * P.n_terms * 4;
-  static bool attr = false;
-  if (!attr) {
-    const int mx = 220 * 1024;
-    cudaFuncSetAttribute(k_bsgs<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_bsgs<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr = true;
-  }
-  if (gpt_need <= 1) k_bsgs<NB, 1><<<grid, kBsgsWarps * 32, smem, st>>>(P);
-  else k_bsgs<NB, 2><<<grid, kBsgsWarps * 32, smem, st>>>(P);
+  constexpr int W = NB == 1 ? 32 : 16;  // 64 / 128 registers per thread
+  dim3 grid((1 << P.log_n) / kBsgsTile, k, (P.n_giants + W - 1) / W);
+  k_bsgs<NB, W><<<grid, W * 32, 0, st>>>(P);
 }
 
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
@@ -903,7 +891,7 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                  int64_t out_gstride, int k, cudaStream_t st) {
   if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
   if ((1 << log_n) % kBsgsTile) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
-  const int max_giants = kBsgsWarps * 2;
+  const int max_giants = 1 << 20;  // giant groups are a grid dimension
   for (int b0 = 0; b0 < n_batch; b0 += 2) {
     const int nb = n_batch - b0 < 2 ? n_batch - b0 : 2;
     for (int g0 = 0; g0 < n_giants; g0 += max_giants) {
