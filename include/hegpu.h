@@ -227,11 +227,15 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
  * n_terms <= 64 device pointers); diagonal i at pt_base + i*pt_stride;
  * pt_idx a DEVICE int32 array [n_giants][n_terms] (-1 = zero diagonal);
  * out[g]_b.c0 at out + g*out_gstride + b*bstride, c1 at +c1_off.  Every
- * diagonal, baby and output crosses HBM once. */
+ * diagonal, baby and output crosses HBM once.
+ * pt_log_run = r in [0, 5]: the diagonals are run-compressed, k limbs of
+ * N >> r words each, and coefficient x of limb l reads word (l*N + x) >> r.
+ * Evaluation vectors of polynomials in X^(2^r) have this form in the
+ * bit-reversed NTT order (slot vectors periodic with period N / 2^(r+1)). */
 int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
                int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
-               const int32_t* pt_idx, int n_giants, uint64_t* out, int64_t out_gstride, int k,
-               void* stream);
+               int pt_log_run, const int32_t* pt_idx, int n_giants, uint64_t* out,
+               int64_t out_gstride, int k, void* stream);
 
 /* -------------------------------------------------------------------------
  * host-array kernel table: drop-in for hebert._kernels (_kernels.py:319-328)

@@ -48,7 +48,7 @@ SIGNATURES = {
     "hegpu_mod_raise": [_P, _P, _I64, _P, _I64, _I, _I, _P],
     "hegpu_encrypt_combine": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "hegpu_diag_mac": [_P, _P, _I64, _I64, _P, _I, _I, _P, _I64, _I64, _I, _I, _P],
-    "hegpu_bsgs": [_P, _P, _I, _I64, _I64, _I, _P, _I64, _P, _I, _P, _I64, _I, _P],
+    "hegpu_bsgs": [_P, _P, _I, _I64, _I64, _I, _P, _I64, _I, _P, _I, _P, _I64, _I, _P],
     "hegpu_k_ntt_forward_inplace": [_P, _I, _I, _P, _P, _P],
     "hegpu_k_ntt_inverse_inplace": [_P, _I, _I, _P, _P, _P, _P],
     "hegpu_k_elementwise_mont": [_P, _P, _P, _I, _I, _P, _P],
@@ -66,7 +66,9 @@ _RESTYPES = {
     "hegpu_launch_count": ctypes.c_longlong,
 }
 PROF_CLASSES = ("ntt", "elementwise", "lift", "automorphism", "tensor", "conv", "ks_ip",
-                "diag_mac", "encrypt")
+                "diag_mac", "encrypt",
+                # subsets of "ntt" by the step that issued them (not additive)
+                "ntt_modup", "ntt_moddown", "ntt_rescale")
 
 _lock = threading.Lock()
 _lib = None

@@ -106,6 +106,73 @@ struct Acc128 {
   }
 };
 
+// 128-bit multiply-accumulator with deferred carries: 4 IMAD.WIDE + 1 IADD3.X
+// per product (the portable 64-bit formulation costs ~18 SASS instructions).
+// Value = W + M * 2^32 + c * 2^96 with W = H:L, M (the two
+// cross products) and C the count of M's carries out.  Inputs must be < 2^62.
+// Invariant: after fold() the value is < q * 2^64; from there kMacFold more
+// products (< 2^124 each) keep it below 2^128, so callers fold at least every
+// kMacFold products.
+constexpr int kMacFold = 8;
+
+struct Mac128 {
+  // 64-bit halves keep the IMAD.WIDE operands in aligned register pairs
+  uint64_t L, H, M;  // W = H:L, M = m1:m0
+  uint32_t c;
+  __device__ __forceinline__ void zero() {
+    L = H = M = 0;
+    c = 0;
+  }
+  __device__ __forceinline__ void add(uint64_t a, uint64_t b) {
+    asm("{\n\t.reg .u32 a0, a1, b0, b1, l0, l1, h0, h1, m0, m1;\n\t"
+        "mov.b64 {a0, a1}, %4;\n\tmov.b64 {b0, b1}, %5;\n\t"
+        "mov.b64 {l0, l1}, %0;\n\tmov.b64 {h0, h1}, %1;\n\tmov.b64 {m0, m1}, %2;\n\t"
+        "mad.lo.cc.u32 l0, a0, b0, l0;\n\tmadc.hi.cc.u32 l1, a0, b0, l1;\n\t"
+        "madc.lo.cc.u32 h0, a1, b1, h0;\n\tmadc.hi.u32 h1, a1, b1, h1;\n\t"
+        "mad.lo.cc.u32 m0, a0, b1, m0;\n\tmadc.hi.cc.u32 m1, a0, b1, m1;\n\taddc.u32 %3, %3, 0;\n\t"
+        "mad.lo.cc.u32 m0, a1, b0, m0;\n\tmadc.hi.cc.u32 m1, a1, b0, m1;\n\taddc.u32 %3, %3, 0;\n\t"
+        "mov.b64 %0, {l0, l1};\n\tmov.b64 %1, {h0, h1};\n\tmov.b64 %2, {m0, m1};\n\t}"
+        : "+l"(L), "+l"(H), "+l"(M), "+r"(c)
+        : "l"(a), "l"(b));
+  }
+  // exact 128-bit value (hi, lo)
+  __device__ __forceinline__ void value(uint64_t& hi, uint64_t& lo) const {
+    lo = L + (M << 32);
+    hi = H + (M >> 32) + (static_cast<uint64_t>(c) << 32) + (lo < L);
+  }
+  // hi <- hi mod q (value mod q*2^64 unchanged modulo q); bar = floor(2^64/q)
+  __device__ __forceinline__ void fold(uint64_t q, uint64_t bar) {
+    uint64_t hi, lo;
+    value(hi, lo);
+    uint64_t r = hi - __umul64hi(hi, bar) * q;
+    L = lo;
+    H = r >= q ? r - q : r;
+    M = 0;
+    c = 0;
+  }
+  // value * 2^-64 mod q, in [0, q)
+  __device__ __forceinline__ uint64_t redc(const PrimeConst& pc) const {
+    uint64_t hi, lo;
+    value(hi, lo);
+    uint64_t r = hi - __umul64hi(hi, pc.bar) * pc.q;
+    r = r >= pc.q ? r - pc.q : r;
+    return redc128(r, lo, pc.q, pc.qinv_neg);
+  }
+};
+
+// 16-byte global -> shared copy that does not occupy registers (LDGSTS).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // operand descriptors
 // ---------------------------------------------------------------------------

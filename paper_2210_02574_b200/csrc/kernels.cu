@@ -319,12 +319,11 @@ __global__ void __launch_bounds__(kEwThreads) k_tensor(const __grid_constant__ T
   const uint64_t a0 = P.a0[poly * P.as + l], a1 = P.a1[poly * P.as + l];
   const uint64_t b0 = P.b0[poly * P.bs + l], b1 = P.b1[poly * P.bs + l];
   P.d0[poly * P.ds + l] = mul_mod(a0, b0, pc);
-  Acc128 acc;
+  Mac128 acc;
   acc.zero();
-  acc.mac(a0, b1, pc.q);
-  acc.mac(a1, b0, pc.q);
-  P.d1[poly * P.ds + l] =
-      mont_mul(redc128(acc.hi, acc.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
+  acc.add(a0, b1);
+  acc.add(a1, b0);
+  P.d1[poly * P.ds + l] = mont_mul(acc.redc(pc), pc.r2, pc.q, pc.qinv_neg);
   P.d2[poly * P.ds + l] = mul_mod(a1, b1, pc);
 }
 
@@ -404,23 +403,29 @@ __global__ void __launch_bounds__(kEwThreads) k_diag_mac(const __grid_constant__
   if (x >= N) return;
   const PrimeConst pc = P.pc[limb];
   const size_t l = (size_t)limb * N + x;
-  Acc128 a[NB][4];
+  Mac128 a[NB][4];
 #pragma unroll
   for (int b = 0; b < NB; ++b)
 #pragma unroll
     for (int c = 0; c < 4; ++c) a[b][c].zero();
 #pragma unroll 2
   for (int t = 0; t < P.n_terms; ++t) {
+    if (t % kMacFold == kMacFold - 1) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[b][c].fold(pc.q, pc.bar);
+    }
     const ulonglong2 p = __ldg(reinterpret_cast<const ulonglong2*>(P.pt[t] + l));
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const uint64_t* base = P.ct[t] + b * P.ct_bstride + l;
       const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(base));
       const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(base + P.ct_c1_off));
-      a[b][0].mac(v0.x, p.x, pc.q);
-      a[b][1].mac(v0.y, p.y, pc.q);
-      a[b][2].mac(v1.x, p.x, pc.q);
-      a[b][3].mac(v1.y, p.y, pc.q);
+      a[b][0].add(v0.x, p.x);
+      a[b][1].add(v0.y, p.y);
+      a[b][2].add(v1.x, p.x);
+      a[b][3].add(v1.y, p.y);
     }
   }
 #pragma unroll
@@ -428,8 +433,7 @@ __global__ void __launch_bounds__(kEwThreads) k_diag_mac(const __grid_constant__
     uint64_t r[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      r[c] = mont_mul(redc128(a[b][c].hi, a[b][c].lo, pc.q, pc.qinv_neg), pc.r2, pc.q,
-                      pc.qinv_neg);
+      r[c] = mont_mul(a[b][c].redc(pc), pc.r2, pc.q, pc.qinv_neg);
     uint64_t* o0 = P.out + b * P.out_bstride + l;
     uint64_t* o1 = o0 + P.out_c1_off;
     if (P.accumulate) {
@@ -518,7 +522,7 @@ struct Acc2 {
 template <int NS>
 __global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ ConvParams P) {
   __shared__ uint64_t s_punc[NS * kMaxPrimes];
-  __shared__ uint64_t s_q[kMaxPrimes], s_qi[kMaxPrimes];
+  __shared__ uint64_t s_q[kMaxPrimes], s_qi[kMaxPrimes], s_bar[kMaxPrimes];
   const int N = 1 << P.log_n;
   const int j = blockIdx.y;
   const int poly = blockIdx.z;
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ Con
     const PrimeConst pc = P.pc[P.dst_sel[j][t]];
     s_q[t] = pc.q;
     s_qi[t] = pc.qinv_neg;
+    s_bar[t] = pc.bar;
   }
   __syncthreads();
   const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
@@ -557,8 +562,11 @@ __global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ Con
   }
   uint64_t* dst = J.dst + poly * J.dst_stride + x;
   for (int t = 0; t < nd; ++t) {
-    const uint64_t q = s_q[t], qi = s_qi[t];
-    Acc2 a0, a1;
+    PrimeConst pt;
+    pt.q = s_q[t];
+    pt.qinv_neg = s_qi[t];
+    pt.bar = s_bar[t];
+    Mac128 a0, a1;
     a0.zero();
     a1.zero();
 #pragma unroll
@@ -567,16 +575,13 @@ __global__ void __launch_bounds__(kEwThreads) k_conv(const __grid_constant__ Con
         const uint64_t c = s_punc[i * kMaxPrimes + t];
         a0.add(h0[i], c);
         a1.add(h1[i], c);
-        if (i & 1) {
-          a0.fold(q);
-          a1.fold(q);
+        if (i % kMacFold == kMacFold - 1) {
+          a0.fold(pt.q, pt.bar);
+          a1.fold(pt.q, pt.bar);
         }
       }
     }
-    a0.fold(q);
-    a1.fold(q);
-    *reinterpret_cast<ulonglong2*>(dst + (size_t)t * N) =
-        make_ulonglong2(redc128(a0.hi, a0.lo, q, qi), redc128(a1.hi, a1.lo, q, qi));
+    *reinterpret_cast<ulonglong2*>(dst + (size_t)t * N) = make_ulonglong2(a0.redc(pt), a1.redc(pt));
   }
 }
 
@@ -632,7 +637,7 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ Ip
     }
   }
   for (int b = 0; b < P.n_batch; ++b) {
-    Acc2 b0, b1, a0, a1;
+    Mac128 b0, b1, a0, a1;
     b0.zero();
     b1.zero();
     a0.zero();
@@ -652,24 +657,18 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ Ip
         b1.add(v.y, kb[j].y);
         a0.add(v.x, ka[j].x);
         a1.add(v.y, ka[j].y);
-        if (j & 1) {
-          b0.fold(pc.q);
-          b1.fold(pc.q);
-          a0.fold(pc.q);
-          a1.fold(pc.q);
+        if (j % kMacFold == kMacFold - 1) {
+          b0.fold(pc.q, pc.bar);
+          b1.fold(pc.q, pc.bar);
+          a0.fold(pc.q, pc.bar);
+          a1.fold(pc.q, pc.bar);
         }
       }
     }
-    b0.fold(pc.q);
-    b1.fold(pc.q);
-    a0.fold(pc.q);
-    a1.fold(pc.q);
     uint64_t* o = P.acc + b * P.acc_sb + (size_t)r * N + x;
     const uint64_t q = pc.q, qn = pc.qinv_neg, r2 = pc.r2;
-    ulonglong2 vb = make_ulonglong2(mont_mul(redc128(b0.hi, b0.lo, q, qn), r2, q, qn),
-                                    mont_mul(redc128(b1.hi, b1.lo, q, qn), r2, q, qn));
-    ulonglong2 va = make_ulonglong2(mont_mul(redc128(a0.hi, a0.lo, q, qn), r2, q, qn),
-                                    mont_mul(redc128(a1.hi, a1.lo, q, qn), r2, q, qn));
+    ulonglong2 vb = make_ulonglong2(mont_mul(b0.redc(pc), r2, q, qn), mont_mul(b1.redc(pc), r2, q, qn));
+    ulonglong2 va = make_ulonglong2(mont_mul(a0.redc(pc), r2, q, qn), mont_mul(a1.redc(pc), r2, q, qn));
     if (P.accumulate) {
       const ulonglong2 pb = *reinterpret_cast<const ulonglong2*>(o);
       const ulonglong2 pa = *reinterpret_cast<const ulonglong2*>(o + (size_t)P.n_ext * N);
@@ -767,6 +766,7 @@ struct BsgsParams {
   int64_t c1_off, bstride;          // baby / output component and batch strides
   const uint64_t* pt_base;
   int64_t pt_stride;                // elements between diagonals
+  int pt_log_run;                   // diagonals stored run-compressed (see launch_bsgs)
   const int32_t* pt_idx;            // device [n_giants][n_terms], -1 = zero diagonal
   uint64_t* out;
   int64_t out_gstride;              // elements between giants' outputs
@@ -799,8 +799,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int xi = lane * 2;
   const size_t coef = (size_t)limb * N + x0 + xi;
+  // run-compressed diagonal: one stored word per 2^lr consecutive coefficients
+  const int lr = P.pt_log_run;
+  const size_t pcoef = ((size_t)limb * N + x0 + xi) >> lr;
   const int g = warp;  // local giant
-  Acc2 acc[NB][2][2];
+  Mac128 acc[NB][2][2];
 #pragma unroll
   for (int b = 0; b < NB; ++b)
 #pragma unroll
@@ -829,9 +832,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
         for (int u = 0; u < 4; ++u) {
           const int t = t0 + u;
           const int idx = t < nt ? s_idx[g * P.n_terms + tc + t] : -1;
-          pv[u] = idx >= 0 ? __ldg(reinterpret_cast<const ulonglong2*>(
-                                 P.pt_base + (size_t)idx * P.pt_stride + coef))
-                           : make_ulonglong2(0, 0);
+          if (idx < 0) {
+            pv[u] = make_ulonglong2(0, 0);
+          } else if (lr == 0) {
+            pv[u] = __ldg(reinterpret_cast<const ulonglong2*>(
+                P.pt_base + (size_t)idx * P.pt_stride + coef));
+          } else {
+            const uint64_t v = __ldg(P.pt_base + (size_t)idx * P.pt_stride + pcoef);
+            pv[u] = make_ulonglong2(v, v);
+          }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -847,15 +856,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
               acc[b][c][1].add(bv.y, pv[u].y);
             }
           }
-          if (u & 1) {
+        }
+        if ((t0 + 4) % kMacFold == 0) {  // 4 products per accumulator per t0 step
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
+          for (int b = 0; b < NB; ++b)
 #pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                acc[b][c][0].fold(pc.q);
-                acc[b][c][1].fold(pc.q);
-              }
-          }
+            for (int c = 0; c < 2; ++c) {
+              acc[b][c][0].fold(pc.q, pc.bar);
+              acc[b][c][1].fold(pc.q, pc.bar);
+            }
         }
       }
     }
@@ -867,29 +876,148 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
     for (int c = 0; c < 2; ++c) {
       uint64_t r[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        Acc2 a = acc[b][c][h];
-        a.fold(pc.q);
-        r[h] = mont_mul(redc128(a.hi, a.lo, pc.q, pc.qinv_neg), pc.r2, pc.q, pc.qinv_neg);
-      }
+      for (int h = 0; h < 2; ++h) r[h] = mont_mul(acc[b][c][h].redc(pc), pc.r2, pc.q, pc.qinv_neg);
       *reinterpret_cast<ulonglong2*>(P.out + (g0 + g) * P.out_gstride + b * P.bstride +
                                      c * P.c1_off + coef) = make_ulonglong2(r[0], r[1]);
     }
   }
 }
 
+// Run-compressed diagonals (pt_log_run >= 4): the problem per 32-coefficient
+// tile of one limb is a small GEMM, out[g][col] = sum_t P[g][t] * B[t][col],
+// with P (giants x terms, one word per run) and B (terms x NB*2*32 columns).
+// The CTA stages B and its P slice in shared memory, then each thread
+// accumulates GPT giants x 2 adjacent columns (2*GPT independent accumulators)
+// reading one 16-byte baby word and GPT/2 broadcast 16-byte P words (P is
+// stored [term][run][giant]) per term.
+constexpr int kRunTile = 32;   // coefficients per CTA
+constexpr int kRunGiants = 32; // giants per CTA (grid.z covers more)
+
+constexpr size_t bsgs_run_smem(int n_terms) {
+  return (size_t)n_terms * 2 * kRunTile * 8 + (size_t)kRunGiants * n_terms * 2 * 8;
+}
+
+// RT = runs per tile (2 for pt_log_run 4, 1 for 5); one batch element per CTA.
+template <int RT, int GPT>
+__global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
+    k_bsgs_run(const __grid_constant__ BsgsParams P) {
+  constexpr int kRunGpt = GPT;
+  extern __shared__ __align__(16) uint64_t sm[];
+  constexpr int COLS = 2 * kRunTile;  // (c0, c1) x 32 coefficients
+  constexpr int LR = RT == 2 ? 4 : 5;
+  const int N = 1 << P.log_n;
+  const int limb = blockIdx.y;
+  const int x0 = blockIdx.x * kRunTile;
+  const int g0 = blockIdx.z * kRunGiants;
+  const int T = P.n_terms;
+  uint64_t* bab = sm;                     // [T][2][32]
+  uint64_t* pts = sm + (size_t)T * COLS;  // [T][RT][32 giants]
+  for (int e = threadIdx.x; e < T * COLS / 2; e += blockDim.x) {
+    const int t = e / (COLS / 2), rem = e - t * (COLS / 2);
+    const int c = rem / (kRunTile / 2), xx = (rem - c * (kRunTile / 2)) * 2;
+    cp_async16(bab + (size_t)t * COLS + c * kRunTile + xx,
+               P.baby[t] + c * P.c1_off + (size_t)limb * N + x0 + xx);
+  }
+  const size_t pcol = ((size_t)limb * N + x0) >> LR;
+  for (int e = threadIdx.x; e < kRunGiants * T; e += blockDim.x) {
+    const int g = e / T, t = e - g * T;
+    const int idx = g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + t) : -1;
+    uint64_t* d = pts + (size_t)t * RT * kRunGiants + g;
+    if (RT == 2) {
+      const ulonglong2 v = idx < 0 ? make_ulonglong2(0, 0)
+                                   : __ldg(reinterpret_cast<const ulonglong2*>(
+                                         P.pt_base + (size_t)idx * P.pt_stride + pcol));
+      d[0] = v.x;
+      d[kRunGiants] = v.y;
+    } else {
+      d[0] = idx < 0 ? 0 : __ldg(P.pt_base + (size_t)idx * P.pt_stride + pcol);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  constexpr int PAIRS = kRunTile;  // (c, x pair)
+  const int p = threadIdx.x % PAIRS, gg = threadIdx.x / PAIRS;
+  const int c = p / (kRunTile / 2), xl = (p % (kRunTile / 2)) * 2;
+  const int run = xl >> LR;
+  const PrimeConst pc = P.pc[limb];
+  // products < q^2; fold often enough to stay below 2^128 (see Mac128)
+  const int fold_every = pc.q < (1ull << 61) ? 32 : kMacFold;
+  Mac128 acc[kRunGpt][2];
+#pragma unroll
+  for (int g = 0; g < kRunGpt; ++g) {
+    acc[g][0].zero();
+    acc[g][1].zero();
+  }
+  const uint64_t* pt_g = pts + run * kRunGiants + gg * kRunGpt;
+  const uint64_t* bab_c = bab + c * kRunTile + xl;
+#pragma unroll 2
+  for (int t = 0; t < T; ++t) {
+    const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(bab_c + (size_t)t * COLS);
+    const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(pt_g + (size_t)t * RT * kRunGiants);
+#pragma unroll
+    for (int h = 0; h < kRunGpt / 2; ++h) {
+      const ulonglong2 pv = pp[h];
+      acc[2 * h][0].add(bv.x, pv.x);
+      acc[2 * h][1].add(bv.y, pv.x);
+      acc[2 * h + 1][0].add(bv.x, pv.y);
+      acc[2 * h + 1][1].add(bv.y, pv.y);
+    }
+    if ((t + 1) % fold_every == 0) {
+#pragma unroll
+      for (int g = 0; g < kRunGpt; ++g) {
+        acc[g][0].fold(pc.q, pc.bar);
+        acc[g][1].fold(pc.q, pc.bar);
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < kRunGpt; ++g) {
+    const int gi = g0 + gg * kRunGpt + g;
+    if (gi >= P.n_giants) break;
+    const uint64_t r0 = mont_mul(acc[g][0].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+    const uint64_t r1 = mont_mul(acc[g][1].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+    *reinterpret_cast<ulonglong2*>(P.out + (size_t)gi * P.out_gstride + c * P.c1_off +
+                                   (size_t)limb * N + x0 + xl) = make_ulonglong2(r0, r1);
+  }
+}
+
+template <int RT, int GPT>
+static void launch_bsgs_run_g(const BsgsParams& P, int k, cudaStream_t st) {
+  const size_t smem = bsgs_run_smem(P.n_terms);
+  static bool attr_set = false;
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(k_bsgs_run<RT, GPT>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bsgs_run_smem(kBsgsMaxTerms)),
+               "bsgs smem attr");
+    attr_set = true;
+  }
+  dim3 grid((1 << P.log_n) / kRunTile, k, (P.n_giants + kRunGiants - 1) / kRunGiants);
+  k_bsgs_run<RT, GPT><<<grid, 32 * (kRunGiants / GPT), smem, st>>>(P);
+}
+
+// 4 giants x 2 columns per thread (8 accumulators, 256 threads): measured
+// 1.38 T products/s vs 1.19 (8 giants, 128 threads) and 1.00 (2 giants) on
+// the CtS shape; the register-only ceiling of Mac128 is 2.16 T/s.
+template <int RT>
+static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
+  launch_bsgs_run_g<RT, 4>(P, k, st);
+}
+
 template <int NB>
 static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
-  constexpr int W = NB == 1 ? 32 : 16;  // 64 / 128 registers per thread
+  constexpr int W = 16;  // <= 128 registers per thread (7-word accumulators)
   dim3 grid((1 << P.log_n) / kBsgsTile, k, (P.n_giants + W - 1) / W);
   k_bsgs<NB, W><<<grid, W * 32, 0, st>>>(P);
 }
 
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
                  int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
-                 int64_t pt_stride, const int32_t* pt_idx, int n_giants, uint64_t* out,
-                 int64_t out_gstride, int k, cudaStream_t st) {
+                 int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
+                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st) {
   if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
+  if (pt_log_run < 0 || pt_log_run > 5 || pt_log_run >= log_n)
+    throw HegpuError{HEGPU_E_ARG, "bsgs: pt_log_run must be in [0, 5]"};
   if ((1 << log_n) % kBsgsTile) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
   const int max_giants = 1 << 20;  // giant groups are a grid dimension
   for (int b0 = 0; b0 < n_batch; b0 += 2) {
@@ -905,18 +1033,34 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
       P.bstride = bstride;
       P.pt_base = pt_base;
       P.pt_stride = pt_stride;
+      P.pt_log_run = pt_log_run;
       P.pt_idx = pt_idx + (size_t)g0 * n_terms;
       P.out = out + (size_t)g0 * out_gstride + b0 * bstride;
       P.out_gstride = out_gstride;
       P.pc = dpc;
       const double el = (double)k * (1 << log_n);
       ProfScope ps(PROF_DIAG_MAC, st,
-                   el * 8.0 * ((double)P.n_giants * n_terms + 2.0 * nb * (n_terms + P.n_giants)),
+                   el * 8.0 * ((double)P.n_giants * n_terms / (1 << pt_log_run) +
+                               2.0 * nb * (n_terms + P.n_giants)),
                    el * 2.0 * nb * ((double)P.n_giants * n_terms + P.n_giants));
-      if (nb == 1)
+      if (pt_log_run >= 4 && (1 << log_n) % kRunTile == 0) {
+        // one batch element per launch: 16 accumulators per thread at 3 CTAs/SM
+        // (the compressed diagonals are re-read per element, 1/16 of a baby)
+        for (int bi = 0; bi < nb; ++bi) {
+          BsgsParams Q = P;
+          for (int t = 0; t < n_terms; ++t) Q.baby[t] = P.baby[t] + bi * bstride;
+          Q.out = P.out + bi * bstride;
+          Q.n_batch = 1;
+          if (pt_log_run == 4)
+            launch_bsgs_run<2>(Q, k, st);
+          else
+            launch_bsgs_run<1>(Q, k, st);
+        }
+      } else if (nb == 1) {
         launch_bsgs_nb<1>(P, k, st);
-      else
+      } else {
         launch_bsgs_nb<2>(P, k, st);
+      }
       check_cuda(cudaGetLastError(), "bsgs launch");
     }
   }

@@ -216,10 +216,25 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
 // register-radix passes (N >= 2^12): one warp per S-point sub-transform
 // ---------------------------------------------------------------------------
 
-constexpr int kRegWarps = 8;
+constexpr int kRegWarps = 8;  // the blocks pass's twiddle re-basing assumes 2^3 warps
+static_assert(kRegWarps == 8, "k_ntt_blocks_r twiddle staging uses log2(kRegWarps) == 3");
+
+// Shared memory of the register passes (bytes): the cols pass holds its
+// S x 8 tile, the warp buffers and the S twiddle pairs of stages [0, LOGS);
+// the blocks pass holds the warp buffers and its 8 blocks' twiddle pairs
+// (8 * S, re-based so block-local index = (8 << st) + (warp << st) + i).
+template <int LOGS>
+constexpr size_t cols_r_smem() {
+  return ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8 +
+         (size_t)(1 << LOGS) * 16;
+}
+template <int LOGS>
+constexpr size_t blocks_r_smem() {
+  return (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8 + (size_t)kRegWarps * (1 << LOGS) * 16;
+}
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 5)) k_ntt_cols_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   constexpr int TS = kRegWarps + 1;  // padded tile row (conflict-free column reads)
@@ -241,6 +256,9 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
   uint64_t* tile = sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + S * TS + kRegWarps * Sh::PAD_S);
+  // every column transform of this pass uses twiddles [1, S) of its table
+  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tw + i);
   const int c0 = blockIdx.x * kRegWarps;
   if (!INV && sg.csrc != nullptr && sg.cmode == 1) {
     // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
@@ -259,18 +277,15 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
     for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
       const int r = e / kRegWarps, c = e % kRegWarps;
       const size_t x = c0 + c + (size_t)C * r;
-      uint64_t hi = 0, lo = 0;
+      Mac128 acc;
+      acc.zero();
       for (int i = 0; i < sg.c_nsrc; ++i) {
         const uint64_t h = __ldg(hs + (size_t)i * N + x);
         const uint64_t m = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
-        const uint64_t plo = h * m, phi = __umul64hi(h, m);
-        const uint64_t nlo = lo + plo;
-        hi = hi + phi + (nlo < lo);
-        lo = nlo;
-        if (i & 1) hi = hi >= q ? hi - q : hi;
+        acc.add(h, m);
+        if (i % kMacFold == kMacFold - 1) acc.fold(q, pc.bar);
       }
-      hi = hi >= q ? hi - q : hi;
-      tile[r * TS + c] = redc128(hi, lo, q, pc.qinv_neg);
+      tile[r * TS + c] = acc.redc(pc);
     }
   } else {
     for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
@@ -278,15 +293,16 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
       tile[r * TS + c] = src[c0 + c + (size_t)C * r];
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
   uint64_t x[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
   if (!INV)
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, tw, pc.q);
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, stw, pc.q);
   else
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, tw, pc,
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc,
                   P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh),
                   P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
@@ -299,7 +315,7 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_cols_r(const _
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 4)) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
@@ -322,12 +338,25 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const
                             : (sg.out + poly * sg.out_stride + off);
   uint64_t* dst = sg.out + poly * sg.out_stride + off;
   uint64_t* wbuf = sm + warp * Sh::PAD_S;
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kRegWarps * Sh::PAD_S);
   constexpr int LO_S = LOGS - EB;
   uint64_t x[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
+  {
+    // stage st of blocks [blk0, blk0 + 8) uses global twiddles
+    // (1 << (a + st)) + (blk0 << st) + [0, 8 << st)  ->  smem (8 << st) + ...
+    const int blk0 = blockIdx.x * kRegWarps;
+    for (int v = kRegWarps + threadIdx.x; v < kRegWarps * S; v += blockDim.x) {
+      const int st = 31 - __clz(v) - 3;
+      const int i = v - (kRegWarps << st);
+      cp_async16(stw + v, tw + (1 << (a + st)) + (blk0 << st) + i);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
   if (!INV) {
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, a, blk, tw, q);
+    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 3, warp, stw, q);
     if (P.epi) {
       const uint64_t* other = sg.other + poly * sg.other_stride + off;
       uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
@@ -350,7 +379,8 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 3 : 5)) k_ntt_blocks_r(const
       dst[lane + 32 * e] = y >= q ? y - q : y;
     }
   } else {
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, 0, blk, tw, pc,
+    // re-based table: log_n' = LOGS + 3 (the last-stage scaling is never in this pass)
+    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + 3, 0, warp, stw, pc,
                   make_ulonglong2(pc.ninv, pc.ninv_sh), make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
     for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
@@ -362,7 +392,7 @@ static void launch_cols_r(bool inverse, const NttParams& P, int n_rows, int log_
                           cudaStream_t st) {
   const int C = (1 << log_n) >> LOGS;
   dim3 grid(C / kRegWarps, n_rows);
-  const size_t smem = ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8;
+  const size_t smem = cols_r_smem<LOGS>();
   static bool attr_set = false;  // opt in to > 48 KiB dynamic shared memory once
   if (!attr_set) {
     check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, true>,
@@ -384,7 +414,17 @@ static void launch_blocks_r(bool inverse, const NttParams& P, int n_rows, int lo
                             cudaStream_t st) {
   const int R = (1 << log_n) >> LOGS;
   dim3 grid(R / kRegWarps, n_rows);
-  const size_t smem = (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8;
+  const size_t smem = blocks_r_smem<LOGS>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(k_ntt_blocks_r<LOGS, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    check_cuda(cudaFuncSetAttribute(k_ntt_blocks_r<LOGS, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    attr_set = true;
+  }
   if (inverse)
     k_ntt_blocks_r<LOGS, true><<<grid, 32 * kRegWarps, smem, st>>>(P);
   else

@@ -12,6 +12,11 @@
 // Twiddle indices are the reference's psi_rev[m + i] / ipsi_rev[h + i]
 // (hebert/_kernels.py:152-203) expressed in global stage/group terms, so the
 // output is bit-identical to the CT/GS transforms.
+//
+// The kernels stage the twiddles a CTA needs in shared memory first (the
+// round functions index `tw` with the same formulas, on a re-based table),
+// so the butterflies' twiddle reads are shared-memory loads instead of
+// long-latency global loads on the dependency chain.
 #pragma once
 #include "common.cuh"
 
@@ -30,6 +35,7 @@ __device__ __forceinline__ int reg_j(int lane, int e, int lo, int eb) {
   return (lane & ((1 << lo) - 1)) | (e << lo) | ((lane >> lo) << (lo + eb));
 }
 __device__ __forceinline__ int padi(int j) { return j + (j >> 4); }
+
 
 // Forward CT butterflies on register window [lo, lo+EB) for bit positions
 // p = phi down to plo (t = 2^p within the sub-transform).  Twiddle index of
@@ -54,7 +60,7 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
       const int ti = base + (j >> (p + 1));
       uint64_t u = x[e];
       u = u >= q2 ? u - q2 : u;
-      const ulonglong2 wp = __ldg(tw + ti);
+      const ulonglong2 wp = tw[ti];
       const uint64_t v = shoup_lazy(x[e + d], wp.x, wp.y, q);
       x[e] = u + v;
       x[e + d] = u - v + q2;
@@ -93,7 +99,7 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
         const int j = reg_j(lane, e, lo, EB);
         const int ti = base + (j >> (p + 1));
         x[e] = s;
-        const ulonglong2 wp = __ldg(tw + ti);
+        const ulonglong2 wp = tw[ti];
         x[e + d] = shoup_lazy(df, wp.x, wp.y, q);
       } else {
         x[e] = shoup(s, fin_s.x, fin_s.y, q);

@@ -25,8 +25,12 @@ void check_cuda(cudaError_t e, const char* what) {
 static std::atomic<long long> g_launches{0};
 static std::atomic<bool> g_prof_on{false};
 static std::mutex g_prof_mu;
+static thread_local int g_ntt_tag = NTT_TAG_OTHER;
+NttTagScope::NttTagScope(int tag) : prev(g_ntt_tag) { g_ntt_tag = tag; }
+NttTagScope::~NttTagScope() { g_ntt_tag = prev; }
+
 struct ProfRec {
-  int cls;
+  int cls, sub;
   double bytes, modmuls;
   cudaEvent_t a, b;
 };
@@ -37,6 +41,7 @@ ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double modmuls) : st
   if (!g_prof_on.load(std::memory_order_relaxed)) return;
   ProfRec r;
   r.cls = cls;
+  r.sub = cls == PROF_NTT ? g_ntt_tag : 0;
   r.bytes = bytes;
   r.modmuls = modmuls;
   cudaEventCreate(&r.a);
@@ -371,6 +376,7 @@ static void ntt_simple(Ring& R, bool inverse, const uint64_t* in, int64_t is, ui
 // ext[b][j][t][N] (t < n_ext - |group j|).  dcoeff: B*(level+1)*N scratch.
 static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, int B,
                      uint64_t* dcoeff, uint64_t* ext, cudaStream_t st) {
+  NttTagScope tag_(NTT_TAG_MODUP);
   const int level = L.level, alpha = L.alpha;
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
@@ -497,6 +503,7 @@ static void ks_ip(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, cons
 static void ks_moddown(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr, int B,
                        uint64_t* out_b, int64_t os_b, uint64_t* out_a, int64_t os_a,
                        cudaStream_t st, bool acc_b, bool acc_a) {
+  NttTagScope tag_(NTT_TAG_MODDOWN);
   const int level = L.level;
   const int k = level + 1, K = R.n_special, n_ext = L.n_ext;
   const size_t N = R.n;
@@ -705,6 +712,7 @@ static void bsgs_giants_impl(Ring& R, int level, int alpha, const uint64_t* part
 
 static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uint64_t* out,
                          int64_t os, int P, cudaStream_t st) {
+  NttTagScope tag_(NTT_TAG_RESCALE);
   if (level < 1 || level >= R.n_chain) throw HegpuError{HEGPU_E_ARG, "rescale level out of range"};
   if (P <= 0) return;
   const size_t N = R.n;
@@ -744,6 +752,7 @@ static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uin
 
 static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* out, int64_t os,
                            int P, int to_level, cudaStream_t st) {
+  NttTagScope tag_(NTT_TAG_RESCALE);
   if (to_level < 0 || to_level >= R.n_chain) throw HegpuError{HEGPU_E_ARG, "bad target level"};
   if (P <= 0) return;
   const size_t N = R.n;
@@ -943,11 +952,13 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
     for (auto& r : g_prof) {
       float t = 0;
       check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "event time");
-      if (r.cls < n_classes) {
-        ms[r.cls] += t;
-        counts[r.cls] += 1;
-        bytes[r.cls] += r.bytes;
-        modmuls[r.cls] += r.modmuls;
+      const int sub = r.sub > 0 ? PROF_NUM_CLASSES + r.sub - 1 : -1;
+      for (int c : {r.cls, sub}) {
+        if (c < 0 || c >= n_classes) continue;
+        ms[c] += t;
+        counts[c] += 1;
+        bytes[c] += r.bytes;
+        modmuls[c] += r.modmuls;
       }
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -1142,13 +1153,13 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
 
 int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
                int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
-               const int32_t* pt_idx, int n_giants, uint64_t* out, int64_t out_gstride, int k,
-               void* stream) {
+               int pt_log_run, const int32_t* pt_idx, int n_giants, uint64_t* out,
+               int64_t out_gstride, int k, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
     launch_bsgs(R.dpc, R.log_n, babies, n_terms, c1_off, bstride, n_batch, pt_base, pt_stride,
-                pt_idx, n_giants, out, out_gstride, k, S_(stream));
+                pt_log_run, pt_idx, n_giants, out, out_gstride, k, S_(stream));
   })
 }
 

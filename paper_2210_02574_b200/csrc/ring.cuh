@@ -100,6 +100,14 @@ enum ProfClass {
 };
 // bytes / modmuls: ALGORITHMIC traffic and modular multiplications of the
 // launch (each input read once, each output written once).
+// NTT launches are additionally attributed to the step that issued them
+// (profile classes after PROF_NUM_CLASSES: ntt_modup, ntt_moddown, ntt_rescale).
+enum NttTag { NTT_TAG_OTHER = 0, NTT_TAG_MODUP, NTT_TAG_MODDOWN, NTT_TAG_RESCALE, NTT_TAG_N };
+struct NttTagScope {
+  int prev;
+  explicit NttTagScope(int tag);
+  ~NttTagScope();
+};
 struct ProfScope {
   int slot = -1;
   cudaStream_t st;
@@ -211,7 +219,7 @@ void launch_ks_ip(IpParams& P, cudaStream_t st);
 double bench_modmul_peak(int iters);
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
                  int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
-                 int64_t pt_stride, const int32_t* pt_idx, int n_giants, uint64_t* out,
-                 int64_t out_gstride, int k, cudaStream_t st);
+                 int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
+                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st);
 
 }  // namespace hegpu

@@ -130,3 +130,44 @@ def test_batched_ops_equal_single():
     for i, x in enumerate(polys):
         assert np.array_equal(prod.limbs[i], ring.poly_mul(x, other).limbs)
         assert np.array_equal(coeff.limbs[i], ring.to_coeff(x).limbs)
+
+
+@pytest.mark.parametrize("lr", [2, 4, 5])
+def test_bsgs_run_compressed_matches_dense_and_exact(lr):
+    """hegpu_bsgs on run-compressed diagonals (pt_log_run, the sparse-bootstrap
+    cache layout; lr >= 4 takes the shared-memory GEMM kernel) equals the dense
+    kernel on the expanded diagonals and the exact sum mod q."""
+    import ctypes
+
+    import torch
+
+    from paper_2210_02574_b200 import _dev, _lib, ckks
+
+    params = ckks.get_preset("desk")
+    n, k, T, G, nb = params.ring_degree, 3, 21, 5, 2
+    qs = [int(q) for q in params.ring.moduli_chain[:k]]
+    rng = np.random.default_rng(lr)
+
+    def rand(shape):
+        return np.stack([rng.integers(0, q, shape[:-2] + (shape[-1],), dtype=np.uint64)
+                         for q in qs], axis=-2)
+
+    babies = _dev.to_device(rand((T, nb, 2, k, n)).view(np.int64))
+    pts_c = rand((9, k, n >> lr))
+    idx = rng.integers(-1, 9, (G, T)).astype(np.int32)
+    idx_d = torch.from_numpy(idx).to(_dev.device())
+    ptrs = (ctypes.c_void_p * T)(*[babies[t].data_ptr() for t in range(T)])
+    outs = []
+    for run_log, pts in ((lr, pts_c), (0, np.repeat(pts_c, 1 << lr, axis=-1))):
+        pd = _dev.to_device(np.ascontiguousarray(pts).view(np.int64))
+        out = _dev.empty(G, nb, 2, k, n)
+        _lib.call("hegpu_bsgs", params.ring.device(), ptrs, T, k * n, 2 * k * n, nb,
+                  pd.data_ptr(), k * (n >> run_log), run_log, idx_d.data_ptr(), G,
+                  out.data_ptr(), nb * 2 * k * n, k, _dev.stream())
+        outs.append(out.cpu().numpy().view(np.uint64))
+    assert np.array_equal(outs[0], outs[1])
+    bab = babies.cpu().numpy().view(np.uint64)
+    for (g, b, c, l, x) in [(0, 0, 0, 0, 0), (4, 1, 1, 2, n - 1), (2, 1, 0, 1, 37)]:
+        want = sum(int(pts_c[idx[g, t], l, x >> lr]) * int(bab[t, b, c, l, x])
+                   for t in range(T) if idx[g, t] >= 0) % qs[l]
+        assert int(outs[0][g, b, c, l, x]) == want

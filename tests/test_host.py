@@ -146,3 +146,29 @@ def test_wrapping_allreduce_contract():
     want = np.stack([sum(r[i].astype(object) for r in ranks) % q for i, q in enumerate(primes)])
     assert got.astype(object).tolist() == want.tolist()
     assert shard.refresh_owner(0, 1) == 0 and shard.refresh_owner(1, 2) == 1
+
+
+def test_periodic_diagonal_run_compression():
+    """Slot vectors periodic with period P encode to polynomials in X^(N/2P)
+    (the small-ring embedding the diagonal cache uses), whose evaluation
+    vectors are constant on runs of N/2P coefficients in the reference's
+    bit-reversed NTT order -- the layout hegpu_bsgs reads (pt_log_run)."""
+    from oracle import scheme as S
+    from paper_2210_02574_b200 import bootstrap as bs
+
+    p = S.Params.from_text(preset_text("p14"))
+    n = p.n
+    rng = np.random.default_rng(4)
+    for period in (n // 8, n // 32):
+        r = n // (2 * period)
+        v = rng.uniform(-1, 1, period) + 1j * rng.uniform(-1, 1, period)
+        dense = bs._coeffs_from_rows(n, np.tile(v, (n // 2) // period)[None], 2.0 ** 20)
+        emb = np.zeros((1, n))
+        emb[:, ::r] = bs._coeffs_from_rows(2 * period, v[None], 2.0 ** 20)
+        assert np.max(np.abs(dense - emb)) <= 1
+        assert not np.any(np.delete(dense, np.s_[::r], axis=1))
+        primes = list(p.chain[:2])
+        ev = S.ntt_fwd(p, S.from_signed(emb[0].astype(np.int64), primes), primes)
+        runs = ev.reshape(len(primes), n // r, r)
+        assert (runs == runs[..., :1]).all()
+        assert bs._run_log(type("P", (), {"ring_degree": n})(), period) == min(r.bit_length() - 1, 5)
