@@ -105,6 +105,7 @@ int hegpu_ntt(hegpu_ring_t ring, int inverse, const uint64_t* in, int64_t in_str
 #define HEGPU_OP_COPY 8 /* out = a                                             */
 #define HEGPU_OP_ADDC 9 /* a + c[l], c natural per limb (constant add_plain)   */
 #define HEGPU_OP_REDUCE 10 /* a mod q for any 64-bit a (after a wrapping NCCL sum) */
+#define HEGPU_OP_AXPYC 11 /* b + a * c[l], c natural per limb                  */
 
 /* Elementwise op over a poly group.  b may be NULL for unary ops; consts is a
  * host array of k per-limb scalars for SCALAR / ROWMONT. */
@@ -159,6 +160,20 @@ int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
                    int64_t d_stride, int n_batch, const uint64_t* const* key_b,
                    const uint64_t* const* key_a, int n_digits, uint64_t* out_b,
                    uint64_t* out_a, int64_t out_stride, int accumulate, void* stream);
+
+/* Key switch fused with the following rescale (relinearize-then-rescale of
+ * mult, ops.py:346-367): for each batch element b,
+ *   out.c{0,1} = round((P * in.c{0,1} + KS(d).{b,a}) / (P * q_level))
+ * at level-1, by ONE ModDown from the basis {q_level} + P.  Decrypts like
+ * hegpu_ks_apply(accumulate=3) followed by hegpu_rescale (same message and
+ * scale); limbs differ by the conversion rounding.  in.c0 at in +
+ * b*in_stride, c1 at + in_c1_off (level+1 limbs, may be clobbered); out
+ * likewise with `level` limbs.  Needs level >= 1. */
+int hegpu_ks_apply_rescale(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
+                           int64_t d_stride, int n_batch, const uint64_t* const* key_b,
+                           const uint64_t* const* key_a, int n_digits, uint64_t* in,
+                           int64_t in_stride, int64_t in_c1_off, uint64_t* out,
+                           int64_t out_stride, int64_t out_c1_off, void* stream);
 
 /* Hoisted rotations of one (batched) ciphertext by n_rot Galois elements
  * (the bootstrap baby steps, bootstrap.py:214-217): ModUp of c1 once, then

@@ -11,8 +11,10 @@ once per batch.  Batched and unbatched operands broadcast (a shared weight
 ciphertext against a batch of data ciphertexts).
 """
 
+import contextlib
 import logging
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -26,6 +28,30 @@ from . import keys as keysmod
 from .encoding import Plaintext, decode, decode_real, encode, encode_coeffs
 
 log = logging.getLogger(__name__)
+
+_mode = threading.local()
+
+
+@contextlib.contextmanager
+def fused_rescale(enabled=True):
+    """Inside this context `mult(..., rescale_after=True)` relinearizes and
+    rescales with ONE ModDown from the basis {q_level} + P
+    (hegpu_ks_apply_rescale) instead of the reference's ModDown-then-rescale:
+    same message and scale, limbs differ by the conversion rounding, and the
+    separate rescale's INTT/NTT of every limb disappears.  The public API is
+    reference-exact by default; the bootstrap and the trainer use this for
+    their internal products (their results are tolerance-checked)."""
+    prev = getattr(_mode, "fused", False)
+    _mode.fused = enabled
+    try:
+        yield
+    finally:
+        _mode.fused = prev
+
+
+def fused_rescale_enabled():
+    return getattr(_mode, "fused", False)
+
 
 SCALE_MATCH_RTOL = 2.0 ** -10
 SCALE_EXACT_RTOL = 1e-9
@@ -519,6 +545,20 @@ def mult(ct1, ct2, relin_key_or_keyset, rescale_after=True):
     k = level + 1
     n = params.ring_degree
     d2 = rg.RnsPoly(ring, d[..., 2, :, :], rg.EVAL, level)
+    if rescale_after and fused_rescale_enabled():
+        out = _packed(params, tuple(d.shape[:-3]), level - 1)
+        dp, cnt, ds = d2._group()
+        kb, ka = keyset.relin_key.ptr_arrays()
+        _stats.count("ks", level, cnt)
+        _stats.count("rescale_poly", level, 2 * cnt)
+        _lib.call(
+            "hegpu_ks_apply_rescale", ring.device(), level, params.digit_size, dp, ds, cnt, kb, ka,
+            keyset.relin_key.dnum, d.data_ptr(), 3 * k * n, k * n, out.data_ptr(),
+            2 * level * n, level * n, _dev.stream(),
+        )
+        q_l = ring.moduli_chain[level]
+        return _ct(out, level - 1, ct1.scale * ct2.scale / q_l, ct1.slot_count, params,
+                   ct1.insecure_provenance or ct2.insecure_provenance)
     # (d0, d1) += KS(d2): the ModDown epilogue accumulates in place
     keysmod.ks_apply_into(keyset, keyset.relin_key, d2, d[..., 0, :, :].data_ptr(),
                           d[..., 1, :, :].data_ptr(), 3 * k * n, 3)

@@ -198,11 +198,20 @@ struct Seg {
   const uint64_t* cpunc;
   int c_nsrc;
   int cpunc_ld;
-  int eacc;  // epilogue accumulates: eout = eout + (other - y) * c
+  int eacc;  // epilogue: 1 -> eout += (other - y) * c; 2 -> eout = ein * s + (other - y) * c
+  const uint64_t* ein;
+  int64_t ein_stride;
   // cmode 1: the prologue instead lifts one coefficient-form limb (modulus
   // csrc_q, at csrc + p*csrc_stride) centered into every limb (rescale/ModRaise)
+  // cmode 2: conversion of the CENTERED representative: the overflow count
+  // e = round(sum_i hat_i / d_i) is estimated in fp32 from (hat_i >> cfs[i]) *
+  // cfw[i] (cfw = 2^cfs / d_i; both read at stride 2, one per 64-bit word)
+  // and e * cnegd[t] (= -D R mod p_t) is added
   int cmode;
   uint64_t csrc_q;
+  const uint64_t* cnegd;
+  const float* cfw;
+  const int32_t* cfs;
 };
 
 struct SegSet {

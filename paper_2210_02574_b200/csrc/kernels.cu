@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kEwThreads) k_elementwise(const __grid_constan
   const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(P.a + poly * P.as + la);
   ulonglong2 vb = make_ulonglong2(0, 0);
   if (OP == HEGPU_OP_ADD || OP == HEGPU_OP_SUB || OP == HEGPU_OP_MUL || OP == HEGPU_OP_MONT ||
-      OP == HEGPU_OP_FMA)
+      OP == HEGPU_OP_FMA || OP == HEGPU_OP_AXPYC)
     vb = *reinterpret_cast<const ulonglong2*>(P.b + poly * P.bs + la);
   uint64_t* op = P.o + poly * P.os + la;
   ulonglong2 r;
@@ -68,6 +68,9 @@ __global__ void __launch_bounds__(kEwThreads) k_elementwise(const __grid_constan
   } else if (OP == HEGPU_OP_ADDC) {
     r.x = add_mod(va.x, P.c[limb], q);
     r.y = add_mod(va.y, P.c[limb], q);
+  } else if (OP == HEGPU_OP_AXPYC) {
+    r.x = add_mod(vb.x, shoup(va.x, P.c[limb], P.csh[limb], q), q);
+    r.y = add_mod(vb.y, shoup(va.y, P.c[limb], P.csh[limb], q), q);
   } else if (OP == HEGPU_OP_FMA) {
     const ulonglong2 acc = *reinterpret_cast<const ulonglong2*>(op);
     r.x = add_mod(acc.x, mul_mod(va.x, vb.x, pc), q);
@@ -108,20 +111,21 @@ void launch_elementwise(const PrimeConst* dpc, const std::vector<uint64_t>& hq, 
     if (A.consts) {
       const uint64_t q = hq[p];
       P.c[l] = A.consts[l];
-      if (A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ADDC) {
+      if (A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ADDC || A.op == HEGPU_OP_AXPYC) {
         if (A.consts[l] >= q) throw HegpuError{HEGPU_E_ARG, "scalar not reduced"};
         P.csh[l] = h_shoup(A.consts[l], q);
       }
     }
   }
-  if ((A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ROWMONT || A.op == HEGPU_OP_ADDC) &&
+  if ((A.op == HEGPU_OP_SCALAR || A.op == HEGPU_OP_ROWMONT || A.op == HEGPU_OP_ADDC ||
+       A.op == HEGPU_OP_AXPYC) &&
       !A.consts)
     throw HegpuError{HEGPU_E_ARG, "scalar op needs consts"};
   const int n = 1 << log_n;
   if (n < 2) throw HegpuError{HEGPU_E_ARG, "N too small"};
   const dim3 grid = rows_grid(n, rows, 2);
   const bool two_in = A.op == HEGPU_OP_ADD || A.op == HEGPU_OP_SUB || A.op == HEGPU_OP_MUL ||
-                      A.op == HEGPU_OP_MONT || A.op == HEGPU_OP_FMA;
+                      A.op == HEGPU_OP_MONT || A.op == HEGPU_OP_FMA || A.op == HEGPU_OP_AXPYC;
   const double ew_elems = (double)rows * n;
   const double ew_mm = (A.op == HEGPU_OP_MUL || A.op == HEGPU_OP_FMA) ? 2 * ew_elems
                        : (A.op == HEGPU_OP_MONT || A.op == HEGPU_OP_SCALAR ||
@@ -140,6 +144,7 @@ void launch_elementwise(const PrimeConst* dpc, const std::vector<uint64_t>& hq, 
     case HEGPU_OP_COPY: k_elementwise<HEGPU_OP_COPY><<<grid, kEwThreads, 0, st>>>(P); break;
     case HEGPU_OP_ADDC: k_elementwise<HEGPU_OP_ADDC><<<grid, kEwThreads, 0, st>>>(P); break;
     case HEGPU_OP_REDUCE: k_elementwise<HEGPU_OP_REDUCE><<<grid, kEwThreads, 0, st>>>(P); break;
+    case HEGPU_OP_AXPYC: k_elementwise<HEGPU_OP_AXPYC><<<grid, kEwThreads, 0, st>>>(P); break;
     default: throw HegpuError{HEGPU_E_ARG, "unknown elementwise op"};
   }
   check_cuda(cudaGetLastError(), "elementwise launch");

@@ -34,6 +34,8 @@ struct NttParams {
   int epi;
   uint64_t c[kMaxPrimes];
   uint64_t csh[kMaxPrimes];
+  uint64_t es[kMaxPrimes];  // eacc == 2 input scale (Shoup pairs)
+  uint64_t essh[kMaxPrimes];
   // inverse with post-scale: final-stage constants per limb (sum, difference)
   int post;
   ulonglong2 fin_s[kMaxPrimes];
@@ -178,7 +180,11 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
         y = y >= q2 ? y - q2 : y;
         y = y >= q ? y - q : y;
         uint64_t r = shoup(other[e] + q - y, cc, ccsh, q);
-        if (sg.eacc) r = add_mod(r, eout[e], q);
+        if (sg.eacc == 1) r = add_mod(r, eout[e], q);
+        if (sg.eacc == 2) {
+          const uint64_t* ein = sg.ein + poly * sg.ein_stride + (size_t)limb * N + base;
+          r = add_mod(r, shoup(ein[e], P.es[limb], P.essh[limb], q), q);
+        }
         eout[e] = r;
       }
       return;
@@ -274,16 +280,26 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 5)) k_ntt_cols_r(const _
     // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
     const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
     const uint64_t q = pc.q;
+    const bool centered = sg.cmode == 2;
+    const uint64_t negd = centered ? __ldg(sg.cnegd + limb) : 0;
     for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
       const int r = e / kRegWarps, c = e % kRegWarps;
       const size_t x = c0 + c + (size_t)C * r;
       Mac128 acc;
       acc.zero();
+      float f = 0.f;
       for (int i = 0; i < sg.c_nsrc; ++i) {
         const uint64_t h = __ldg(hs + (size_t)i * N + x);
         const uint64_t m = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
         acc.add(h, m);
+        if (centered)
+          f = fmaf(__uint2float_rn(static_cast<uint32_t>(h >> __ldg(sg.cfs + 2 * i))),
+                   __ldg(sg.cfw + 2 * i), f);
         if (i % kMacFold == kMacFold - 1) acc.fold(q, pc.bar);
+      }
+      if (centered) {
+        if (sg.c_nsrc % kMacFold == 0) acc.fold(q, pc.bar);
+        acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
       }
       tile[r * TS + c] = acc.redc(pc);
     }
@@ -367,7 +383,11 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 4)) k_ntt_blocks_r(const
         y = y >= q2 ? y - q2 : y;
         y = y >= q ? y - q : y;
         uint64_t r = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
-        if (sg.eacc) r = add_mod(r, eout[lane + 32 * e], q);
+        if (sg.eacc == 1) r = add_mod(r, eout[lane + 32 * e], q);
+        if (sg.eacc == 2)
+          r = add_mod(r, shoup(sg.ein[poly * sg.ein_stride + off + lane + 32 * e], P.es[limb],
+                               P.essh[limb], q),
+                      q);
         eout[lane + 32 * e] = r;
       }
       return;
@@ -477,6 +497,8 @@ void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inve
     for (int i = 0; i < kMaxPrimes; ++i) {
       local.c[i] = epi->c[i];
       local.csh[i] = epi->csh[i];
+      local.es[i] = epi->s[i];
+      local.essh[i] = epi->ssh[i];
     }
   }
   local.post = (epi && epi->post) ? 1 : 0;

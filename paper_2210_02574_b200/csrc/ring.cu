@@ -1,6 +1,7 @@
 // Ring context, fused CKKS operations (key switch, rescale, ModRaise,
 // encryption) and the C ABI of libhegpu.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <exception>
@@ -239,7 +240,47 @@ const KsLevel& Ring::ks_level(int level, int alpha) {
     L->pinv[t] = h_inv(prod_mod(sp, -1, q), q);
     L->pinv_sh[t] = h_shoup(L->pinv[t], q);
   }
-  const size_t total = mu_inv.size() * 2 + mu_punc.size() + md_inv.size() * 2 + md_punc.size();
+  // ModDown fused with the rescale: D = q_level * P, sources (q_level, specials)
+  std::vector<uint64_t> mdr_punc, mdr_negd;
+  std::vector<float> mdr_fw;
+  std::vector<int32_t> mdr_fs;
+  if (level >= 1) {
+    std::vector<uint64_t> D{primes[level]};
+    std::vector<int> dp{level};
+    for (int i = 0; i < K; ++i) {
+      D.push_back(sp[i]);
+      dp.push_back(n_chain + i);
+    }
+    mdr_punc.resize((size_t)(K + 1) * level);
+    for (int i = 0; i <= K; ++i) {
+      fin(dp[i], h_inv(prod_mod(D, i, D[i]), D[i]), L->mdr_fin_s, L->mdr_fin_d);
+      for (int t = 0; t < level; ++t) {
+        const uint64_t q = primes[t];
+        mdr_punc[(size_t)i * level + t] = h_mulmod(prod_mod(D, i, q), h_rmod(q), q);
+      }
+    }
+    for (int t = 0; t < level; ++t) {
+      const uint64_t q = primes[t];
+      L->dinv.push_back(h_inv(prod_mod(D, -1, q), q));
+      L->dinv_sh.push_back(h_shoup(L->dinv.back(), q));
+      L->qlinv.push_back(h_inv(primes[level] % q, q));
+      L->qlinv_sh.push_back(h_shoup(L->qlinv.back(), q));
+    }
+    L->p_mod_ql = prod_mod(sp, -1, primes[level]);
+    for (int i = 0; i <= K; ++i) {
+      int bits = 0;
+      while (bits < 64 && (D[i] >> bits)) ++bits;
+      const int sh = bits > 32 ? bits - 32 : 0;
+      mdr_fs.push_back(sh);
+      mdr_fw.push_back(static_cast<float>(std::ldexp(1.0, sh) / static_cast<double>(D[i])));
+    }
+    for (int t = 0; t < level; ++t) {
+      const uint64_t q = primes[t];
+      mdr_negd.push_back(h_mulmod((q - prod_mod(D, -1, q)) % q, h_rmod(q), q));
+    }
+  }
+  const size_t total = mu_inv.size() * 2 + mu_punc.size() + md_inv.size() * 2 + md_punc.size() +
+                       mdr_punc.size() + mdr_negd.size() + mdr_fw.size() + mdr_fs.size();
   std::vector<uint64_t> host;
   host.reserve(total);
   auto append = [&](const std::vector<uint64_t>& v) {
@@ -249,6 +290,16 @@ const KsLevel& Ring::ks_level(int level, int alpha) {
   };
   const size_t o1 = append(mu_inv), o2 = append(mu_inv_sh), o3 = append(mu_punc);
   const size_t o4 = append(md_inv), o5 = append(md_inv_sh), o6 = append(md_punc);
+  const size_t o7 = append(mdr_punc), o8 = append(mdr_negd);
+  // fp32 weights and int32 shifts, one 64-bit word each
+  std::vector<uint64_t> fw64(mdr_fw.size()), fs64(mdr_fs.size());
+  for (size_t i = 0; i < mdr_fw.size(); ++i) {
+    uint32_t bits;
+    std::memcpy(&bits, &mdr_fw[i], 4);
+    fw64[i] = bits;
+    fs64[i] = static_cast<uint32_t>(mdr_fs[i]);
+  }
+  const size_t o9 = append(fw64), o10 = append(fs64);
   check_cuda(cudaMalloc(&L->dmem, std::max<size_t>(total, 1) * 8), "ks const alloc");
   check_cuda(cudaMemcpy(L->dmem, host.data(), total * 8, cudaMemcpyHostToDevice), "ks const copy");
   L->mu_inv = L->dmem + o1;
@@ -257,6 +308,10 @@ const KsLevel& Ring::ks_level(int level, int alpha) {
   L->md_inv = L->dmem + o4;
   L->md_inv_sh = L->dmem + o5;
   L->md_punc = L->dmem + o6;
+  L->mdr_punc = L->dmem + o7;
+  L->mdr_negd = L->dmem + o8;
+  L->mdr_fw_words = L->dmem + o9;
+  L->mdr_fs_words = L->dmem + o10;
   const KsLevel& ref = *L;
   ks[key] = std::move(L);
   return ref;
@@ -339,8 +394,13 @@ static void add_seg(SegSet& S, const uint64_t* in, int64_t is, uint64_t* out, in
   g.c_nsrc = 0;
   g.cpunc_ld = 0;
   g.eacc = 0;
+  g.ein = nullptr;
+  g.ein_stride = 0;
   g.cmode = 0;
   g.csrc_q = 0;
+  g.cnegd = nullptr;
+  g.cfw = nullptr;
+  g.cfs = nullptr;
   g.other_stride = 0;
   g.eout_stride = 0;
   g.n_polys = n_polys;
@@ -615,6 +675,111 @@ static void ks_apply_impl(Ring& R, int level, int alpha, const uint64_t* d, int6
   ks_modup(R, L, d, ds, B, dcoeff, ext, st);
   ks_ipdown(R, L, d, ds, ext, B, key_b, key_a, acc, corr, out_b, os, out_a, os, st, acc_b,
             acc_a);
+}
+
+static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uint64_t* out,
+                         int64_t os, int P, cudaStream_t st);
+
+// ModDown fused with the following rescale (mult = tensor, relinearize,
+// rescale): out = (P * in + acc) / (q_level * P) at level - 1, for both
+// components, with ONE approximate basis conversion from D = {q_level} + P
+// (keys.py:325-338 followed by ops.py:160-178 in the reference, which
+// converts from P and then rounds by q_level separately: same message, the
+// rounding error differs by at most the conversion's).  in: B (c0, c1) pairs
+// at level (c0 at in + b*is, c1 at + in_c1); out at level - 1 likewise.
+// `in` is clobbered on the unfused (N < 2^12) path.
+static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr, int B,
+                               uint64_t* in, int64_t is, int64_t in_c1, uint64_t* out,
+                               int64_t os, int64_t out_c1, cudaStream_t st) {
+  const int level = L.level, K = R.n_special, n_ext = L.n_ext;
+  const size_t N = R.n;
+  if (level < 1) throw HegpuError{HEGPU_E_ARG, "rescale at level 0"};
+  if (R.log_n < 12 || K == 0) {
+    ks_moddown(R, L, acc, corr, B, in, is, in + in_c1, is, st, true, true);
+    rescale_impl(R, level, in, is, out, os, B, st);
+    rescale_impl(R, level, in + in_c1, is, out + out_c1, os, B, st);
+    return;
+  }
+  NttTagScope tag_(NTT_TAG_MODDOWN);
+  const int32_t lp = level;
+  const uint64_t pm = L.p_mod_ql;
+  for (int g = 0; g < 2; ++g) {  // the q_level source row: acc + P * in
+    uint64_t* row = acc + (size_t)g * n_ext * N + (size_t)level * N;
+    EwArgs A{HEGPU_OP_AXPYC, in + g * in_c1 + (size_t)level * N, is, row, (int64_t)2 * n_ext * N,
+             row, (int64_t)2 * n_ext * N, B, 1, &lp, &pm};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
+  }
+  std::vector<int32_t> dsel{level};
+  for (int i = 0; i < K; ++i) dsel.push_back(R.n_chain + i);
+  SegSet S0;
+  S0.n_seg = 0;
+  S0.n_rows = 0;
+  add_seg(S0, acc + (size_t)level * N, (int64_t)n_ext * N, acc + (size_t)level * N,
+          (int64_t)n_ext * N, 2 * B, K + 1, dsel.data());
+  NttEpilogue E0;
+  E0.post = true;
+  for (int i = 0; i <= K; ++i) {
+    E0.fin_s[i] = L.mdr_fin_s[i];
+    E0.fin_d[i] = L.mdr_fin_d[i];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+  const std::vector<int32_t> chain = range_primes(0, level);
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  for (int g = 0; g < 2; ++g) {
+    add_seg(S, corr + (size_t)g * level * N, (int64_t)2 * level * N,
+            corr + (size_t)g * level * N, (int64_t)2 * level * N, B, level, chain.data());
+    Seg& sg = S.seg[g];
+    sg.other = acc + (size_t)g * n_ext * N;
+    sg.other_stride = (int64_t)2 * n_ext * N;
+    sg.eout = out + g * out_c1;
+    sg.eout_stride = os;
+    sg.eacc = 2;
+    sg.ein = in + g * in_c1;
+    sg.ein_stride = is;
+    sg.csrc = acc + (size_t)g * n_ext * N + (size_t)level * N;
+    sg.csrc_stride = (int64_t)2 * n_ext * N;
+    sg.cpunc = L.mdr_punc;
+    sg.c_nsrc = K + 1;
+    sg.cpunc_ld = level;
+    sg.cmode = 2;  // centered: (X - y) / D is round(X / D)
+    sg.cnegd = L.mdr_negd;
+    sg.cfw = reinterpret_cast<const float*>(L.mdr_fw_words);
+    sg.cfs = reinterpret_cast<const int32_t*>(L.mdr_fs_words);
+  }
+  NttEpilogue E;
+  E.enabled = true;
+  for (int t = 0; t < level; ++t) {
+    E.c[t] = L.dinv[t];
+    E.csh[t] = L.dinv_sh[t];
+    E.s[t] = L.qlinv[t];
+    E.ssh[t] = L.qlinv_sh[t];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+}
+
+static void ks_apply_rescale_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds,
+                                  int B, const uint64_t* const* key_b,
+                                  const uint64_t* const* key_a, int n_digits, uint64_t* in,
+                                  int64_t is, int64_t in_c1, uint64_t* out, int64_t os,
+                                  int64_t out_c1, cudaStream_t st) {
+  if (B <= 0) return;
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many digits"};
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  ks_modup(R, L, d, ds, B, dcoeff, ext, st);
+  ks_ip(R, L, d, ds, ext, B, key_b, key_a, acc, false, st);
+  ks_moddown_rescale(R, L, acc, corr, B, in, is, in_c1, out, os, out_c1, st);
 }
 
 // Hoisted rotations (bootstrap baby steps): ModUp of c1 once, then per
@@ -1078,6 +1243,18 @@ int hegpu_ks_apply(hegpu_ring_t ring, int level, int alpha, const uint64_t* d, i
     Ring& R = RR(ring);
     ks_apply_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, out_b, out_a,
                   out_stride, S_(stream), (accumulate & 1) != 0, (accumulate & 2) != 0);
+  })
+}
+
+int hegpu_ks_apply_rescale(hegpu_ring_t ring, int level, int alpha, const uint64_t* d,
+                           int64_t d_stride, int n_batch, const uint64_t* const* key_b,
+                           const uint64_t* const* key_a, int n_digits, uint64_t* in,
+                           int64_t in_stride, int64_t in_c1_off, uint64_t* out,
+                           int64_t out_stride, int64_t out_c1_off, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    ks_apply_rescale_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, in,
+                          in_stride, in_c1_off, out, out_stride, out_c1_off, S_(stream));
   })
 }
 

@@ -31,6 +31,18 @@ struct KsLevel {
   std::vector<ulonglong2> mu_fin_s, mu_fin_d;  // [level+1]
   std::vector<ulonglong2> md_fin_s, md_fin_d;  // [K]
   std::vector<int> dst_prime_of_digit;  // flattened [beta][n_ext] compact dst -> global prime
+  // ModDown fused with the rescale (level >= 1): divide by D = q_level * P.
+  // Sources are the acc rows level, level+1 .. level+K (q_level, specials).
+  const uint64_t* mdr_punc = nullptr;          // (D/d_i mod q_t) R mod q_t  [K+1][level]
+  const uint64_t* mdr_negd = nullptr;          // (-D mod q_t) R mod q_t      [level]
+  // centered-conversion estimate (Seg::cmode 2): fp32 2^s_i / d_i and s_i,
+  // one per 64-bit word (low 32 bits) [K+1]
+  const uint64_t* mdr_fw_words = nullptr;
+  const uint64_t* mdr_fs_words = nullptr;
+  std::vector<ulonglong2> mdr_fin_s, mdr_fin_d;  // post-scaled INTT, [K+1]
+  std::vector<uint64_t> dinv, dinv_sh;    // D^-1 mod q_t, t < level
+  std::vector<uint64_t> qlinv, qlinv_sh;  // q_level^-1 mod q_t, t < level
+  uint64_t p_mod_ql = 0;                  // P mod q_level
 };
 
 struct Ring {
@@ -120,6 +132,9 @@ struct NttEpilogue {
   bool enabled = false;  // forward: eout = (other - y) * c[limb]
   uint64_t c[kMaxPrimes];
   uint64_t csh[kMaxPrimes];
+  // seg.eacc == 2: eout = ein * s[limb] + (other - y) * c[limb]
+  uint64_t s[kMaxPrimes];
+  uint64_t ssh[kMaxPrimes];
   bool post = false;     // inverse: final stage scales by fin_s / fin_d (Shoup pairs)
   ulonglong2 fin_s[kMaxPrimes];
   ulonglong2 fin_d[kMaxPrimes];

@@ -105,6 +105,35 @@ def test_ciphertext_ops_bit_exact(name, digests):
         assert ct_digest(ckks.conjugate(cu, keys)) == d["conj_ct"]
 
 
+@pytest.mark.parametrize("name", ["desk", "p14"])
+def test_fused_relin_rescale_decrypts_like_reference(name, digests):
+    """ops.fused_rescale(): one ModDown from {q_l} + P replaces ModDown then
+    rescale (desk: N < 2^12 takes the unfused fallback).  Same level/scale,
+    the decryption agrees with the reference-exact product to noise level,
+    and batched operands work."""
+    d = digests[name]
+    params, keys = keyset(name, d)
+    rng = np.random.default_rng(9)
+    u = rng.uniform(-1, 1, params.slot_count)
+    v = rng.uniform(-1, 1, params.slot_count)
+    cu = ckks.encrypt_vector(params, u, keys, rng_seed=1)
+    cv = ckks.encrypt_vector(params, v, keys, rng_seed=2)
+    exact = ckks.mult(cu, cv, keys)
+    with ops.fused_rescale():
+        fused = ckks.mult(cu, cv, keys)
+        sq = ckks.mult(fused, fused, keys)
+        batch = ckks.mult(ops.stack([cu, cv]), cv, keys)
+    assert (fused.level, fused.scale) == (exact.level, exact.scale)
+    de, df = ckks.decrypt_vector(exact, keys), ckks.decrypt_vector(fused, keys)
+    assert np.max(np.abs(df - de)) < 1e-6
+    assert np.max(np.abs(df - u * v)) < 1e-4
+    assert np.max(np.abs(ckks.decrypt_vector(sq, keys) - (u * v) ** 2)) < 1e-4
+    b0, b1 = ops.unstack(batch)
+    assert np.max(np.abs(ckks.decrypt_vector(b0, keys) - u * v)) < 1e-4
+    assert np.max(np.abs(ckks.decrypt_vector(b1, keys) - v * v)) < 1e-4
+    assert not ops.fused_rescale_enabled()
+
+
 def test_sigmoid_bsgs_bit_exact(digests, sigmoid15):
     d = digests["desk"]
     params, keys = keyset("desk", d)
