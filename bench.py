@@ -309,17 +309,12 @@ class BootstrapWorkload:
 
 
 def logreg_rotation_steps(layout):
-    """Rotation steps of the gradient pipeline (logreg.py:202-229)."""
-    steps = set()
-    sh = 1
-    while sh < layout.padded_dim:
-        steps.update((sh, -sh))
-        sh <<= 1
-    sh = layout.padded_dim
-    while sh < layout.padded_dim * layout.rows_per_ct:
-        steps.add(sh)
-        sh <<= 1
-    return steps
+    """Rotation steps of the gradient pipeline (logreg.py:202-229): the
+    reference's doubling steps plus the multiples the hoisted radix-4 rounds
+    use (logreg.rotation_steps)."""
+    from paper_2210_02574_b200 import logreg
+
+    return logreg.rotation_steps(layout)
 
 
 class TrainWorkload:

@@ -189,6 +189,19 @@ int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c,
                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
                      uint64_t* const* outs, void* stream);
 
+/* Hoisted rotation sum: out = ct + sum_{r < n_rot} rot_r(ct), rot_r = X ->
+ * X^galois[r] then a key switch with key r (key_b/key_a: host arrays of
+ * n_rot*n_digits device pointers, rotation-major).  One ModUp of c1, n_rot
+ * digit permutations + inner products accumulated in the extended basis, one
+ * ModDown (the reference's rotate-and-sum loops run one full key switch per
+ * rotation, logreg.py:202-229).  Decrypts like the sequential sum; limbs
+ * differ.  c: n_batch packed ciphertexts (c0 at c + b*cs, c1 at + c1_off);
+ * out likewise with out_stride / out_c1_off; out must not alias c. */
+int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
+                    int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
+                    const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                    uint64_t* out, int64_t out_stride, int64_t out_c1_off, void* stream);
+
 /* Giant steps of a BSGS linear transform with one lazy ModDown:
  * out = partial[0] + sum_{g=1}^{n_giants-1} rot_g(partial[g]) where rot_g is
  * X -> X^galois[g] followed by a key switch with key g (key_b/key_a: host

@@ -8,6 +8,7 @@ histogram to weight the CPU oracle's per-op timings into a modelled
 reference step time.
 """
 
+import contextlib
 from collections import Counter
 
 _enabled = [False]
@@ -27,3 +28,14 @@ def count(op, level, n=1):
 
 def snapshot():
     return {f"{op}@{lvl}": n for (op, lvl), n in sorted(_counts.items())}
+
+
+@contextlib.contextmanager
+def paused():
+    """Suspend counting (the caller counts the reference's ops itself)."""
+    prev = _enabled[0]
+    _enabled[0] = False
+    try:
+        yield
+    finally:
+        _enabled[0] = prev

@@ -671,6 +671,59 @@ def rotate_hoisted(ct, steps, keyset):
     return [out[int(s) % ct.slot_count] for s in steps]
 
 
+def _keyed(keyset, s, slot_count):
+    return s in keyset.rotation_keys or s - slot_count in keyset.rotation_keys
+
+
+def can_rotate_sum(keyset, steps, slot_count):
+    return all(_keyed(keyset, int(s) % slot_count, slot_count) for s in steps
+               if int(s) % slot_count)
+
+
+def rotate_sum(ct, steps, keyset):
+    """ct + sum_s rotate(ct, s) with ONE ModUp and ONE ModDown
+    (hegpu_ks_rotsum): the rotations' inner products accumulate in the
+    extended basis.  Decrypts like the sequential rotate-and-add (the
+    reference's loops, logreg.py:202-229); limbs differ.  Every nonzero step
+    must have its own rotation key (can_rotate_sum)."""
+    import ctypes
+
+    params = ct.params
+    n = params.ring_degree
+    k = ct.level + 1
+    todo = [int(s) % ct.slot_count for s in steps]
+    zeros = sum(1 for s in todo if s == 0)
+    todo = [s for s in todo if s]
+    if not can_rotate_sum(keyset, todo, ct.slot_count):
+        raise CryptoError("rotate_sum needs a rotation key for every step")
+    src = ct if _pair_group(ct) is not None else ct.copy()
+    cnt = 1 if src.batch is None else src.batch
+    out = _packed(params, _lead(ct), ct.level)
+    if todo:
+        keys = [keysmod.rotation_key_for(keyset, s if s in keyset.rotation_keys
+                                         else s - ct.slot_count) for s in todo]
+        dnum = keys[0].dnum
+        gal = np.array([keysmod.galois_exponent_for_step(params, s) % (2 * n) for s in todo],
+                       dtype=np.uint64)
+        kb = (ctypes.c_void_p * (len(todo) * dnum))(
+            *[kk.b[j].data_ptr() for kk in keys for j in range(dnum)])
+        ka = (ctypes.c_void_p * (len(todo) * dnum))(
+            *[kk.a[j].data_ptr() for kk in keys for j in range(dnum)])
+        for _ in todo:
+            _stats.count("ks", ct.level, cnt)
+    else:
+        gal, kb, ka, dnum = np.zeros(1, dtype=np.uint64), None, None, 1
+    _lib.call(
+        "hegpu_ks_rotsum", params.ring.device(), ct.level, params.digit_size,
+        src.c0.data.data_ptr(), 2 * k * n, k * n, cnt, len(todo), gal.ctypes.data, kb, ka, dnum,
+        out.data_ptr(), 2 * k * n, k * n, _dev.stream(),
+    )
+    res = _ct(out, ct.level, ct.scale, ct.slot_count, params, ct.insecure_provenance)
+    for _ in range(zeros):  # rotation by 0 adds ct itself
+        res = add(res, ct)
+    return res
+
+
 def conjugate(ct, keyset):
     if keyset.conj_key is None:
         raise CryptoError("key set has no conjugation key")

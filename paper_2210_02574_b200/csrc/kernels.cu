@@ -685,6 +685,154 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip(const __grid_constant__ Ip
   }
 }
 
+// Source index of output slot i under X -> X^g (eval form, see k_auto_eval).
+// The map keeps aligned blocks of 2^b slots together for every b, so a warp's
+// 32 consecutive outputs gather from one aligned 32-slot source block.
+__device__ __forceinline__ uint32_t auto_src(uint32_t i, uint32_t g, int log_n) {
+  const uint32_t mask2n = (2u << log_n) - 1u;
+  const uint32_t bi = __brev(i) >> (32 - log_n);
+  const uint32_t e = (uint32_t)(((uint64_t)(2u * bi + 1u) * g) & mask2n);
+  return __brev((e - 1u) >> 1) >> (32 - log_n);
+}
+
+// One coefficient per thread, BG batch elements per CTA (grid.z groups).
+template <int BG>
+__global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant__ IpRotParams P) {
+  const int N = 1 << P.log_n;
+  const int r = blockIdx.y;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const int b0 = blockIdx.z * BG;
+  const int nb = P.n_batch - b0 < BG ? P.n_batch - b0 : BG;
+  const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
+  const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
+  const PrimeConst pc = P.pc[prime];
+  Mac128 ab[BG], aa[BG];
+  int since = 0;
+#pragma unroll
+  for (int b = 0; b < BG; ++b) {
+    ab[b].zero();
+    aa[b].zero();
+  }
+  for (int rot = 0; rot < P.n_rot; ++rot) {
+    const uint32_t src = auto_src((uint32_t)x, P.gal[rot], P.log_n);
+    for (int j = 0; j < P.beta; ++j) {
+      const uint64_t kb = __ldg(P.kb[rot][j] + (size_t)krow * N + x);
+      const uint64_t ka = __ldg(P.ka[rot][j] + (size_t)krow * N + x);
+      const int g0 = j * P.alpha;
+      const int g1 = min(g0 + P.alpha, P.level + 1);
+      const uint64_t* base;
+      int64_t bstr;
+      if (r >= g0 && r < g1) {
+        base = P.d + rot * P.d_sr + (size_t)r * N + src;
+        bstr = P.ds;
+      } else {
+        base = P.ext + rot * P.ext_sr + j * P.ext_sj +
+               (size_t)(r < g0 ? r : r - (g1 - g0)) * N + src;
+        bstr = P.ext_sb;
+      }
+#pragma unroll
+      for (int b = 0; b < BG; ++b) {
+        if (b < nb) {
+          const uint64_t v = __ldg(base + (size_t)(b0 + b) * bstr);
+          ab[b].add(v, kb);
+          aa[b].add(v, ka);
+        }
+      }
+      if (++since == kMacFold) {
+        since = 0;
+#pragma unroll
+        for (int b = 0; b < BG; ++b) {
+          ab[b].fold(pc.q, pc.bar);
+          aa[b].fold(pc.q, pc.bar);
+        }
+      }
+    }
+    if (!P.sum_mode || rot == P.n_rot - 1) {
+      uint64_t* o = P.acc + (P.sum_mode ? 0 : rot * P.acc_sr) + (size_t)r * N + x;
+#pragma unroll
+      for (int b = 0; b < BG; ++b) {
+        if (b < nb) {
+          uint64_t* ob = o + (size_t)(b0 + b) * P.acc_sb;
+          uint64_t vb = mont_mul(ab[b].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+          uint64_t va = mont_mul(aa[b].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+          if (P.accumulate) {
+            vb = add_mod(vb, ob[0], pc.q);
+            va = add_mod(va, ob[(size_t)P.n_ext * N], pc.q);
+          }
+          ob[0] = vb;
+          ob[(size_t)P.n_ext * N] = va;
+        }
+        ab[b].zero();
+        aa[b].zero();
+      }
+      since = 0;
+    }
+  }
+}
+
+void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
+  if (P.beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
+  if (P.n_rot < 1 || P.n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
+  constexpr int BG = 4;
+  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext, (P.n_batch + BG - 1) / BG);
+  const double ipn = (double)(1 << P.log_n) * P.n_ext;
+  ProfScope ps(PROF_KS_IP, st,
+               ipn * 8.0 * P.n_rot * (2.0 * P.beta + P.n_batch * P.beta) +
+                   ipn * 8.0 * 2.0 * P.n_batch * (P.sum_mode ? 1 : P.n_rot),
+               ipn * P.n_batch * P.n_rot * 2.0 * P.beta);
+  k_ks_ip_rot<BG><<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "ks rotation inner product launch");
+}
+
+struct AutoSumParams {
+  const uint64_t* in;
+  int64_t is;
+  const uint64_t* base;  // out = base + sum_r sigma_r(in); base == in when null
+  int64_t bs;
+  uint64_t* out;
+  int64_t os;
+  uint32_t gal[kMaxRot];
+  int n_rot, k, log_n;
+  const PrimeConst* pc;
+};
+
+__global__ void __launch_bounds__(kEwThreads) k_auto_sum(const __grid_constant__ AutoSumParams P) {
+  const int N = 1 << P.log_n;
+  const int row = blockIdx.y + blockIdx.z * 65535;
+  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  if (x >= N) return;
+  const int poly = row / P.k, limb = row - poly * P.k;
+  const uint64_t q = P.pc[limb].q;
+  const uint64_t* in = P.in + poly * P.is + (size_t)limb * N;
+  uint64_t s = P.base ? P.base[poly * P.bs + (size_t)limb * N + x] : in[x];
+  for (int r = 0; r < P.n_rot; ++r) s = add_mod(s, __ldg(in + auto_src((uint32_t)x, P.gal[r], P.log_n)), q);
+  P.out[poly * P.os + (size_t)limb * N + x] = s;
+}
+
+void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
+                     const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
+                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st) {
+  if (n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
+  AutoSumParams P;
+  P.in = in;
+  P.is = is;
+  P.base = base;
+  P.bs = bs;
+  P.out = out;
+  P.os = os;
+  for (int r = 0; r < n_rot; ++r) P.gal[r] = gal[r];
+  P.n_rot = n_rot;
+  P.k = k;
+  P.log_n = log_n;
+  P.pc = dpc;
+  const int rows = n_polys * k;
+  const dim3 grid = rows_grid(1 << log_n, rows, 1);
+  ProfScope ps(PROF_AUTOMORPHISM, st, (double)rows * (1 << log_n) * 8.0 * (n_rot + 2), 0.0);
+  k_auto_sum<<<grid, kEwThreads, 0, st>>>(P);
+  check_cuda(cudaGetLastError(), "automorphism sum launch");
+}
+
 void launch_ks_ip(IpParams& P, cudaStream_t st) {
   if (P.beta > kMaxDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
   dim3 grid(((1 << P.log_n) / 2 + kEwThreads - 1) / kEwThreads, P.n_ext);

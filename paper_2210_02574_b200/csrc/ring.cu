@@ -828,6 +828,85 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
   }
 }
 
+// Hoisted rotation sum: out = ct + sum_r rot_r(ct).  One ModUp of c1, then
+// per rotation the digits are permuted (eval-form gather) and the inner
+// product with key r accumulates in the extended basis; the sum is brought
+// down by ONE ModDown whose epilogue adds it to c0 + sum_r sigma_r(c0) and
+// c1.  Replaces n_rot sequential rotate-and-add key switches (each with its
+// own ModUp and ModDown) of the reference's rotate-and-sum loops
+// (logreg.py:202-229): same slots, limbs differ by the conversion rounding.
+// c / out: B packed ciphertexts (c0 at +b*cs / +b*os, c1 at +c1_off /
+// +out_c1); out may not alias c.
+static void ks_rotsum_impl(Ring& R, int level, int alpha, const uint64_t* c, int64_t cs,
+                           int64_t c1_off, int B, int n_rot, const uint64_t* galois,
+                           const uint64_t* const* key_b, const uint64_t* const* key_a,
+                           int n_digits, uint64_t* out, int64_t os, int64_t out_c1,
+                           cudaStream_t st) {
+  if (B <= 0) return;
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  const std::vector<int32_t> chain = range_primes(0, k);
+  std::vector<uint32_t> gal(n_rot > 0 ? n_rot : 1);
+  for (int r = 0; r < n_rot; ++r) gal[r] = (uint32_t)galois[r];
+  // c1' = c1 (+ ModDown of the accumulated inner products below)
+  EwArgs A{HEGPU_OP_COPY, c + c1_off, cs, nullptr, 0, out + out_c1, os, B, k, chain.data(),
+           nullptr};
+  launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
+  // c0' = c0 + sum_r sigma_r(c0): one gather-sum pass per 16 rotations
+  for (int r0 = 0; r0 < std::max(n_rot, 1); r0 += kMaxRot) {
+    const int nr = std::min(kMaxRot, n_rot - r0);
+    launch_auto_sum(R.dpc, R.log_n, gal.data() + r0, std::max(nr, 0), c, cs, r0 ? out : nullptr,
+                    os, out, os, B, k, st);
+  }
+  if (n_rot <= 0) return;
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many digits for rotsum"};
+  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
+  uint64_t* dcoeff = ws.u64();
+  uint64_t* ext = dcoeff + sz_dc;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + sz_acc;
+  ks_modup(R, L, c + c1_off, cs, B, dcoeff, ext, st);
+  for (int r0 = 0; r0 < n_rot; r0 += kMaxRot) {
+    const int nr = std::min(kMaxRot, n_rot - r0);
+    IpRotParams P;
+    P.d = c + c1_off;
+    P.ds = cs;
+    P.d_sr = 0;
+    P.ext = ext;
+    P.ext_sb = (int64_t)beta * n_ext * N;
+    P.ext_sj = (int64_t)n_ext * N;
+    P.ext_sr = 0;
+    for (int r = 0; r < nr; ++r) {
+      P.gal[r] = gal[r0 + r];
+      for (int j = 0; j < beta; ++j) {
+        P.kb[r][j] = key_b[(size_t)(r0 + r) * n_digits + j];
+        P.ka[r][j] = key_a[(size_t)(r0 + r) * n_digits + j];
+      }
+    }
+    P.n_rot = nr;
+    P.sum_mode = 1;
+    P.accumulate = r0 > 0;
+    P.acc = acc;
+    P.acc_sb = (int64_t)2 * n_ext * N;
+    P.acc_sr = 0;
+    P.level = level;
+    P.alpha = alpha;
+    P.beta = beta;
+    P.n_ext = n_ext;
+    P.n_chain = R.n_chain;
+    P.key_sp_row0 = R.n_chain;
+    P.n_batch = B;
+    P.log_n = R.log_n;
+    P.pc = R.dpc;
+    launch_ks_ip_rot(P, st);
+  }
+  ks_moddown(R, L, acc, corr, B, out, os, out + out_c1, os, st, /*acc_b=*/true, /*acc_a=*/true);
+}
+
 // Giant steps of a BSGS transform with one lazy ModDown (double hoisting):
 // out = partial[0] + sum_{g>0} rot_{galois[g]}(partial[g]).  Each giant's key
 // inner product accumulates in the extended basis; the sum is brought down
@@ -1255,6 +1334,18 @@ int hegpu_ks_apply_rescale(hegpu_ring_t ring, int level, int alpha, const uint64
     Ring& R = RR(ring);
     ks_apply_rescale_impl(R, level, alpha, d, d_stride, n_batch, key_b, key_a, n_digits, in,
                           in_stride, in_c1_off, out, out_stride, out_c1_off, S_(stream));
+  })
+}
+
+int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
+                    int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
+                    const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
+                    uint64_t* out, int64_t out_stride, int64_t out_c1_off, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (out == c) throw HegpuError{HEGPU_E_ARG, "rotsum output may not alias the input"};
+    ks_rotsum_impl(R, level, alpha, c, cs, c1_off, n_batch, n_rot, galois, key_b, key_a,
+                   n_digits, out, out_stride, out_c1_off, S_(stream));
   })
 }
 

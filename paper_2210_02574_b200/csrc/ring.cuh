@@ -219,6 +219,34 @@ struct IpParams {
   const PrimeConst* pc;
 };
 
+// Key inner products of several rotations of hoisted digits in ONE launch:
+// for rotation r, the digits are read through X -> X^gal[r] (eval-form
+// gather, fused: no permuted copy is written).  Sources of rotation r:
+// d + r*d_sr (own-digit rows, level+1 limbs per batch element, stride ds)
+// and ext + r*ext_sr (converted rows).  sum_mode: all rotations accumulate
+// into acc; otherwise rotation r writes acc + r*acc_sr.
+constexpr int kMaxRot = 16;
+constexpr int kMaxRotDigits = 8;
+struct IpRotParams {
+  const uint64_t* d;
+  int64_t ds, d_sr;
+  const uint64_t* ext;
+  int64_t ext_sb, ext_sj, ext_sr;
+  const uint64_t* kb[kMaxRot][kMaxRotDigits];
+  const uint64_t* ka[kMaxRot][kMaxRotDigits];
+  uint32_t gal[kMaxRot];
+  int n_rot, sum_mode, accumulate;
+  uint64_t* acc;
+  int64_t acc_sb, acc_sr;
+  int level, alpha, beta, n_ext, n_chain, key_sp_row0, n_batch, log_n;
+  const PrimeConst* pc;
+};
+void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st);
+// out[b] = base[b] + sum_r sigma_r(in[b]) (eval form, k limbs; base = in when null)
+void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
+                     const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
+                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st);
+
 void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint64_t g,
                          const uint64_t* in, int64_t is, uint64_t* out, int64_t os, int n_polys,
                          int k, const int32_t* primes, cudaStream_t st);

@@ -134,6 +134,36 @@ def test_fused_relin_rescale_decrypts_like_reference(name, digests):
     assert not ops.fused_rescale_enabled()
 
 
+def test_rotate_sum_matches_sequential(desk_keys):
+    """ops.rotate_sum (one hoisted key switch for several rotations) decrypts
+    like the reference's sequential rotate-and-add, batched too."""
+    params, keys = desk_keys
+    steps = [s for s in (1, 2, 3) if s in keys.rotation_keys]
+    if len(steps) < 2:
+        keys = ckks.keygen(params, rotation_steps=[1, 2, 3], rng_seed=7)
+        steps = [1, 2, 3]
+    rng = np.random.default_rng(12)
+    v = rng.uniform(-1, 1, params.slot_count)
+    ct = ckks.encrypt_vector(params, v, keys, rng_seed=4)
+    want = v + sum(np.roll(v, -s) for s in steps)
+    got = ops.rotate_sum(ct, steps, keys)
+    assert (got.level, got.scale) == (ct.level, ct.scale)
+    seq = ct
+    for s in steps:
+        seq = ckks.add(seq, ckks.rotate(ct, s, keys))
+    assert np.max(np.abs(ckks.decrypt_vector(got, keys) - ckks.decrypt_vector(seq, keys))) < 1e-6
+    assert np.max(np.abs(ckks.decrypt_vector(got, keys) - want)) < 1e-4
+    batch = ops.rotate_sum(ops.stack([ct, ckks.encrypt_vector(params, -v, keys)]), steps, keys)
+    assert np.max(np.abs(ckks.decrypt_vector(ops.unstack(batch)[1], keys) + want)) < 1e-4
+    assert np.max(np.abs(ckks.decrypt_vector(ops.rotate_sum(ct, [0], keys), keys) - 2 * v)) < 1e-4
+    many = list(range(1, 19))  # more than one 16-rotation chunk
+    keys18 = ckks.keygen(params, rotation_steps=many, rng_seed=7)
+    ct18 = ckks.encrypt_vector(params, v, keys18, rng_seed=4)
+    want18 = v + sum(np.roll(v, -s) for s in many)
+    got18 = ckks.decrypt_vector(ops.rotate_sum(ct18, many, keys18), keys18)
+    assert np.max(np.abs(got18 - want18)) < 1e-3
+
+
 def test_sigmoid_bsgs_bit_exact(digests, sigmoid15):
     d = digests["desk"]
     params, keys = keyset("desk", d)

@@ -35,6 +35,25 @@ def test_training_matches_reference_and_shadow(desk, sigmoid15):
     assert timing[0]["level_refreshes"] == 4
 
 
+def test_training_hoisted_rotsum_radix4(sigmoid15):
+    """With the radix-4 rotation keys (logreg.rotation_steps) every
+    rotate-and-sum round runs 3 rotations through one hoisted key switch;
+    the trained weights still track the shadow trainer and the reference."""
+    params = ckks.get_preset("desk")
+    g = golden_npz("logreg_desk.npz")
+    X, y = g["X"], g["y"]
+    layout = logreg.make_layout(params, 16)
+    keys = ckks.keygen(params, rotation_steps=sorted(logreg.rotation_steps(layout)), rng_seed=7)
+    assert all(s in keys.rotation_keys for s in (3, -3, 12, -12))
+    pairs = logreg.pack_batch(X, y, layout, params, keys)
+    cfg = logreg.TrainConfig(1.0, 0.9, 128, 2)
+    model, _ = logreg.train(pairs, 256, cfg, params, keys, sigmoid15,
+                            bs.DebugRefresher(keys, enabled=True), layout=layout)
+    got = logreg.decrypted_weights(model, keys)
+    assert np.max(np.abs(got - g["shadow_weights"])) <= 2e-2
+    assert np.max(np.abs(got - g["ref_weights"])) <= 2e-2
+
+
 def test_encrypted_vs_shadow_acceptance(desk, sigmoid15):
     """Acceptance criterion (T/test_acceptance.py:98-131), 1000 rows x 768."""
     params, keys = desk
