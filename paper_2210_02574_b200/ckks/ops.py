@@ -657,7 +657,9 @@ def rotate_hoisted(ct, steps, keyset):
         *[kk.b[j].data_ptr() for kk in keys for j in range(dnum)])
     ka = (ctypes.c_void_p * (len(todo) * dnum))(
         *[kk.a[j].data_ptr() for kk in keys for j in range(dnum)])
-    outs = [_packed(params, _lead(ct), ct.level) for _ in todo]
+    # one tensor, rotation-major: the library batches the ModDowns of all rotations
+    allout = _dev.empty(*((len(todo),) + tuple(_lead(ct)) + (2, k, n)))
+    outs = [allout[i] for i in range(len(todo))]
     optr = (ctypes.c_void_p * len(todo))(*[o.data_ptr() for o in outs])
     for _ in todo:
         _stats.count("ks", ct.level, cnt)

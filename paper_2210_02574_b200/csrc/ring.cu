@@ -799,32 +799,69 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
   if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many digits for hoisting"};
+  // outputs laid out back to back (rotation-major) share one batched ModDown
+  bool uniform = true;
+  for (int r = 1; r < n_rot; ++r) uniform &= outs[r] == outs[0] + (int64_t)r * B * cs;
+  const int CH = kMaxRot;
   const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
   const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
-  const size_t sz_kb = (size_t)B * k * N;
-  Scratch ws((sz_dc + 2 * sz_ext + sz_acc + sz_corr + sz_kb) * 8, st);
+  Scratch ws((sz_dc + sz_ext + CH * (sz_acc + sz_corr)) * 8, st);
   uint64_t* dcoeff = ws.u64();
   uint64_t* ext = dcoeff + sz_dc;
-  uint64_t* extp = ext + sz_ext;
-  uint64_t* acc = extp + sz_ext;
-  uint64_t* corr = acc + sz_acc;
-  uint64_t* dp = corr + sz_corr;
+  uint64_t* acc = ext + sz_ext;
+  uint64_t* corr = acc + CH * sz_acc;
   const uint64_t* c1 = c + c1_off;
   ks_modup(R, L, c1, cs, B, dcoeff, ext, st);
   const std::vector<int32_t> chain = range_primes(0, k);
-  const std::vector<int32_t> rows = range_primes(0, n_ext);
-  for (int r = 0; r < n_rot; ++r) {
-    launch_automorphism(R.dpc, R.log_n, true, galois[r], c1, cs, dp, (int64_t)k * N, B, k,
-                        chain.data(), st);
-    launch_automorphism(R.dpc, R.log_n, true, galois[r], ext, (int64_t)n_ext * N, extp,
-                        (int64_t)n_ext * N, B * beta, n_ext, rows.data(), st);
-    uint64_t* out = outs[r];
+  for (int r0 = 0; r0 < n_rot; r0 += CH) {
+    const int nr = std::min(CH, n_rot - r0);
+    // the nr rotations' inner products in one launch, digits gathered through
+    // X -> X^g[r] (no permuted copies), one acc per rotation
+    IpRotParams P;
+    P.d = c1;
+    P.ds = cs;
+    P.d_sr = 0;
+    P.ext = ext;
+    P.ext_sb = (int64_t)beta * n_ext * N;
+    P.ext_sj = (int64_t)n_ext * N;
+    P.ext_sr = 0;
+    for (int r = 0; r < nr; ++r) {
+      P.gal[r] = (uint32_t)galois[r0 + r];
+      for (int j = 0; j < beta; ++j) {
+        P.kb[r][j] = key_b[(size_t)(r0 + r) * n_digits + j];
+        P.ka[r][j] = key_a[(size_t)(r0 + r) * n_digits + j];
+      }
+    }
+    P.n_rot = nr;
+    P.sum_mode = 0;
+    P.accumulate = 0;
+    P.acc = acc;
+    P.acc_sb = (int64_t)2 * n_ext * N;
+    P.acc_sr = (int64_t)sz_acc;
+    P.level = level;
+    P.alpha = alpha;
+    P.beta = beta;
+    P.n_ext = n_ext;
+    P.n_chain = R.n_chain;
+    P.key_sp_row0 = R.n_chain;
+    P.n_batch = B;
+    P.log_n = R.log_n;
+    P.pc = R.dpc;
+    launch_ks_ip_rot(P, st);
     // c0' = sigma(c0) + kb: permute c0 into place, then the ModDown epilogue
     // accumulates kb into it; c1' = ka is written directly
-    launch_automorphism(R.dpc, R.log_n, true, galois[r], c, cs, out, cs, B, k, chain.data(), st);
-    ks_ipdown(R, L, dp, (int64_t)k * N, extp, B, key_b + (size_t)r * n_digits,
-              key_a + (size_t)r * n_digits, acc, corr, out, cs, out + c1_off, cs, st,
-              /*acc_b=*/true, /*acc_a=*/false);
+    for (int r = 0; r < nr; ++r)
+      launch_automorphism(R.dpc, R.log_n, true, galois[r0 + r], c, cs, outs[r0 + r], cs, B, k,
+                          chain.data(), st);
+    if (uniform) {
+      ks_moddown(R, L, acc, corr, nr * B, outs[r0], cs, outs[r0] + c1_off, cs, st,
+                 /*acc_b=*/true, /*acc_a=*/false);
+    } else {
+      for (int r = 0; r < nr; ++r)
+        ks_moddown(R, L, acc + r * sz_acc, corr, B, outs[r0 + r], cs, outs[r0 + r] + c1_off, cs,
+                   st, /*acc_b=*/true, /*acc_a=*/false);
+    }
   }
 }
 
