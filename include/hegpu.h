@@ -210,11 +210,13 @@ int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, 
  * partials + g*gstride; out: packed (n_batch, 2, level+1, N).  The inner
  * products accumulate in the extended basis and are brought down once
  * (bootstrap.py:243-245 rotates and adds per giant); decrypts identically,
- * limbs differ. */
+ * limbs differ.  rescale = 1: the final ModDown also divides by q_level
+ * (the transform's rescale, bootstrap.py:247) and out is packed
+ * (n_batch, 2, level, N) at level - 1. */
 int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
                       int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                      uint64_t* out, void* stream);
+                      uint64_t* out, int rescale, void* stream);
 
 /* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
  * limbs (eval form), out gets `level` limbs.  in may equal out. */

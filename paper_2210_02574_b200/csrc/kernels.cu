@@ -787,7 +787,7 @@ void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
 
 struct AutoSumParams {
   const uint64_t* in;
-  int64_t is;
+  int64_t is, in_sr;  // rotation r permutes in + r*in_sr
   const uint64_t* base;  // out = base + sum_r sigma_r(in); base == in when null
   int64_t bs;
   uint64_t* out;
@@ -806,17 +806,20 @@ __global__ void __launch_bounds__(kEwThreads) k_auto_sum(const __grid_constant__
   const uint64_t q = P.pc[limb].q;
   const uint64_t* in = P.in + poly * P.is + (size_t)limb * N;
   uint64_t s = P.base ? P.base[poly * P.bs + (size_t)limb * N + x] : in[x];
-  for (int r = 0; r < P.n_rot; ++r) s = add_mod(s, __ldg(in + auto_src((uint32_t)x, P.gal[r], P.log_n)), q);
+  for (int r = 0; r < P.n_rot; ++r)
+    s = add_mod(s, __ldg(in + r * P.in_sr + auto_src((uint32_t)x, P.gal[r], P.log_n)), q);
   P.out[poly * P.os + (size_t)limb * N + x] = s;
 }
 
 void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
                      const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
-                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st) {
+                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st,
+                     int64_t in_sr) {
   if (n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
   AutoSumParams P;
   P.in = in;
   P.is = is;
+  P.in_sr = in_sr;
   P.base = base;
   P.bs = bs;
   P.out = out;

@@ -951,42 +951,108 @@ static void ks_rotsum_impl(Ring& R, int level, int alpha, const uint64_t* c, int
 // limbs differ (ModDown is linear only up to its rounding).
 // partials: n_giants packed (B, 2, k, N) ciphertexts, giant g at
 // partials + g*gstride; out: packed (B, 2, k, N).
-static void bsgs_giants_impl(Ring& R, int level, int alpha, const uint64_t* partials,
-                             int64_t gstride, int B, int n_giants, const uint64_t* galois,
-                             const uint64_t* const* key_b, const uint64_t* const* key_a,
-                             int n_digits, uint64_t* out, cudaStream_t st) {
+// out = partial[0] + sum_g rot_g(partial[g]) at `level`; with `down` the
+// final ModDown is fused with the rescale and writes `down` (level - 1)
+// instead (out is then clobbered scratch).
+static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* partials,
+                            int64_t gstride, int B, int n_giants, const uint64_t* galois,
+                            const uint64_t* const* key_b, const uint64_t* const* key_a,
+                            int n_digits, uint64_t* out, cudaStream_t st, uint64_t* down) {
   const KsLevel& L = R.ks_level(level, alpha);
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
   const int64_t cs = (int64_t)2 * k * N;  // packed batch stride
   if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many digits for giant steps"};
+  if (gstride < (int64_t)B * cs) throw HegpuError{HEGPU_E_ARG, "giant stride too small"};
   const std::vector<int32_t> chain = range_primes(0, k);
-  {  // out = partial[0]
-    EwArgs A{HEGPU_OP_COPY, partials, (int64_t)k * N, nullptr, 0, out, (int64_t)k * N, 2 * B, k,
-             chain.data(), nullptr};
+  {  // out.c1 = partial[0].c1 (the ModDown epilogue adds the switched parts)
+    EwArgs A{HEGPU_OP_COPY, partials + (size_t)k * N, cs, nullptr, 0, out + (size_t)k * N, cs, B,
+             k, chain.data(), nullptr};
     launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
   }
+  std::vector<uint32_t> gal(std::max(n_giants, 1));
+  for (int g = 0; g < n_giants; ++g) gal[g] = (uint32_t)galois[g];
+  // out.c0 = partial[0].c0 + sum_g sigma_g(partial[g].c0), 16 giants per pass
+  for (int g0 = 1; g0 < std::max(n_giants, 2); g0 += kMaxRot) {
+    const int ng = std::max(0, std::min(kMaxRot, n_giants - g0));
+    launch_auto_sum(R.dpc, R.log_n, gal.data() + g0, ng, partials + g0 * gstride, cs,
+                    g0 == 1 ? partials : out, cs, out, cs, B, k, st, gstride);
+  }
   if (n_giants <= 1) return;
-  const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+  // ModUp of up to 16 giants' c1 in one batch (uniform stride when the giants
+  // are packed back to back), then one inner-product launch that gathers each
+  // giant's digits through its automorphism and sums over the giants
+  const bool packed = gstride == (int64_t)B * cs;
+  const int CH = packed ? kMaxRot : 1;
+  const size_t sz_dc = (size_t)CH * B * k * N, sz_ext = (size_t)CH * B * beta * n_ext * N;
   const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
-  const size_t sz_tmp = (size_t)B * 2 * k * N;
-  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr + sz_tmp) * 8, st);
+  Scratch ws((sz_dc + sz_ext + sz_acc + sz_corr) * 8, st);
   uint64_t* dcoeff = ws.u64();
   uint64_t* ext = dcoeff + sz_dc;
   uint64_t* acc = ext + sz_ext;
   uint64_t* corr = acc + sz_acc;
-  uint64_t* tmp = corr + sz_corr;
-  for (int g = 1; g < n_giants; ++g) {
-    const uint64_t* part = partials + g * gstride;
-    launch_automorphism(R.dpc, R.log_n, true, galois[g], part, (int64_t)k * N, tmp,
-                        (int64_t)k * N, 2 * B, k, chain.data(), st);
-    ks_modup(R, L, tmp + (size_t)k * N, cs, B, dcoeff, ext, st);
-    ks_ip(R, L, tmp + (size_t)k * N, cs, ext, B, key_b + (size_t)g * n_digits,
-          key_a + (size_t)g * n_digits, acc, g > 1, st);
-    EwArgs A{HEGPU_OP_ADD, out, cs, tmp, cs, out, cs, B, k, chain.data(), nullptr};
-    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);  // out.c0 += sigma(c0)
+  bool first = true;
+  for (int g0 = 1; g0 < n_giants; g0 += CH) {
+    const int ng = std::min(CH, n_giants - g0);
+    const uint64_t* c1 = partials + g0 * gstride + (size_t)k * N;
+    ks_modup(R, L, c1, cs, ng * B, dcoeff, ext, st);
+    IpRotParams P;
+    P.d = c1;
+    P.ds = cs;
+    P.d_sr = gstride;
+    P.ext = ext;
+    P.ext_sb = (int64_t)beta * n_ext * N;
+    P.ext_sj = (int64_t)n_ext * N;
+    P.ext_sr = (int64_t)B * beta * n_ext * N;
+    for (int r = 0; r < ng; ++r) {
+      P.gal[r] = gal[g0 + r];
+      for (int j = 0; j < beta; ++j) {
+        P.kb[r][j] = key_b[(size_t)(g0 + r) * n_digits + j];
+        P.ka[r][j] = key_a[(size_t)(g0 + r) * n_digits + j];
+      }
+    }
+    P.n_rot = ng;
+    P.sum_mode = 1;
+    P.accumulate = first ? 0 : 1;
+    P.acc = acc;
+    P.acc_sb = (int64_t)2 * n_ext * N;
+    P.acc_sr = 0;
+    P.level = level;
+    P.alpha = alpha;
+    P.beta = beta;
+    P.n_ext = n_ext;
+    P.n_chain = R.n_chain;
+    P.key_sp_row0 = R.n_chain;
+    P.n_batch = B;
+    P.log_n = R.log_n;
+    P.pc = R.dpc;
+    launch_ks_ip_rot(P, st);
+    first = false;
+  }
+  if (down) {
+    ks_moddown_rescale(R, L, acc, corr, B, out, cs, (int64_t)k * N, down, (int64_t)2 * level * N,
+                       (int64_t)level * N, st);
+    return;
   }
   ks_moddown(R, L, acc, corr, B, out, cs, out + (size_t)k * N, cs, st, true, true);
+}
+
+static void bsgs_giants_impl(Ring& R, int level, int alpha, const uint64_t* partials,
+                             int64_t gstride, int B, int n_giants, const uint64_t* galois,
+                             const uint64_t* const* key_b, const uint64_t* const* key_a,
+                             int n_digits, uint64_t* out, cudaStream_t st, bool rescale) {
+  if (!rescale) {
+    bsgs_giants_sum(R, level, alpha, partials, gstride, B, n_giants, galois, key_b, key_a,
+                    n_digits, out, st, nullptr);
+    return;
+  }
+  // the level-`level` sum goes to scratch; one ModDown by q_level * P leaves
+  // the rescaled result (level - 1) in out
+  if (level < 1) throw HegpuError{HEGPU_E_ARG, "rescale at level 0"};
+  Scratch tmp((size_t)B * 2 * (level + 1) * R.n * 8, st);
+  bsgs_giants_sum(R, level, alpha, partials, gstride, B, n_giants, galois, key_b, key_a,
+                  n_digits, tmp.u64(), st, out);
 }
 
 // --- rescale (ops.py:164-189) and ModRaise (bootstrap.py:260-275) ----------
@@ -1400,11 +1466,11 @@ int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c,
 int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
                       int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                      uint64_t* out, void* stream) {
+                      uint64_t* out, int rescale, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     bsgs_giants_impl(R, level, alpha, partials, gstride, n_batch, n_giants, galois, key_b, key_a,
-                     n_digits, out, S_(stream));
+                     n_digits, out, S_(stream), rescale != 0);
   })
 }
 

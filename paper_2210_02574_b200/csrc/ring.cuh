@@ -242,10 +242,12 @@ struct IpRotParams {
   const PrimeConst* pc;
 };
 void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st);
-// out[b] = base[b] + sum_r sigma_r(in[b]) (eval form, k limbs; base = in when null)
+// out[b] = base[b] + sum_r sigma_r(in[b] + r*in_sr) (eval form, k limbs;
+// base = the unpermuted in when null)
 void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
                      const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
-                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st);
+                     uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st,
+                     int64_t in_sr = 0);
 
 void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint64_t g,
                          const uint64_t* in, int64_t is, uint64_t* out, int64_t os, int n_polys,
