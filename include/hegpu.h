@@ -77,6 +77,10 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
  * precompute (ring.py:81-177).  Primes must be < 2^62, = 1 mod 2N. */
 int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain,
                       const uint64_t* special, int n_special, hegpu_ring_t* out);
+/* Keep the ring's twiddle tables (n_primes * 4N words) resident in a
+ * persisting L2 carve-out for kernels launched on `stream`. */
+int hegpu_l2_persist_twiddles(hegpu_ring_t ring, void* stream, double hit_ratio);
+
 int hegpu_ring_destroy(hegpu_ring_t ring);
 /* Copy the device twiddle tables of global prime p to host: 4N words,
  * interleaved (psi_rev[i], shoup(psi_rev[i])) pairs for i < N, then
@@ -141,6 +145,14 @@ int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int6
                  const uint64_t* b0, const uint64_t* b1, int64_t b_stride, uint64_t* d0,
                  uint64_t* d1, uint64_t* d2, int64_t d_stride, int n_polys, int k,
                  void* stream);
+
+/* hegpu_tensor with a periodic first operand: product p uses a at index
+ * p % a_period (one batch of a against n_polys / a_period stacked batches
+ * of b, e.g. one giant power against every node of a polynomial level). */
+int hegpu_tensor_periodic(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1,
+                          int64_t a_stride, int a_period, const uint64_t* b0, const uint64_t* b1,
+                          int64_t b_stride, uint64_t* d0, uint64_t* d1, uint64_t* d2,
+                          int64_t d_stride, int n_polys, int k, void* stream);
 
 /* -------------------------------------------------------------------------
  * fused CKKS kernels (ckks/ops.py, ckks/keys.py, bootstrap.py)

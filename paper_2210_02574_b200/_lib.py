@@ -12,7 +12,7 @@ import threading
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegpu.so")
+LIB_PATH = os.environ.get("HEGPU_LIB") or os.path.join(_HERE, "libhegpu.so")  # override: experiments
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hegpu.h")
 
 (OP_ADD, OP_SUB, OP_MUL, OP_MONT, OP_NEG, OP_SCALAR, OP_ROWMONT, OP_FMA, OP_COPY, OP_ADDC,
@@ -42,6 +42,8 @@ SIGNATURES = {
     "hegpu_automorphism": [_P, _I, _U64, _P, _I64, _P, _I64, _I, _I, _P, _P],
     "hegpu_tensor": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_apply": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _P, _I64, _I, _P],
+    "hegpu_l2_persist_twiddles": [_P, _P, ctypes.c_double],
+    "hegpu_tensor_periodic": [_P, _P, _P, _I64, _I, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_rotsum": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _I64, _I64, _P],
     "hegpu_ks_apply_rescale": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _I64, _I64, _P, _I64,
                                _I64, _P],

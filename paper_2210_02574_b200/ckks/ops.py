@@ -514,16 +514,25 @@ def _tensor(ct1, ct2):
     b0p, bcnt, bs = ct2.c0._group()
     b1p, _, _ = ct2.c1._group()
     cnt = max(acnt, bcnt)
+    period = cnt
     if acnt == 1 and cnt > 1:  # the product is symmetric: put the batch first
         a0p, a1p, as_, b0p, b1p, bs = b0p, b1p, bs, a0p, a1p, 0
     elif bcnt == 1 and cnt > 1:
         bs = 0
     elif acnt != bcnt:
-        raise CryptoError("batch size mismatch")
+        # one batch against several stacked copies of its shape: the smaller
+        # operand repeats with period min(acnt, bcnt) (level-batched polynomial
+        # evaluation multiplies one giant power by every node of a level)
+        lo_cnt, hi_cnt = min(acnt, bcnt), max(acnt, bcnt)
+        if hi_cnt % lo_cnt:
+            raise CryptoError("batch size mismatch")
+        if bcnt < acnt:
+            a0p, a1p, as_, b0p, b1p, bs = b0p, b1p, bs, a0p, a1p, as_
+        period = lo_cnt
     lead = _lead(ct1) if acnt >= bcnt else _lead(ct2)
     d = _dev.empty(*(tuple(lead) + (3, k, n)))
     _lib.call(
-        "hegpu_tensor", params.ring.device(), a0p, a1p, as_, b0p, b1p, bs,
+        "hegpu_tensor_periodic", params.ring.device(), a0p, a1p, as_, period, b0p, b1p, bs,
         d[..., 0, :, :].data_ptr(), d[..., 1, :, :].data_ptr(), d[..., 2, :, :].data_ptr(),
         3 * k * n, cnt, k, _dev.stream(),
     )
@@ -773,14 +782,18 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
         giants[2 * g] = add_plain(add(sq, sq), -1.0)
         g *= 2
 
-    def eval_range(c):
+    # The reference's recursion (ops.py:432-506) is planned first and then run
+    # level by level: every leaf's scalar product shares one rescale launch and
+    # all products of one giant power share one key switch.  Each op sees the
+    # same operands as in the recursive order, so the limbs are identical.
+    def plan(c):
         d = len(c) - 1
         while d > 0 and abs(c[d]) <= skip:
             d -= 1
         if d == 0:
-            return float(c[0])
+            return ["const", float(c[0])]
         if d == 1:
-            return add_plain(mult_plain(giants[1], float(c[1])), float(c[0]))
+            return ["leaf", float(c[0]), float(c[1])]
         g = 1 << (math.ceil(math.log2(d + 1)) - 1)
         r = np.zeros(d - g + 1)
         r[0] = c[g]
@@ -788,19 +801,77 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
         q = c[:g].copy()
         for j in range(1, d - g + 1):
             q[g - j] -= c[g + j]
-        r_val = eval_range(r)
-        q_val = eval_range(q)
-        if isinstance(r_val, float):
-            term = None if abs(r_val) <= skip else mult_plain(giants[g], r_val)
-        else:
-            term = mult(giants[g], r_val, keyset)
-        if term is None:
-            return q_val
-        if isinstance(q_val, float):
-            return add_plain(term, q_val) if q_val else term
-        return add(term, q_val)
+        return ["node", g, plan(r), plan(q)]
 
-    result = eval_range(coeffs.copy())
+    root = plan(coeffs.copy())
+    leaves, nodes = [], []
+
+    def walk(t):
+        if t[0] == "leaf":
+            leaves.append(t)
+        elif t[0] == "node":
+            walk(t[2])
+            walk(t[3])
+            nodes.append(t)
+
+    walk(root)
+    values = {}
+
+    def value(t):
+        return t[1] if t[0] == "const" else values[id(t)]
+
+    if leaves:
+        prods = [mult_plain(giants[1], lf[2], rescale_after=False) for lf in leaves]
+        for lf, v in zip(leaves, _split_batch(rescale(_cat_batch(prods)), len(prods), y)):
+            values[id(lf)] = add_plain(v, lf[1])
+    for g in sorted({t[1] for t in nodes}):
+        level_nodes = [t for t in nodes if t[1] == g]
+        groups = {}
+        for t in level_nodes:
+            r_val = value(t[2])
+            if not isinstance(r_val, float):
+                groups.setdefault((r_val.level, r_val.scale), []).append(t)
+        terms = {}
+        for members in groups.values():
+            operands = [value(t[2]) for t in members]
+            prod = mult(giants[g], _cat_batch(operands), keyset)
+            for t, v in zip(members, _split_batch(prod, len(members), y)):
+                terms[id(t)] = v
+        for t in level_nodes:
+            r_val, q_val = value(t[2]), value(t[3])
+            if isinstance(r_val, float):
+                term = None if abs(r_val) <= skip else mult_plain(giants[g], r_val)
+            else:
+                term = terms[id(t)]
+            if term is None:
+                out = q_val
+            elif isinstance(q_val, float):
+                out = add_plain(term, q_val) if q_val else term
+            else:
+                out = add(term, q_val)
+            values[id(t)] = out
+
+    result = value(root)
     if isinstance(result, float):
         result = add_plain(mult_plain(y, 0.0), result)
     return result
+
+
+def _cat_batch(cts):
+    """Stack same-shape ciphertexts (each unbatched or with batch B) into one
+    batch of len(cts) (or len(cts) * B); a single one passes through."""
+    if len(cts) == 1:
+        return cts[0]
+    if cts[0].batch is None:
+        return stack(cts)
+    return concat(cts)
+
+
+def _split_batch(ct, n, like):
+    """Inverse of _cat_batch for n parts shaped like `like`."""
+    if n == 1:
+        return [ct]
+    if like.batch is None:
+        return [ct[i] for i in range(n)]
+    b = like.batch
+    return [ct.narrow(i * b, (i + 1) * b) for i in range(n)]

@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(kEwThreads) k_tensor(const __grid_constant__ T
   if (x >= N) return;
   const PrimeConst pc = P.pc[limb];
   const size_t l = (size_t)limb * N + x;
-  const uint64_t a0 = P.a0[poly * P.as + l], a1 = P.a1[poly * P.as + l];
+  const int64_t ap = (int64_t)(poly % P.amod) * P.as;
+  const uint64_t a0 = P.a0[ap + l], a1 = P.a1[ap + l];
   const uint64_t b0 = P.b0[poly * P.bs + l], b1 = P.b1[poly * P.bs + l];
   P.d0[poly * P.ds + l] = mul_mod(a0, b0, pc);
   Mac128 acc;

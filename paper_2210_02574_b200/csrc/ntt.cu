@@ -40,7 +40,30 @@ struct NttParams {
   int post;
   ulonglong2 fin_s[kMaxPrimes];
   ulonglong2 fin_d[kMaxPrimes];
+  // register passes: blockIdx.y enumerates units (segment, limb, chunk of
+  // ppb polys); all polys of a unit share the prime, hence the twiddles
+  int ppb;
+  int unit_start[kMaxSeg + 1];
 };
+
+// unit -> (segment, limb, first poly, poly count)
+struct UnitPos {
+  int s, limb, p0, np;
+};
+__device__ __forceinline__ UnitPos unit_pos(const NttParams& P, int unit) {
+  UnitPos u;
+  int s = 0;
+#pragma unroll 1
+  while (s + 1 < P.S.n_seg && unit >= P.unit_start[s + 1]) ++s;
+  const Seg& sg = P.S.seg[s];
+  const int r = unit - P.unit_start[s];
+  const int chunk = r / sg.k;
+  u.s = s;
+  u.limb = r - chunk * sg.k;
+  u.p0 = chunk * P.ppb;
+  u.np = min(P.ppb, sg.n_polys - u.p0);
+  return u;
+}
 
 template <bool INV>
 __global__ void __launch_bounds__(256) k_ntt_cols(const __grid_constant__ NttParams P) {
@@ -222,8 +245,16 @@ __global__ void __launch_bounds__(256) k_ntt_blocks(const __grid_constant__ NttP
 // register-radix passes (N >= 2^12): one warp per S-point sub-transform
 // ---------------------------------------------------------------------------
 
-constexpr int kRegWarps = 8;  // the blocks pass's twiddle re-basing assumes 2^3 warps
-static_assert(kRegWarps == 8, "k_ntt_blocks_r twiddle staging uses log2(kRegWarps) == 3");
+#ifndef HEGPU_REG_WARPS_LOG
+#define HEGPU_REG_WARPS_LOG 3
+#endif
+constexpr int kRegWarpsLog = HEGPU_REG_WARPS_LOG;  // warps (sub-transforms) per CTA, log2
+constexpr int kRegWarps = 1 << kRegWarpsLog;
+constexpr int kRegMinBlocks = 8 / kRegWarps;  // scales the launch bounds below
+#ifndef HEGPU_NTT_PPB
+#define HEGPU_NTT_PPB 4
+#endif
+constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
 
 // Shared memory of the register passes (bytes): the cols pass holds its
 // S x 8 tile, the warp buffers and the S twiddle pairs of stages [0, LOGS);
@@ -240,25 +271,20 @@ constexpr size_t blocks_r_smem() {
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 5)) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinBlocks) k_ntt_cols_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   constexpr int TS = kRegWarps + 1;  // padded tile row (conflict-free column reads)
   extern __shared__ uint64_t sm[];
   const int log_n = P.log_n, N = 1 << log_n, C = N >> LOGS;
-  const int row = blockIdx.y;
-  const int s = find_seg(P.S, row);
-  const Seg& sg = P.S.seg[s];
-  const int rr = row - sg.row_start;
-  const int poly = rr / sg.k, limb = rr - poly * sg.k;
-  const int prime = P.S.sel[s][limb];
+  const UnitPos U = unit_pos(P, blockIdx.y);
+  const Seg& sg = P.S.seg[U.s];
+  const int limb = U.limb;
+  const int prime = P.S.sel[U.s][limb];
   const PrimeConst pc = P.pc[prime];
   // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
   const ulonglong2* tw =
       reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
-  const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
-                            : (sg.in + poly * sg.in_stride + (size_t)limb * N);
-  uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
   uint64_t* tile = sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
@@ -266,82 +292,88 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 5)) k_ntt_cols_r(const _
   // every column transform of this pass uses twiddles [1, S) of its table
   for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tw + i);
   const int c0 = blockIdx.x * kRegWarps;
-  if (!INV && sg.csrc != nullptr && sg.cmode == 1) {
-    // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
-    const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
-    const uint64_t qs = sg.csrc_q;
-    for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
-      const int r = e / kRegWarps, c = e % kRegWarps;
-      const uint64_t u = __ldg(hs + c0 + c + (size_t)C * r);
-      const int64_t v = u > (qs >> 1) ? (int64_t)u - (int64_t)qs : (int64_t)u;
-      tile[r * TS + c] = signed_mod(v, pc);
-    }
-  } else if (!INV && sg.csrc != nullptr) {
-    // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
-    const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
-    const uint64_t q = pc.q;
-    const bool centered = sg.cmode == 2;
-    const uint64_t negd = centered ? __ldg(sg.cnegd + limb) : 0;
-    for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
-      const int r = e / kRegWarps, c = e % kRegWarps;
-      const size_t x = c0 + c + (size_t)C * r;
-      Mac128 acc;
-      acc.zero();
-      float f = 0.f;
-      for (int i = 0; i < sg.c_nsrc; ++i) {
-        const uint64_t h = __ldg(hs + (size_t)i * N + x);
-        const uint64_t m = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
-        acc.add(h, m);
-        if (centered)
-          f = fmaf(__uint2float_rn(static_cast<uint32_t>(h >> __ldg(sg.cfs + 2 * i))),
-                   __ldg(sg.cfw + 2 * i), f);
-        if (i % kMacFold == kMacFold - 1) acc.fold(q, pc.bar);
+  const bool centered = sg.cmode == 2;
+  const uint64_t negd = (!INV && centered) ? __ldg(sg.cnegd + limb) : 0;
+  const ulonglong2 fs = P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh);
+  const ulonglong2 fd = P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh);
+#pragma unroll 1
+  for (int pi = 0; pi < U.np; ++pi) {
+    const int poly = U.p0 + pi;
+    const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
+                              : (sg.in + poly * sg.in_stride + (size_t)limb * N);
+    uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
+    if (!INV && sg.csrc != nullptr && sg.cmode == 1) {
+      // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
+      const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
+      const uint64_t qs = sg.csrc_q;
+      for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+        const int r = e / kRegWarps, c = e % kRegWarps;
+        const uint64_t u = __ldg(hs + c0 + c + (size_t)C * r);
+        const int64_t v = u > (qs >> 1) ? (int64_t)u - (int64_t)qs : (int64_t)u;
+        tile[r * TS + c] = signed_mod(v, pc);
       }
-      if (centered) {
-        if (sg.c_nsrc % kMacFold == 0) acc.fold(q, pc.bar);
-        acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
+    } else if (!INV && sg.csrc != nullptr) {
+      // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
+      const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
+      const uint64_t q = pc.q;
+      for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+        const int r = e / kRegWarps, c = e % kRegWarps;
+        const size_t x = c0 + c + (size_t)C * r;
+        Mac128 acc;
+        acc.zero();
+        float f = 0.f;
+        for (int i = 0; i < sg.c_nsrc; ++i) {
+          const uint64_t h = __ldg(hs + (size_t)i * N + x);
+          const uint64_t m = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
+          acc.add(h, m);
+          if (centered)
+            f = fmaf(__uint2float_rn(static_cast<uint32_t>(h >> __ldg(sg.cfs + 2 * i))),
+                     __ldg(sg.cfw + 2 * i), f);
+          if (i % kMacFold == kMacFold - 1) acc.fold(q, pc.bar);
+        }
+        if (centered) {
+          if (sg.c_nsrc % kMacFold == 0) acc.fold(q, pc.bar);
+          acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
+        }
+        tile[r * TS + c] = acc.redc(pc);
       }
-      tile[r * TS + c] = acc.redc(pc);
+    } else {
+      for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+        const int r = e / kRegWarps, c = e % kRegWarps;
+        tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+      }
     }
-  } else {
+    if (pi == 0) cp_async_wait_all();
+    __syncthreads();
+    constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
+    if (!INV)
+      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, stw, pc.q);
+    else
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc, fs, fd);
+#pragma unroll
+    for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
+    __syncthreads();
     for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
       const int r = e / kRegWarps, c = e % kRegWarps;
-      tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+      dst[c0 + c + (size_t)C * r] = tile[r * TS + c];
     }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
-  uint64_t x[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
-  if (!INV)
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, stw, pc.q);
-  else
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc,
-                  P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh),
-                  P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh));
-#pragma unroll
-  for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
-  __syncthreads();
-  for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
-    const int r = e / kRegWarps, c = e % kRegWarps;
-    dst[c0 + c + (size_t)C * r] = tile[r * TS + c];
+    if (pi + 1 < U.np) __syncthreads();  // the tile is reloaded for the next poly
   }
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 4)) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
   const int log_n = P.log_n, N = 1 << log_n, a = log_n - LOGS;
-  const int row = blockIdx.y;
-  const int s = find_seg(P.S, row);
-  const Seg& sg = P.S.seg[s];
-  const int rr = row - sg.row_start;
-  const int poly = rr / sg.k, limb = rr - poly * sg.k;
-  const int prime = P.S.sel[s][limb];
+  const UnitPos U = unit_pos(P, blockIdx.y);
+  const Seg& sg = P.S.seg[U.s];
+  const int limb = U.limb;
+  const int prime = P.S.sel[U.s][limb];
   const PrimeConst pc = P.pc[prime];
   const uint64_t q = pc.q, q2 = q << 1;
   // twiddles are (w, w') Shoup pairs, bit-reversed order, forward then inverse
@@ -350,68 +382,75 @@ __global__ void __launch_bounds__(256, (LOGS >= 9 ? 2 : 4)) k_ntt_blocks_r(const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x * kRegWarps + warp;
   const size_t off = (size_t)limb * N + (size_t)blk * S;
-  const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + off)
-                            : (sg.out + poly * sg.out_stride + off);
-  uint64_t* dst = sg.out + poly * sg.out_stride + off;
   uint64_t* wbuf = sm + warp * Sh::PAD_S;
   ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kRegWarps * Sh::PAD_S);
   constexpr int LO_S = LOGS - EB;
-  uint64_t x[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
   {
-    // stage st of blocks [blk0, blk0 + 8) uses global twiddles
-    // (1 << (a + st)) + (blk0 << st) + [0, 8 << st)  ->  smem (8 << st) + ...
+    // stage st of blocks [blk0, blk0 + W) uses global twiddles
+    // (1 << (a + st)) + (blk0 << st) + [0, W << st)  ->  smem (W << st) + ...
     const int blk0 = blockIdx.x * kRegWarps;
     for (int v = kRegWarps + threadIdx.x; v < kRegWarps * S; v += blockDim.x) {
-      const int st = 31 - __clz(v) - 3;
+      const int st = 31 - __clz(v) - kRegWarpsLog;
       const int i = v - (kRegWarps << st);
       cp_async16(stw + v, tw + (1 << (a + st)) + (blk0 << st) + i);
     }
-    cp_async_wait_all();
-    __syncthreads();
   }
-  if (!INV) {
-    fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 3, warp, stw, q);
-    if (P.epi) {
-      const uint64_t* other = sg.other + poly * sg.other_stride + off;
-      uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
-      const uint64_t cc = P.c[limb], ccsh = P.csh[limb];
+  const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;
+  uint64_t x[E];
+#pragma unroll 1
+  for (int pi = 0; pi < U.np; ++pi) {
+    const int poly = U.p0 + pi;
+    const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + off)
+                              : (sg.out + poly * sg.out_stride + off);
+    uint64_t* dst = sg.out + poly * sg.out_stride + off;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        uint64_t y = x[e];
-        y = y >= q2 ? y - q2 : y;
-        y = y >= q ? y - q : y;
-        uint64_t r = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
-        if (sg.eacc == 1) r = add_mod(r, eout[lane + 32 * e], q);
-        if (sg.eacc == 2)
-          r = add_mod(r, shoup(sg.ein[poly * sg.ein_stride + off + lane + 32 * e], P.es[limb],
-                               P.essh[limb], q),
-                      q);
-        eout[lane + 32 * e] = r;
+    for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
+    if (pi == 0) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (!INV) {
+      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
+      if (P.epi) {
+        const uint64_t* other = sg.other + poly * sg.other_stride + off;
+        uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          uint64_t y = x[e];
+          y = y >= q2 ? y - q2 : y;
+          y = y >= q ? y - q : y;
+          uint64_t r = shoup(other[lane + 32 * e] + q - y, cc, ccsh, q);
+          if (sg.eacc == 1) r = add_mod(r, eout[lane + 32 * e], q);
+          if (sg.eacc == 2)
+            r = add_mod(r, shoup(sg.ein[poly * sg.ein_stride + off + lane + 32 * e],
+                                 P.es[limb], P.essh[limb], q),
+                        q);
+          eout[lane + 32 * e] = r;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          uint64_t y = x[e];
+          y = y >= q2 ? y - q2 : y;
+          dst[lane + 32 * e] = y >= q ? y - q : y;
+        }
       }
-      return;
-    }
+    } else {
+      // re-based table: log_n' = LOGS + log2(warps) (the last-stage scaling
+      // is never in this pass)
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw, pc,
+                    make_ulonglong2(pc.ninv, pc.ninv_sh), make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      uint64_t y = x[e];
-      y = y >= q2 ? y - q2 : y;
-      dst[lane + 32 * e] = y >= q ? y - q : y;
+      for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
     }
-  } else {
-    // re-based table: log_n' = LOGS + 3 (the last-stage scaling is never in this pass)
-    inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + 3, 0, warp, stw, pc,
-                  make_ulonglong2(pc.ninv, pc.ninv_sh), make_ulonglong2(pc.ilast, pc.ilast_sh));
-#pragma unroll
-    for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
   }
 }
 
 template <int LOGS>
-static void launch_cols_r(bool inverse, const NttParams& P, int n_rows, int log_n,
+static void launch_cols_r(bool inverse, const NttParams& P, int n_units, int log_n,
                           cudaStream_t st) {
   const int C = (1 << log_n) >> LOGS;
-  dim3 grid(C / kRegWarps, n_rows);
+  dim3 grid(C / kRegWarps, n_units);
   const size_t smem = cols_r_smem<LOGS>();
   static bool attr_set = false;  // opt in to > 48 KiB dynamic shared memory once
   if (!attr_set) {
@@ -430,10 +469,10 @@ static void launch_cols_r(bool inverse, const NttParams& P, int n_rows, int log_
 }
 
 template <int LOGS>
-static void launch_blocks_r(bool inverse, const NttParams& P, int n_rows, int log_n,
+static void launch_blocks_r(bool inverse, const NttParams& P, int n_units, int log_n,
                             cudaStream_t st) {
   const int R = (1 << log_n) >> LOGS;
-  dim3 grid(R / kRegWarps, n_rows);
+  dim3 grid(R / kRegWarps, n_units);
   const size_t smem = blocks_r_smem<LOGS>();
   static bool attr_set = false;
   if (!attr_set) {
@@ -535,21 +574,34 @@ void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inve
   pb.tile_log = ilog2(bpc);
   if (log_n >= 12) {
     const int logs_b = log_n - a;
+    // units: (segment, limb, chunk of ppb polys); a unit's polys share the
+    // twiddles and the CTA prologue
+    int max_polys = 1;
+    for (int g = 0; g < S.n_seg; ++g) max_polys = std::max(max_polys, S.seg[g].n_polys);
+    const int ppb = std::max(1, std::min(kNttPolysPerCta, max_polys));
+    int n_units = 0;
+    for (int g = 0; g < S.n_seg; ++g) {
+      pa.unit_start[g] = pb.unit_start[g] = n_units;
+      n_units += S.seg[g].k * ((S.seg[g].n_polys + ppb - 1) / ppb);
+    }
+    pa.unit_start[S.n_seg] = pb.unit_start[S.n_seg] = n_units;
+    pa.ppb = pb.ppb = ppb;
+    if (n_units > 65535) throw HegpuError{1, "NTT batch exceeds 65535 units"};
     if (!inverse) {
       pa.epi = 0;
       {
         ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
-        cols_r(a, false, pa, S.n_rows, log_n, st);
+        cols_r(a, false, pa, n_units, log_n, st);
       }
       ProfScope ps(PROF_NTT, st, bytes_pass * (P_epi_guard(epi) ? 1.5 : 1.0), mm_b);
-      blocks_r(logs_b, false, pb, S.n_rows, log_n, st);
+      blocks_r(logs_b, false, pb, n_units, log_n, st);
     } else {
       {
         ProfScope ps(PROF_NTT, st, bytes_pass, rows * nn / 2 * (log_n - a));
-        blocks_r(logs_b, true, pb, S.n_rows, log_n, st);
+        blocks_r(logs_b, true, pb, n_units, log_n, st);
       }
       ProfScope ps(PROF_NTT, st, bytes_pass, mm_a);
-      cols_r(a, true, pa, S.n_rows, log_n, st);
+      cols_r(a, true, pa, n_units, log_n, st);
     }
     check_cuda(cudaGetLastError(), "ntt launch");
     return;

@@ -705,8 +705,9 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
   const uint64_t pm = L.p_mod_ql;
   for (int g = 0; g < 2; ++g) {  // the q_level source row: acc + P * in
     uint64_t* row = acc + (size_t)g * n_ext * N + (size_t)level * N;
-    EwArgs A{HEGPU_OP_AXPYC, in + g * in_c1 + (size_t)level * N, is, row, (int64_t)2 * n_ext * N,
-             row, (int64_t)2 * n_ext * N, B, 1, &lp, &pm};
+    const int64_t rs = (int64_t)2 * n_ext * (int64_t)N;
+    EwArgs A{HEGPU_OP_AXPYC, in + g * in_c1 + (size_t)level * N, is, row, rs, row, rs, B, 1, &lp,
+             &pm};
     launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
   }
   std::vector<int32_t> dsel{level};
@@ -1314,6 +1315,27 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
   })
 }
 
+int hegpu_l2_persist_twiddles(hegpu_ring_t ring, void* stream, double hit_ratio) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "get device");
+    cudaDeviceProp prop;
+    check_cuda(cudaGetDeviceProperties(&prop, dev), "device props");
+    const size_t bytes = (size_t)R.n_primes * 4 * R.n * 8;
+    const size_t carve = std::min<size_t>(bytes, prop.persistingL2CacheMaxSize);
+    check_cuda(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve), "persisting L2 limit");
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.base_ptr = R.dtw;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, prop.accessPolicyMaxWindowSize);
+    attr.accessPolicyWindow.hitRatio = (float)hit_ratio;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    check_cuda(cudaStreamSetAttribute(S_(stream), cudaStreamAttributeAccessPolicyWindow, &attr),
+               "access policy window");
+  })
+}
+
 int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
                       int n_special, hegpu_ring_t* out) {
   HEGPU_TRY({
@@ -1398,10 +1420,20 @@ int hegpu_tensor(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1, int6
                  const uint64_t* b0, const uint64_t* b1, int64_t b_stride, uint64_t* d0,
                  uint64_t* d1, uint64_t* d2, int64_t d_stride, int n_polys, int k,
                  void* stream) {
+  return hegpu_tensor_periodic(ring, a0, a1, a_stride, n_polys, b0, b1, b_stride, d0, d1, d2,
+                               d_stride, n_polys, k, stream);
+}
+
+int hegpu_tensor_periodic(hegpu_ring_t ring, const uint64_t* a0, const uint64_t* a1,
+                          int64_t a_stride, int a_period, const uint64_t* b0, const uint64_t* b1,
+                          int64_t b_stride, uint64_t* d0, uint64_t* d1, uint64_t* d2,
+                          int64_t d_stride, int n_polys, int k, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    if (a_period < 1) throw HegpuError{HEGPU_E_ARG, "a_period must be >= 1"};
     TensorParams T;
+    T.amod = a_period;
     T.a0 = a0;
     T.a1 = a1;
     T.b0 = b0;

@@ -193,6 +193,7 @@ struct TensorParams {
   const uint64_t *a0, *a1, *b0, *b1;
   uint64_t *d0, *d1, *d2;
   int64_t as, bs, ds;
+  int amod;  // operand a of poly p is a[(p % amod) * as] (periodic broadcast)
   int k, log_n;
   const PrimeConst* pc;
 };
