@@ -837,6 +837,7 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
             prod = mult(giants[g], _cat_batch(operands), keyset)
             for t, v in zip(members, _split_batch(prod, len(members), y)):
                 terms[id(t)] = v
+        adds = {}
         for t in level_nodes:
             r_val, q_val = value(t[2]), value(t[3])
             if isinstance(r_val, float):
@@ -844,12 +845,17 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
             else:
                 term = terms[id(t)]
             if term is None:
-                out = q_val
+                values[id(t)] = q_val
             elif isinstance(q_val, float):
-                out = add_plain(term, q_val) if q_val else term
-            else:
-                out = add(term, q_val)
-            values[id(t)] = out
+                values[id(t)] = add_plain(term, q_val) if q_val else term
+            else:  # batched below: the level alignment of q_val is shared
+                key = (term.level, term.scale, q_val.level, q_val.scale)
+                adds.setdefault(key, []).append((t, term, q_val))
+        for members in adds.values():
+            summed = add(_cat_batch([m[1] for m in members]),
+                         _cat_batch([m[2] for m in members]))
+            for m, v in zip(members, _split_batch(summed, len(members), y)):
+                values[id(m[0])] = v
 
     result = value(root)
     if isinstance(result, float):
