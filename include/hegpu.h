@@ -195,11 +195,15 @@ int hegpu_ks_apply_rescale(hegpu_ring_t ring, int level, int alpha, const uint64
  * rotated ciphertexts (c0 at outs[r] + b*cs, c1 at +c1_off).  Input c0 at
  * c + b*cs, c1 at c + b*cs + c1_off.  Decrypts like the unhoisted rotation;
  * limbs are not bit-identical to it (the digit lift commutes with the
- * automorphism only up to a multiple of the digit modulus). */
+ * automorphism only up to a multiple of the digit modulus).
+ * pq_out = 1 (double hoisting): no ModDown; outs[r] receives the P-scaled
+ * extended-basis rotation (n_batch, 2, level+1+K, N) = (P sigma(c0) + kb, ka),
+ * and the outputs must be packed rotation-major (outs[r] = outs[0] +
+ * r*n_batch*2*(level+1+K)*N). */
 int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
                      int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                     uint64_t* const* outs, void* stream);
+                     uint64_t* const* outs, int pq_out, void* stream);
 
 /* Hoisted rotation sum: out = ct + sum_{r < n_rot} rot_r(ct), rot_r = X ->
  * X^galois[r] then a key switch with key r (key_b/key_a: host arrays of
@@ -224,11 +228,15 @@ int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, 
  * (bootstrap.py:243-245 rotates and adds per giant); decrypts identically,
  * limbs differ.  rescale = 1: the final ModDown also divides by q_level
  * (the transform's rescale, bootstrap.py:247) and out is packed
- * (n_batch, 2, level, N) at level - 1. */
+ * (n_batch, 2, level, N) at level - 1.  pq_in = 1 (with rescale = 1): the
+ * partials are P-scaled extended-basis ciphertexts (n_batch, 2, level+1+K, N)
+ * from double-hoisted babies; only each giant's c1 is brought down for its
+ * key switch, one final ModDown by q_level * P remains; partials are
+ * clobbered.  N >= 2^12. */
 int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
                       int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                      uint64_t* out, int rescale, void* stream);
+                      uint64_t* out, int rescale, int pq_in, void* stream);
 
 /* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
  * limbs (eval form), out gets `level` limbs.  in may equal out. */
@@ -273,11 +281,13 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
  * pt_log_run = r in [0, 5]: the diagonals are run-compressed, k limbs of
  * N >> r words each, and coefficient x of limb l reads word (l*N + x) >> r.
  * Evaluation vectors of polynomials in X^(2^r) have this form in the
- * bit-reversed NTT order (slot vectors periodic with period N / 2^(r+1)). */
+ * bit-reversed NTT order (slot vectors periodic with period N / 2^(r+1)).
+ * The last n_special_rows of the k limbs are the special primes (babies in
+ * the extended basis Q_level + P of double-hoisted transforms), else 0. */
 int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
                int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
                int pt_log_run, const int32_t* pt_idx, int n_giants, uint64_t* out,
-               int64_t out_gstride, int k, void* stream);
+               int64_t out_gstride, int k, int n_special_rows, void* stream);
 
 /* -------------------------------------------------------------------------
  * host-array kernel table: drop-in for hebert._kernels (_kernels.py:319-328)

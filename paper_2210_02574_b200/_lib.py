@@ -47,13 +47,13 @@ SIGNATURES = {
     "hegpu_ks_rotsum": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _I64, _I64, _P],
     "hegpu_ks_apply_rescale": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _I64, _I64, _P, _I64,
                                _I64, _P],
-    "hegpu_ks_hoisted": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _P],
-    "hegpu_bsgs_giants": [_P, _I, _I, _P, _I64, _I, _I, _P, _P, _P, _I, _P, _I, _P],
+    "hegpu_ks_hoisted": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _I, _P],
+    "hegpu_bsgs_giants": [_P, _I, _I, _P, _I64, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P],
     "hegpu_rescale": [_P, _I, _P, _I64, _P, _I64, _I, _P],
     "hegpu_mod_raise": [_P, _P, _I64, _P, _I64, _I, _I, _P],
     "hegpu_encrypt_combine": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "hegpu_diag_mac": [_P, _P, _I64, _I64, _P, _I, _I, _P, _I64, _I64, _I, _I, _P],
-    "hegpu_bsgs": [_P, _P, _I, _I64, _I64, _I, _P, _I64, _I, _P, _I, _P, _I64, _I, _P],
+    "hegpu_bsgs": [_P, _P, _I, _I64, _I64, _I, _P, _I64, _I, _P, _I, _P, _I64, _I, _I, _P],
     "hegpu_k_ntt_forward_inplace": [_P, _I, _I, _P, _P, _P],
     "hegpu_k_ntt_inverse_inplace": [_P, _I, _I, _P, _P, _P, _P],
     "hegpu_k_elementwise_mont": [_P, _P, _P, _I, _I, _P, _P],

@@ -675,11 +675,85 @@ def rotate_hoisted(ct, steps, keyset):
     _lib.call(
         "hegpu_ks_hoisted", params.ring.device(), ct.level, params.digit_size,
         src.c0.data.data_ptr(), 2 * k * n, k * n, cnt, len(todo), gal.ctypes.data, kb, ka, dnum,
-        optr, _dev.stream(),
+        optr, 0, _dev.stream(),
     )
     for s, o in zip(todo, outs):
         out[s] = _ct(o, ct.level, ct.scale, ct.slot_count, params, ct.insecure_provenance)
     return [out[int(s) % ct.slot_count] for s in steps]
+
+
+def p_mod_chain(params, k):
+    """P mod q_i (P = product of the special primes) for chain limbs i < k."""
+    p = 1
+    for s in params.ring.special_moduli:
+        p *= int(s)
+    return np.array([p % int(q) for q in params.ring.moduli_chain[:k]], dtype=np.uint64)
+
+
+def to_extended(ct):
+    """P-scaled extended-basis copy of ct: (P c0, P c1) on the chain limbs and
+    0 on the special limbs, packed (..., 2, level+1+K, N) -- the form of a
+    double-hoisted rotation by 0."""
+    params = ct.params
+    k = ct.level + 1
+    n = params.ring_degree
+    K = len(params.ring.special_moduli)
+    src = ct if _pair_group(ct) is not None else ct.copy()
+    cnt = 1 if src.batch is None else src.batch
+    out = _dev.zeros(*(tuple(_lead(ct)) + (2, k + K, n)))
+    _ew_group(params, _lib.OP_SCALAR, src.c0.data.data_ptr(), k * n, None, 0, out.data_ptr(),
+              (k + K) * n, 2 * cnt, k, p_mod_chain(params, k))
+    return out
+
+
+def rotate_hoisted_ext(ct, steps, keyset):
+    """Double-hoisted rotations: one ModUp, then every rotation's inner
+    product stays in the extended basis (no ModDown): returns a packed
+    (len(steps), ..., 2, level+1+K, N) tensor of P-scaled rotations
+    (hegpu_ks_hoisted with pq_out).  Steps must be keyed (or 0)."""
+    import ctypes
+
+    params = ct.params
+    n = params.ring_degree
+    k = ct.level + 1
+    K = len(params.ring.special_moduli)
+    src = ct if _pair_group(ct) is not None else ct.copy()
+    cnt = 1 if src.batch is None else src.batch
+    steps = [int(s) % ct.slot_count for s in steps]
+    out = _dev.empty(*((len(steps),) + tuple(_lead(ct)) + (2, k + K, n)))
+    todo = [i for i, s in enumerate(steps) if s]
+    for i, s in enumerate(steps):
+        if not s:
+            out[i].copy_(to_extended(ct))
+    if not todo:
+        return out
+    if not can_rotate_sum(keyset, [steps[i] for i in todo], ct.slot_count):
+        raise CryptoError("double-hoisted rotations need a key for every step")
+    keys = [keysmod.rotation_key_for(keyset, steps[i] if steps[i] in keyset.rotation_keys
+                                     else steps[i] - ct.slot_count) for i in todo]
+    dnum = keys[0].dnum
+    gal = np.array([keysmod.galois_exponent_for_step(params, steps[i]) % (2 * n) for i in todo],
+                   dtype=np.uint64)
+    kb = (ctypes.c_void_p * (len(todo) * dnum))(
+        *[kk.b[j].data_ptr() for kk in keys for j in range(dnum)])
+    ka = (ctypes.c_void_p * (len(todo) * dnum))(
+        *[kk.a[j].data_ptr() for kk in keys for j in range(dnum)])
+    # the rotated outputs must be packed back to back: compute into a dense
+    # block, then scatter if step 0 sits in between
+    block = out if todo == list(range(len(todo))) else _dev.empty(
+        *((len(todo),) + tuple(_lead(ct)) + (2, k + K, n)))
+    optr = (ctypes.c_void_p * len(todo))(*[block[i].data_ptr() for i in range(len(todo))])
+    for _ in todo:
+        _stats.count("ks", ct.level, cnt)
+    _lib.call(
+        "hegpu_ks_hoisted", params.ring.device(), ct.level, params.digit_size,
+        src.c0.data.data_ptr(), 2 * k * n, k * n, cnt, len(todo), gal.ctypes.data, kb, ka, dnum,
+        optr, 1, _dev.stream(),
+    )
+    if block is not out:
+        for j, i in enumerate(todo):
+            out[i].copy_(block[j])
+    return out
 
 
 def _keyed(keyset, s, slot_count):

@@ -757,6 +757,10 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant_
           uint64_t* ob = o + (size_t)(b0 + b) * P.acc_sb;
           uint64_t vb = mont_mul(ab[b].redc(pc), pc.r2, pc.q, pc.qinv_neg);
           uint64_t va = mont_mul(aa[b].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+          if (P.c0 && r <= P.level)
+            vb = add_mod(vb, shoup(__ldg(P.c0 + (size_t)(b0 + b) * P.c0s + (size_t)r * N + src),
+                                   P.pm[r], P.pm_sh[r], pc.q),
+                         pc.q);
           if (P.accumulate) {
             vb = add_mod(vb, ob[0], pc.q);
             va = add_mod(va, ob[(size_t)P.n_ext * N], pc.q);
@@ -787,6 +791,7 @@ void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
 }
 
 struct AutoSumParams {
+  int kq, n_chain;  // limbs >= kq: special primes
   const uint64_t* in;
   int64_t is, in_sr;  // rotation r permutes in + r*in_sr
   const uint64_t* base;  // out = base + sum_r sigma_r(in); base == in when null
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(kEwThreads) k_auto_sum(const __grid_constant__
   const int x = blockIdx.x * kEwThreads + threadIdx.x;
   if (x >= N) return;
   const int poly = row / P.k, limb = row - poly * P.k;
-  const uint64_t q = P.pc[limb].q;
+  const uint64_t q = P.pc[limb < P.kq ? limb : P.n_chain + (limb - P.kq)].q;
   const uint64_t* in = P.in + poly * P.is + (size_t)limb * N;
   uint64_t s = P.base ? P.base[poly * P.bs + (size_t)limb * N + x] : in[x];
   for (int r = 0; r < P.n_rot; ++r)
@@ -815,9 +820,11 @@ __global__ void __launch_bounds__(kEwThreads) k_auto_sum(const __grid_constant__
 void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
                      const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
                      uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st,
-                     int64_t in_sr) {
+                     int64_t in_sr, int kq, int n_chain) {
   if (n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
   AutoSumParams P;
+  P.kq = kq < 0 ? k : kq;
+  P.n_chain = n_chain;
   P.in = in;
   P.is = is;
   P.in_sr = in_sr;
@@ -928,6 +935,7 @@ struct BsgsParams {
   uint64_t* out;
   int64_t out_gstride;              // elements between giants' outputs
   const PrimeConst* pc;
+  int kq, n_chain;                  // limbs >= kq are special primes n_chain + (limb - kq)
 };
 
 // CTA = 32 warps over a 64-coefficient tile of one limb; warp w accumulates
@@ -946,7 +954,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
   const int x0 = blockIdx.x * kBsgsTile;
-  const PrimeConst pc = P.pc[limb];
+  const PrimeConst pc = P.pc[limb < P.kq ? limb : P.n_chain + (limb - P.kq)];
   constexpr int per_term = NB * 2 * kBsgsTile;
   const int nthr = WARPS * 32;
   const int g0 = blockIdx.z * WARPS;  // first giant of this CTA
@@ -1096,7 +1104,7 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
   const int p = threadIdx.x % PAIRS, gg = threadIdx.x / PAIRS;
   const int c = p / (kRunTile / 2), xl = (p % (kRunTile / 2)) * 2;
   const int run = xl >> LR;
-  const PrimeConst pc = P.pc[limb];
+  const PrimeConst pc = P.pc[limb < P.kq ? limb : P.n_chain + (limb - P.kq)];
   // products < q^2; fold often enough to stay below 2^128 (see Mac128)
   const int fold_every = pc.q < (1ull << 61) ? 32 : kMacFold;
   Mac128 acc[kRunGpt][2];
@@ -1171,7 +1179,8 @@ static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
                  int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
-                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st) {
+                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st, int kq,
+                 int n_chain) {
   if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
   if (pt_log_run < 0 || pt_log_run > 5 || pt_log_run >= log_n)
     throw HegpuError{HEGPU_E_ARG, "bsgs: pt_log_run must be in [0, 5]"};
@@ -1195,6 +1204,8 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
       P.out = out + (size_t)g0 * out_gstride + b0 * bstride;
       P.out_gstride = out_gstride;
       P.pc = dpc;
+      P.kq = kq;
+      P.n_chain = n_chain;
       const double el = (double)k * (1 << log_n);
       ProfScope ps(PROF_DIAG_MAC, st,
                    el * 8.0 * ((double)P.n_giants * n_terms / (1 << pt_log_run) +

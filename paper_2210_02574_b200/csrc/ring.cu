@@ -646,6 +646,51 @@ static void ks_moddown(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr,
 }
 
 
+// ModDown of single polys in the extended basis (P-scaled, eval form):
+// out = (in - conv(in_P)) * P^-1 over the chain limbs 0..level.  The special
+// rows of `in` are overwritten (post-scaled INTT in place).  N >= 2^12.
+static void ks_moddown_polys(Ring& R, const KsLevel& L, uint64_t* in, int64_t is, int n_polys,
+                             uint64_t* out, int64_t os, uint64_t* corr, cudaStream_t st) {
+  NttTagScope tag_(NTT_TAG_MODDOWN);
+  const int k = L.level + 1, K = R.n_special;
+  const size_t N = R.n;
+  if (R.log_n < 12 || K == 0) throw HegpuError{HEGPU_E_ARG, "ModDown of polys needs N >= 2^12"};
+  const std::vector<int32_t> sp = range_primes(R.n_chain, K);
+  SegSet S0;
+  S0.n_seg = 0;
+  S0.n_rows = 0;
+  add_seg(S0, in + (size_t)k * N, is, in + (size_t)k * N, is, n_polys, K, sp.data());
+  NttEpilogue E0;
+  E0.post = true;
+  for (int i = 0; i < K; ++i) {
+    E0.fin_s[i] = L.md_fin_s[i];
+    E0.fin_d[i] = L.md_fin_d[i];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+  const std::vector<int32_t> chain = range_primes(0, k);
+  SegSet S;
+  S.n_seg = 0;
+  S.n_rows = 0;
+  add_seg(S, corr, (int64_t)k * N, corr, (int64_t)k * N, n_polys, k, chain.data());
+  Seg& sg = S.seg[0];
+  sg.other = in;
+  sg.other_stride = is;
+  sg.eout = out;
+  sg.eout_stride = os;
+  sg.csrc = in + (size_t)k * N;
+  sg.csrc_stride = is;
+  sg.cpunc = L.md_punc;
+  sg.c_nsrc = K;
+  sg.cpunc_ld = k;
+  NttEpilogue E;
+  E.enabled = true;
+  for (int t = 0; t < k; ++t) {
+    E.c[t] = L.pinv[t];
+    E.csh[t] = L.pinv_sh[t];
+  }
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+}
+
 static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
                       const uint64_t* ext, int B, const uint64_t* const* key_b,
                       const uint64_t* const* key_a, uint64_t* acc, uint64_t* corr,
@@ -694,6 +739,8 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
   const int level = L.level, K = R.n_special, n_ext = L.n_ext;
   const size_t N = R.n;
   if (level < 1) throw HegpuError{HEGPU_E_ARG, "rescale at level 0"};
+  if (!in && (R.log_n < 12 || K == 0))
+    throw HegpuError{HEGPU_E_ARG, "extended-basis ModDown-rescale needs N >= 2^12"};
   if (R.log_n < 12 || K == 0) {
     ks_moddown(R, L, acc, corr, B, in, is, in + in_c1, is, st, true, true);
     rescale_impl(R, level, in, is, out, os, B, st);
@@ -703,7 +750,7 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
   NttTagScope tag_(NTT_TAG_MODDOWN);
   const int32_t lp = level;
   const uint64_t pm = L.p_mod_ql;
-  for (int g = 0; g < 2; ++g) {  // the q_level source row: acc + P * in
+  for (int g = 0; g < 2 && in; ++g) {  // the q_level source row: acc + P * in
     uint64_t* row = acc + (size_t)g * n_ext * N + (size_t)level * N;
     const int64_t rs = (int64_t)2 * n_ext * (int64_t)N;
     EwArgs A{HEGPU_OP_AXPYC, in + g * in_c1 + (size_t)level * N, is, row, rs, row, rs, B, 1, &lp,
@@ -736,8 +783,8 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
     sg.other_stride = (int64_t)2 * n_ext * N;
     sg.eout = out + g * out_c1;
     sg.eout_stride = os;
-    sg.eacc = 2;
-    sg.ein = in + g * in_c1;
+    sg.eacc = in ? 2 : 0;  // in == nullptr: acc already holds P * in + KS (extended basis)
+    sg.ein = in ? in + g * in_c1 : nullptr;
     sg.ein_stride = is;
     sg.csrc = acc + (size_t)g * n_ext * N + (size_t)level * N;
     sg.csrc_stride = (int64_t)2 * n_ext * N;
@@ -794,7 +841,8 @@ static void ks_apply_rescale_impl(Ring& R, int level, int alpha, const uint64_t*
 static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, int64_t cs,
                             int64_t c1_off, int B, int n_rot, const uint64_t* galois,
                             const uint64_t* const* key_b, const uint64_t* const* key_a,
-                            int n_digits, uint64_t* const* outs, cudaStream_t st) {
+                            int n_digits, uint64_t* const* outs, cudaStream_t st,
+                            bool pq_out = false) {
   if (B <= 0 || n_rot <= 0) return;
   const KsLevel& L = R.ks_level(level, alpha);
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
@@ -802,8 +850,58 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
   if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
   if (beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many digits for hoisting"};
   // outputs laid out back to back (rotation-major) share one batched ModDown
+  const int64_t ocs = pq_out ? (int64_t)2 * n_ext * N : cs;  // output ct stride
   bool uniform = true;
-  for (int r = 1; r < n_rot; ++r) uniform &= outs[r] == outs[0] + (int64_t)r * B * cs;
+  for (int r = 1; r < n_rot; ++r) uniform &= outs[r] == outs[0] + (int64_t)r * B * ocs;
+  if (pq_out) {
+    // double hoisting: the rotations stay in the extended basis Q_level + P,
+    // P-scaled (c0' = P sigma(c0) + kb, c1' = ka); no ModDown at all.  The
+    // inner-product launch writes them directly (c0 term fused).
+    if (!uniform) throw HegpuError{HEGPU_E_ARG, "extended-basis outputs must be packed"};
+    const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
+    Scratch ws((sz_dc + sz_ext) * 8, st);
+    uint64_t* dcoeff = ws.u64();
+    uint64_t* ext = dcoeff + sz_dc;
+    ks_modup(R, L, c + c1_off, cs, B, dcoeff, ext, st);
+    const std::vector<uint64_t> sp(R.primes.begin() + R.n_chain, R.primes.end());
+    for (int r0 = 0; r0 < n_rot; r0 += kMaxRot) {
+      const int nr = std::min(kMaxRot, n_rot - r0);
+      IpRotParams P{};
+      P.d = c + c1_off;
+      P.ds = cs;
+      P.ext = ext;
+      P.ext_sb = (int64_t)beta * n_ext * N;
+      P.ext_sj = (int64_t)n_ext * N;
+      for (int r = 0; r < nr; ++r) {
+        P.gal[r] = (uint32_t)galois[r0 + r];
+        for (int j = 0; j < beta; ++j) {
+          P.kb[r][j] = key_b[(size_t)(r0 + r) * n_digits + j];
+          P.ka[r][j] = key_a[(size_t)(r0 + r) * n_digits + j];
+        }
+      }
+      P.n_rot = nr;
+      P.acc = outs[r0];
+      P.acc_sb = ocs;
+      P.acc_sr = (int64_t)B * ocs;
+      P.level = level;
+      P.alpha = alpha;
+      P.beta = beta;
+      P.n_ext = n_ext;
+      P.n_chain = R.n_chain;
+      P.key_sp_row0 = R.n_chain;
+      P.n_batch = B;
+      P.log_n = R.log_n;
+      P.pc = R.dpc;
+      P.c0 = c;
+      P.c0s = cs;
+      for (int t = 0; t < k; ++t) {
+        P.pm[t] = prod_mod(sp, -1, R.primes[t]);
+        P.pm_sh[t] = h_shoup(P.pm[t], R.primes[t]);
+      }
+      launch_ks_ip_rot(P, st);
+    }
+    return;
+  }
   const int CH = kMaxRot;
   const size_t sz_dc = (size_t)B * k * N, sz_ext = (size_t)B * beta * n_ext * N;
   const size_t sz_acc = (size_t)B * 2 * n_ext * N, sz_corr = (size_t)B * 2 * k * N;
@@ -819,7 +917,7 @@ static void ks_hoisted_impl(Ring& R, int level, int alpha, const uint64_t* c, in
     const int nr = std::min(CH, n_rot - r0);
     // the nr rotations' inner products in one launch, digits gathered through
     // X -> X^g[r] (no permuted copies), one acc per rotation
-    IpRotParams P;
+    IpRotParams P{};
     P.d = c1;
     P.ds = cs;
     P.d_sr = 0;
@@ -910,7 +1008,7 @@ static void ks_rotsum_impl(Ring& R, int level, int alpha, const uint64_t* c, int
   ks_modup(R, L, c + c1_off, cs, B, dcoeff, ext, st);
   for (int r0 = 0; r0 < n_rot; r0 += kMaxRot) {
     const int nr = std::min(kMaxRot, n_rot - r0);
-    IpRotParams P;
+    IpRotParams P{};
     P.d = c + c1_off;
     P.ds = cs;
     P.d_sr = 0;
@@ -955,6 +1053,11 @@ static void ks_rotsum_impl(Ring& R, int level, int alpha, const uint64_t* c, int
 // out = partial[0] + sum_g rot_g(partial[g]) at `level`; with `down` the
 // final ModDown is fused with the rescale and writes `down` (level - 1)
 // instead (out is then clobbered scratch).
+static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials,
+                               int64_t gstride, int B, int n_giants, const uint64_t* galois,
+                               const uint64_t* const* key_b, const uint64_t* const* key_a,
+                               int n_digits, uint64_t* down, cudaStream_t st);
+
 static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* partials,
                             int64_t gstride, int B, int n_giants, const uint64_t* galois,
                             const uint64_t* const* key_b, const uint64_t* const* key_a,
@@ -998,7 +1101,7 @@ static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* parti
     const int ng = std::min(CH, n_giants - g0);
     const uint64_t* c1 = partials + g0 * gstride + (size_t)k * N;
     ks_modup(R, L, c1, cs, ng * B, dcoeff, ext, st);
-    IpRotParams P;
+    IpRotParams P{};
     P.d = c1;
     P.ds = cs;
     P.d_sr = gstride;
@@ -1037,6 +1140,100 @@ static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* parti
     return;
   }
   ks_moddown(R, L, acc, corr, B, out, cs, out + (size_t)k * N, cs, st, true, true);
+}
+
+// Giant steps of a double-hoisted transform: the partial sums are P-scaled
+// extended-basis ciphertexts (babies never went through ModDown).  Per giant
+// g >= 1 only c1 is brought down (one-poly ModDown, needed for its digit
+// decomposition); the permuted c0 parts and every giant's inner products
+// accumulate in the extended basis, and ONE ModDown by q_level * P (fused
+// with the transform's rescale) ends at level - 1 in `down`.  partials
+// (packed (n_giants, B, 2, n_ext, N)) are clobbered.  N >= 2^12.
+static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials,
+                               int64_t gstride, int B, int n_giants, const uint64_t* galois,
+                               const uint64_t* const* key_b, const uint64_t* const* key_a,
+                               int n_digits, uint64_t* down, cudaStream_t st) {
+  const KsLevel& L = R.ks_level(level, alpha);
+  const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
+  const size_t N = R.n;
+  const int64_t cs = (int64_t)2 * n_ext * N;
+  if (level < 1) throw HegpuError{HEGPU_E_ARG, "rescale at level 0"};
+  if (n_digits < beta) throw HegpuError{HEGPU_E_ARG, "switching key has too few digits"};
+  if (beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many digits for giant steps"};
+  if (gstride != (int64_t)B * cs) throw HegpuError{HEGPU_E_ARG, "partials must be packed"};
+  const std::vector<int32_t> ext_rows = [&] {
+    std::vector<int32_t> v = range_primes(0, k);
+    for (int i = 0; i < R.n_special; ++i) v.push_back(R.n_chain + i);
+    return v;
+  }();
+  std::vector<uint32_t> gal(std::max(n_giants, 1));
+  for (int g = 0; g < n_giants; ++g) gal[g] = (uint32_t)galois[g];
+  const int CH = kMaxRot;
+  const size_t sz_pq = (size_t)B * cs, sz_q = (size_t)CH * B * k * N;
+  const size_t sz_ext = (size_t)CH * B * beta * n_ext * N;
+  Scratch ws((sz_pq + 2 * sz_q + sz_ext + sz_pq + sz_q) * 8, st);
+  uint64_t* sum = ws.u64();     // (B, 2, n_ext, N)
+  uint64_t* c1q = sum + sz_pq;  // (CH*B, k, N)
+  uint64_t* dcoeff = c1q + sz_q;
+  uint64_t* ext = dcoeff + sz_q;
+  uint64_t* acc = ext + sz_ext;  // (B, 2, n_ext, N)
+  uint64_t* corr = acc + sz_pq;  // >= CH*B*k*N and >= B*2*level*N
+  // sum.c0 = partial[0].c0 + sum_g sigma_g(partial[g].c0); sum.c1 = partial[0].c1
+  for (int g0 = 1; g0 < std::max(n_giants, 2); g0 += kMaxRot) {
+    const int ng = std::max(0, std::min(kMaxRot, n_giants - g0));
+    launch_auto_sum(R.dpc, R.log_n, gal.data() + g0, ng, partials + g0 * gstride, cs,
+                    g0 == 1 ? partials : sum, cs, sum, cs, B, n_ext, st, gstride, k, R.n_chain);
+  }
+  {
+    EwArgs A{HEGPU_OP_COPY, partials + (size_t)n_ext * N, cs, nullptr, 0, sum + (size_t)n_ext * N,
+             cs, B, n_ext, ext_rows.data(), nullptr};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
+  }
+  bool first = true;
+  for (int g0 = 1; g0 < n_giants; g0 += CH) {
+    const int ng = std::min(CH, n_giants - g0);
+    ks_moddown_polys(R, L, partials + g0 * gstride + (size_t)n_ext * N, cs, ng * B, c1q,
+                     (int64_t)k * N, corr, st);
+    ks_modup(R, L, c1q, (int64_t)k * N, ng * B, dcoeff, ext, st);
+    IpRotParams P{};
+    P.d = c1q;
+    P.ds = (int64_t)k * N;
+    P.d_sr = (int64_t)B * k * N;
+    P.ext = ext;
+    P.ext_sb = (int64_t)beta * n_ext * N;
+    P.ext_sj = (int64_t)n_ext * N;
+    P.ext_sr = (int64_t)B * beta * n_ext * N;
+    for (int r = 0; r < ng; ++r) {
+      P.gal[r] = gal[g0 + r];
+      for (int j = 0; j < beta; ++j) {
+        P.kb[r][j] = key_b[(size_t)(g0 + r) * n_digits + j];
+        P.ka[r][j] = key_a[(size_t)(g0 + r) * n_digits + j];
+      }
+    }
+    P.n_rot = ng;
+    P.sum_mode = 1;
+    P.accumulate = first ? 0 : 1;
+    P.acc = acc;
+    P.acc_sb = cs;
+    P.level = level;
+    P.alpha = alpha;
+    P.beta = beta;
+    P.n_ext = n_ext;
+    P.n_chain = R.n_chain;
+    P.key_sp_row0 = R.n_chain;
+    P.n_batch = B;
+    P.log_n = R.log_n;
+    P.pc = R.dpc;
+    launch_ks_ip_rot(P, st);
+    first = false;
+  }
+  if (!first) {  // sum += the giants' switched parts (both components, extended basis)
+    EwArgs A{HEGPU_OP_ADD, sum, (int64_t)n_ext * N, acc, (int64_t)n_ext * N, sum,
+             (int64_t)n_ext * N, 2 * B, n_ext, ext_rows.data(), nullptr};
+    launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
+  }
+  ks_moddown_rescale(R, L, sum, corr, B, nullptr, 0, 0, down, (int64_t)2 * level * N,
+                     (int64_t)level * N, st);
 }
 
 static void bsgs_giants_impl(Ring& R, int level, int alpha, const uint64_t* partials,
@@ -1487,20 +1684,26 @@ int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, 
 int hegpu_ks_hoisted(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, int64_t cs,
                      int64_t c1_off, int n_batch, int n_rot, const uint64_t* galois,
                      const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                     uint64_t* const* outs, void* stream) {
+                     uint64_t* const* outs, int pq_out, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
     ks_hoisted_impl(R, level, alpha, c, cs, c1_off, n_batch, n_rot, galois, key_b, key_a,
-                    n_digits, outs, S_(stream));
+                    n_digits, outs, S_(stream), pq_out != 0);
   })
 }
 
 int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
                       int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
-                      uint64_t* out, int rescale, void* stream) {
+                      uint64_t* out, int rescale, int pq_in, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
+    if (pq_in) {
+      if (!rescale) throw HegpuError{HEGPU_E_ARG, "extended-basis giants need rescale = 1"};
+      bsgs_giants_sum_pq(R, level, alpha, const_cast<uint64_t*>(partials), gstride, n_batch,
+                         n_giants, galois, key_b, key_a, n_digits, out, S_(stream));
+      return HEGPU_OK;
+    }
     bsgs_giants_impl(R, level, alpha, partials, gstride, n_batch, n_giants, galois, key_b, key_a,
                      n_digits, out, S_(stream), rescale != 0);
   })
@@ -1557,12 +1760,16 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
 int hegpu_bsgs(hegpu_ring_t ring, const uint64_t* const* babies, int n_terms, int64_t c1_off,
                int64_t bstride, int n_batch, const uint64_t* pt_base, int64_t pt_stride,
                int pt_log_run, const int32_t* pt_idx, int n_giants, uint64_t* out,
-               int64_t out_gstride, int k, void* stream) {
+               int64_t out_gstride, int k, int n_special_rows, void* stream) {
   HEGPU_TRY({
     Ring& R = RR(ring);
-    if (k > R.n_chain) throw HegpuError{HEGPU_E_ARG, "too many limbs"};
+    if (n_special_rows < 0 || n_special_rows > R.n_special)
+      throw HegpuError{HEGPU_E_ARG, "bad special row count"};
+    if (k - n_special_rows > R.n_chain || k <= n_special_rows)
+      throw HegpuError{HEGPU_E_ARG, "too many limbs"};
     launch_bsgs(R.dpc, R.log_n, babies, n_terms, c1_off, bstride, n_batch, pt_base, pt_stride,
-                pt_log_run, pt_idx, n_giants, out, out_gstride, k, S_(stream));
+                pt_log_run, pt_idx, n_giants, out, out_gstride, k, S_(stream),
+                k - n_special_rows, R.n_chain);
   })
 }
 

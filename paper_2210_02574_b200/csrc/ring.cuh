@@ -241,14 +241,21 @@ struct IpRotParams {
   int64_t acc_sb, acc_sr;
   int level, alpha, beta, n_ext, n_chain, key_sp_row0, n_batch, log_n;
   const PrimeConst* pc;
+  // optional (separate mode): the b part of rows <= level also gets
+  // P * sigma_r(c0) (double-hoisted rotations output P-scaled extended-basis
+  // ciphertexts); c0 of batch element b at c0 + b*c0s
+  const uint64_t* c0;
+  int64_t c0s;
+  uint64_t pm[kMaxPrimes], pm_sh[kMaxPrimes];  // P mod q_r, Shoup
 };
 void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st);
 // out[b] = base[b] + sum_r sigma_r(in[b] + r*in_sr) (eval form, k limbs;
-// base = the unpermuted in when null)
+// base = the unpermuted in when null).  Limbs >= kq are special primes
+// n_chain + (limb - kq) (extended-basis operands); kq < 0: all chain.
 void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int n_rot,
                      const uint64_t* in, int64_t is, const uint64_t* base, int64_t bs,
                      uint64_t* out, int64_t os, int n_polys, int k, cudaStream_t st,
-                     int64_t in_sr = 0);
+                     int64_t in_sr = 0, int kq = -1, int n_chain = 0);
 
 void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint64_t g,
                          const uint64_t* in, int64_t is, uint64_t* out, int64_t os, int n_polys,
@@ -266,6 +273,7 @@ double bench_modmul_peak(int iters);
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
                  int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
-                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st);
+                 uint64_t* out, int64_t out_gstride, int k, cudaStream_t st, int kq,
+                 int n_chain);
 
 }  // namespace hegpu

@@ -132,8 +132,8 @@ def test_batched_ops_equal_single():
         assert np.array_equal(coeff.limbs[i], ring.to_coeff(x).limbs)
 
 
-@pytest.mark.parametrize("lr", [2, 4, 5])
-def test_bsgs_run_compressed_matches_dense_and_exact(lr):
+@pytest.mark.parametrize("lr,ns", [(2, 0), (4, 0), (5, 0), (4, 2)])
+def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns):
     """hegpu_bsgs on run-compressed diagonals (pt_log_run, the sparse-bootstrap
     cache layout; lr >= 4 takes the shared-memory GEMM kernel) equals the dense
     kernel on the expanded diagonals and the exact sum mod q."""
@@ -144,8 +144,10 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr):
     from paper_2210_02574_b200 import _dev, _lib, ckks
 
     params = ckks.get_preset("desk")
-    n, k, T, G, nb = params.ring_degree, 3, 21, 5, 2
-    qs = [int(q) for q in params.ring.moduli_chain[:k]]
+    n, k, T, G, nb = params.ring_degree, 3 + ns, 21, 5, 2
+    # ns > 0: the last ns limbs are special primes (extended-basis babies)
+    qs = ([int(q) for q in params.ring.moduli_chain[:k - ns]]
+          + [int(q) for q in params.ring.special_moduli[:ns]])
     rng = np.random.default_rng(lr)
 
     def rand(shape):
@@ -163,7 +165,7 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr):
         out = _dev.empty(G, nb, 2, k, n)
         _lib.call("hegpu_bsgs", params.ring.device(), ptrs, T, k * n, 2 * k * n, nb,
                   pd.data_ptr(), k * (n >> run_log), run_log, idx_d.data_ptr(), G,
-                  out.data_ptr(), nb * 2 * k * n, k, _dev.stream())
+                  out.data_ptr(), nb * 2 * k * n, k, ns, _dev.stream())
         outs.append(out.cpu().numpy().view(np.uint64))
     assert np.array_equal(outs[0], outs[1])
     bab = babies.cpu().numpy().view(np.uint64)

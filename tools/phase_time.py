@@ -1,0 +1,53 @@
+"""Split one cfg4 training minibatch into its phases (gradient, sum, update,
+bootstrap refresh) with CUDA-event timing and per-class kernel profiles."""
+import os
+import sys
+
+os.environ["BENCH_GRAPH"] = "0"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2210_02574_b200 import _lib, logreg  # noqa: E402
+from paper_2210_02574_b200.ckks import ops  # noqa: E402
+
+wl = bench.TrainWorkload()
+wl.setup(0, 1)
+xb, yb = wl.pool_dev[0]
+cfg, keys, sig, layout = wl.cfg, wl.keys, wl.sig, wl.layout
+
+
+def ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+for it in range(3):
+    w, u = wl.w, wl.u
+    t0 = ev()
+    gu = ops.mult_plain(u, cfg.momentum_gamma)
+    wl_ = ops.sub(w, gu)
+    t1 = ev()
+    g = logreg._batched_gradient(xb, yb, wl_, layout, keys, sig, cfg.learning_rate, wl.batch_rows)
+    t2 = ev()
+    G = logreg._sum_gradient(g, layout, keys)
+    t3 = ev()
+    u2 = ops.add(gu, G)
+    w2 = ops.sub(w, u2)
+    t4 = ev()
+    w3, u3 = wl.refresher.refresh_many([w2, u2])
+    t5 = ev()
+    torch.cuda.synchronize()
+    print(f"iter {it}: lookahead {t0.elapsed_time(t1):.1f} gradient {t1.elapsed_time(t2):.1f} "
+          f"sum+rotsum {t2.elapsed_time(t3):.1f} update {t3.elapsed_time(t4):.1f} "
+          f"refresh {t4.elapsed_time(t5):.1f} ms")
+for name, fn in (("gradient", lambda: logreg._batched_gradient(xb, yb, wl.w, layout, keys, sig,
+                                                                cfg.learning_rate, wl.batch_rows)),
+                 ("refresh", lambda: wl.refresher.refresh_many([wl.w, wl.u]))):
+    _lib.profile_enable(True)
+    fn()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    print(name, {c: round(p["ms"], 1) for c, p in prof.items() if p["launches"]},
+          {c: p["launches"] for c, p in prof.items() if p["launches"]})
