@@ -274,7 +274,7 @@ int hegpu_diag_mac(hegpu_ring_t ring, const uint64_t* const* ct_ptrs, int64_t ct
  * for every giant g < n_giants and batch element b < n_batch,
  *   out[g]_b.c{0,1} = sum_{t < n_terms} pt[idx[g][t]] * baby[t]_b.c{0,1}
  * with baby[t]_b.c0 at babies[t] + b*bstride, c1 at +c1_off (host array of
- * n_terms <= 64 device pointers); diagonal i at pt_base + i*pt_stride;
+ * n_terms <= 128 device pointers); diagonal i at pt_base + i*pt_stride;
  * pt_idx a DEVICE int32 array [n_giants][n_terms] (-1 = zero diagonal);
  * out[g]_b.c0 at out + g*out_gstride + b*bstride, c1 at +c1_off.  Every
  * diagonal, baby and output crosses HBM once.

@@ -21,6 +21,10 @@ def enable(on=True):
         _counts.clear()
 
 
+def enabled():
+    return _enabled[0]
+
+
 def count(op, level, n=1):
     if _enabled[0]:
         _counts[(op, int(level))] += int(n)

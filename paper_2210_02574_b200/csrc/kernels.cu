@@ -922,7 +922,7 @@ namespace hegpu {
 // diagonal, every baby and every output is touched exactly once (the per-giant
 // formulation re-reads all babies once per giant).
 // ---------------------------------------------------------------------------
-constexpr int kBsgsMaxTerms = 64;
+constexpr int kBsgsMaxTerms = 128;
 
 struct BsgsParams {
   const uint64_t* baby[kBsgsMaxTerms];
@@ -1057,9 +1057,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
 // stored [term][run][giant]) per term.
 constexpr int kRunTile = 32;   // coefficients per CTA
 constexpr int kRunGiants = 32; // giants per CTA (grid.z covers more)
+constexpr int kRunChunk = 64;  // terms staged in shared memory at a time
 
-constexpr size_t bsgs_run_smem(int n_terms) {
-  return (size_t)n_terms * 2 * kRunTile * 8 + (size_t)kRunGiants * n_terms * 2 * 8;
+constexpr size_t bsgs_run_smem(int n_terms, int rt) {
+  return (size_t)(n_terms < kRunChunk ? n_terms : kRunChunk) * (2 * kRunTile + kRunGiants * rt) *
+         8;
 }
 
 // RT = runs per tile (2 for pt_log_run 4, 1 for 5); one batch element per CTA.
@@ -1069,37 +1071,16 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
   constexpr int kRunGpt = GPT;
   extern __shared__ __align__(16) uint64_t sm[];
   constexpr int COLS = 2 * kRunTile;  // (c0, c1) x 32 coefficients
-  constexpr int LR = RT == 2 ? 4 : 5;
+  constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
   const int x0 = blockIdx.x * kRunTile;
   const int g0 = blockIdx.z * kRunGiants;
   const int T = P.n_terms;
-  uint64_t* bab = sm;                     // [T][2][32]
-  uint64_t* pts = sm + (size_t)T * COLS;  // [T][RT][32 giants]
-  for (int e = threadIdx.x; e < T * COLS / 2; e += blockDim.x) {
-    const int t = e / (COLS / 2), rem = e - t * (COLS / 2);
-    const int c = rem / (kRunTile / 2), xx = (rem - c * (kRunTile / 2)) * 2;
-    cp_async16(bab + (size_t)t * COLS + c * kRunTile + xx,
-               P.baby[t] + c * P.c1_off + (size_t)limb * N + x0 + xx);
-  }
-  const size_t pcol = ((size_t)limb * N + x0) >> LR;
-  for (int e = threadIdx.x; e < kRunGiants * T; e += blockDim.x) {
-    const int g = e / T, t = e - g * T;
-    const int idx = g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + t) : -1;
-    uint64_t* d = pts + (size_t)t * RT * kRunGiants + g;
-    if (RT == 2) {
-      const ulonglong2 v = idx < 0 ? make_ulonglong2(0, 0)
-                                   : __ldg(reinterpret_cast<const ulonglong2*>(
-                                         P.pt_base + (size_t)idx * P.pt_stride + pcol));
-      d[0] = v.x;
-      d[kRunGiants] = v.y;
-    } else {
-      d[0] = idx < 0 ? 0 : __ldg(P.pt_base + (size_t)idx * P.pt_stride + pcol);
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
+  // terms are staged kRunChunk at a time (babies [t][2][32], diagonals
+  // [t][RT][32 giants]); the accumulators carry over between chunks
+  uint64_t* bab = sm;
+  uint64_t* pts = sm + (size_t)(T < kRunChunk ? T : kRunChunk) * COLS;  // see bsgs_run_smem
   constexpr int PAIRS = kRunTile;  // (c, x pair)
   const int p = threadIdx.x % PAIRS, gg = threadIdx.x / PAIRS;
   const int c = p / (kRunTile / 2), xl = (p % (kRunTile / 2)) * 2;
@@ -1113,25 +1094,51 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
     acc[g][0].zero();
     acc[g][1].zero();
   }
+  const size_t pcol = ((size_t)limb * N + x0) >> LR;
   const uint64_t* pt_g = pts + run * kRunGiants + gg * kRunGpt;
   const uint64_t* bab_c = bab + c * kRunTile + xl;
-#pragma unroll 2
-  for (int t = 0; t < T; ++t) {
-    const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(bab_c + (size_t)t * COLS);
-    const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(pt_g + (size_t)t * RT * kRunGiants);
-#pragma unroll
-    for (int h = 0; h < kRunGpt / 2; ++h) {
-      const ulonglong2 pv = pp[h];
-      acc[2 * h][0].add(bv.x, pv.x);
-      acc[2 * h][1].add(bv.y, pv.x);
-      acc[2 * h + 1][0].add(bv.x, pv.y);
-      acc[2 * h + 1][1].add(bv.y, pv.y);
+  int since = 0;
+#pragma unroll 1
+  for (int tc = 0; tc < T; tc += kRunChunk) {
+    const int nt = T - tc < kRunChunk ? T - tc : kRunChunk;
+    if (tc) __syncthreads();  // previous chunk consumed
+    for (int e = threadIdx.x; e < nt * COLS / 2; e += blockDim.x) {
+      const int t = e / (COLS / 2), rem = e - t * (COLS / 2);
+      const int cc = rem / (kRunTile / 2), xx = (rem - cc * (kRunTile / 2)) * 2;
+      cp_async16(bab + (size_t)t * COLS + cc * kRunTile + xx,
+                 P.baby[tc + t] + cc * P.c1_off + (size_t)limb * N + x0 + xx);
     }
-    if ((t + 1) % fold_every == 0) {
+    for (int e = threadIdx.x; e < kRunGiants * nt; e += blockDim.x) {
+      const int g = e / nt, t = e - g * nt;
+      const int idx =
+          g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + tc + t) : -1;
+      uint64_t* d = pts + (size_t)t * RT * kRunGiants + g;
+      const uint64_t* srcp = P.pt_base + (size_t)(idx < 0 ? 0 : idx) * P.pt_stride + pcol;
 #pragma unroll
-      for (int g = 0; g < kRunGpt; ++g) {
-        acc[g][0].fold(pc.q, pc.bar);
-        acc[g][1].fold(pc.q, pc.bar);
+      for (int r = 0; r < RT; ++r) d[r * kRunGiants] = idx < 0 ? 0 : __ldg(srcp + r);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 2
+    for (int t = 0; t < nt; ++t) {
+      const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(bab_c + (size_t)t * COLS);
+      const ulonglong2* pp =
+          reinterpret_cast<const ulonglong2*>(pt_g + (size_t)t * RT * kRunGiants);
+#pragma unroll
+      for (int h = 0; h < kRunGpt / 2; ++h) {
+        const ulonglong2 pv = pp[h];
+        acc[2 * h][0].add(bv.x, pv.x);
+        acc[2 * h][1].add(bv.y, pv.x);
+        acc[2 * h + 1][0].add(bv.x, pv.y);
+        acc[2 * h + 1][1].add(bv.y, pv.y);
+      }
+      if (++since == fold_every) {
+        since = 0;
+#pragma unroll
+        for (int g = 0; g < kRunGpt; ++g) {
+          acc[g][0].fold(pc.q, pc.bar);
+          acc[g][1].fold(pc.q, pc.bar);
+        }
       }
     }
   }
@@ -1145,15 +1152,14 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
                                    (size_t)limb * N + x0 + xl) = make_ulonglong2(r0, r1);
   }
 }
-
 template <int RT, int GPT>
 static void launch_bsgs_run_g(const BsgsParams& P, int k, cudaStream_t st) {
-  const size_t smem = bsgs_run_smem(P.n_terms);
+  const size_t smem = bsgs_run_smem(P.n_terms, RT);
   static bool attr_set = false;
   if (!attr_set) {
     check_cuda(cudaFuncSetAttribute(k_bsgs_run<RT, GPT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)bsgs_run_smem(kBsgsMaxTerms)),
+                                    (int)bsgs_run_smem(kBsgsMaxTerms, RT)),
                "bsgs smem attr");
     attr_set = true;
   }
@@ -1181,7 +1187,7 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
                  uint64_t* out, int64_t out_gstride, int k, cudaStream_t st, int kq,
                  int n_chain) {
-  if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..64 terms"};
+  if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..128 terms"};
   if (pt_log_run < 0 || pt_log_run > 5 || pt_log_run >= log_n)
     throw HegpuError{HEGPU_E_ARG, "bsgs: pt_log_run must be in [0, 5]"};
   if ((1 << log_n) % kBsgsTile) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};
@@ -1211,7 +1217,7 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                    el * 8.0 * ((double)P.n_giants * n_terms / (1 << pt_log_run) +
                                2.0 * nb * (n_terms + P.n_giants)),
                    el * 2.0 * nb * ((double)P.n_giants * n_terms + P.n_giants));
-      if (pt_log_run >= 4 && (1 << log_n) % kRunTile == 0) {
+      if (pt_log_run >= 3 && (1 << log_n) % kRunTile == 0) {
         // one batch element per launch: 16 accumulators per thread at 3 CTAs/SM
         // (the compressed diagonals are re-read per element, 1/16 of a baby)
         for (int bi = 0; bi < nb; ++bi) {
@@ -1219,7 +1225,9 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
           for (int t = 0; t < n_terms; ++t) Q.baby[t] = P.baby[t] + bi * bstride;
           Q.out = P.out + bi * bstride;
           Q.n_batch = 1;
-          if (pt_log_run == 4)
+          if (pt_log_run == 3)
+            launch_bsgs_run<4>(Q, k, st);
+          else if (pt_log_run == 4)
             launch_bsgs_run<2>(Q, k, st);
           else
             launch_bsgs_run<1>(Q, k, st);

@@ -131,3 +131,24 @@ def test_hoisted_rotations_decrypt_like_rotate(boot):
     batch = ops.stack([ct, ckks.encrypt_vector(params, -v, keys, rng_seed=4)])
     hb = ops.rotate_hoisted(batch, [1, 2], keys)
     assert np.max(np.abs(ckks.decrypt_vector(hb[1][1], keys) - np.roll(-v, -2))) < 1e-3
+
+
+def test_packed_pair_refresh(boot):
+    """Two periodic ciphertexts refreshed by ONE bootstrap of twice the period
+    (BootstrapRefresher.refresh_many): each output decrypts like its own
+    bootstrap, at the same level and the default scale."""
+    params, ctx0, _, _ = boot
+    ctx = bs.build_context(params, n_slots=64, input_periodic=True)
+    keys = ckks.keygen(params, rotation_steps=bs.refresh_rotation_steps(ctx), rng_seed=11)
+    rng = np.random.default_rng(17)
+    va, vb = rng.uniform(-1, 1, 64), rng.uniform(-1, 1, 64)
+    reps = params.slot_count // 64
+    a = ckks.encrypt(ckks.encode(params, np.tile(va, reps), 2, scale=params.default_scale * 1.02),
+                     keys)
+    b = ckks.encrypt(ckks.encode(params, np.tile(vb, reps), 2), keys)
+    ref = bs.BootstrapRefresher(ctx, keys)
+    assert bs._pair_packable([a, b], ctx, keys)
+    ra, rb = ref.refresh_many([a, b])
+    for r, v in ((ra, va), (rb, vb)):
+        assert r.level == ctx.output_level and r.scale == params.default_scale
+        assert np.max(np.abs(ckks.decrypt_vector(r, keys) - np.tile(v, reps))) < 1e-2

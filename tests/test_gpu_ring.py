@@ -132,8 +132,8 @@ def test_batched_ops_equal_single():
         assert np.array_equal(coeff.limbs[i], ring.to_coeff(x).limbs)
 
 
-@pytest.mark.parametrize("lr,ns", [(2, 0), (4, 0), (5, 0), (4, 2)])
-def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns):
+@pytest.mark.parametrize("lr,ns,T", [(2, 0, 21), (3, 0, 100), (4, 0, 21), (5, 0, 21), (4, 2, 21)])
+def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T):
     """hegpu_bsgs on run-compressed diagonals (pt_log_run, the sparse-bootstrap
     cache layout; lr >= 4 takes the shared-memory GEMM kernel) equals the dense
     kernel on the expanded diagonals and the exact sum mod q."""
@@ -144,7 +144,7 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns):
     from paper_2210_02574_b200 import _dev, _lib, ckks
 
     params = ckks.get_preset("desk")
-    n, k, T, G, nb = params.ring_degree, 3 + ns, 21, 5, 2
+    n, k, G, nb = params.ring_degree, 3 + ns, 5, 2
     # ns > 0: the last ns limbs are special primes (extended-basis babies)
     qs = ([int(q) for q in params.ring.moduli_chain[:k - ns]]
           + [int(q) for q in params.ring.special_moduli[:ns]])
