@@ -696,8 +696,12 @@ __device__ __forceinline__ uint32_t auto_src(uint32_t i, uint32_t g, int log_n) 
   return __brev((e - 1u) >> 1) >> (32 - log_n);
 }
 
-// One coefficient per thread, BG batch elements per CTA (grid.z groups).
-template <int BG>
+// One coefficient per thread, BG batch elements per CTA (grid.z groups),
+// BETA = compile-time bound on the digit count.  Per rotation all digits'
+// key words and gathered digit words are loaded first (2*BETA + BG*BETA
+// independent loads in flight), then multiplied: the kernel is bound by
+// load latency, not arithmetic.
+template <int BG, int BETA>
 __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant__ IpRotParams P) {
   const int N = 1 << P.log_n;
   const int r = blockIdx.y;
@@ -708,44 +712,60 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant_
   const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
   const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
   const PrimeConst pc = P.pc[prime];
+  // digit j's source row (own rows come from d, the others from ext)
+  const uint64_t* base[BETA];
+  int64_t bstr[BETA], rstr[BETA];
+#pragma unroll
+  for (int j = 0; j < BETA; ++j) {
+    const int g0 = j * P.alpha;
+    const int g1 = min(g0 + P.alpha, P.level + 1);
+    if (r >= g0 && r < g1) {
+      base[j] = P.d + (size_t)r * N + (size_t)b0 * P.ds;
+      bstr[j] = P.ds;
+      rstr[j] = P.d_sr;
+    } else {
+      base[j] = P.ext + j * P.ext_sj + (size_t)(r < g0 ? r : r - (g1 - g0)) * N +
+                (size_t)b0 * P.ext_sb;
+      bstr[j] = P.ext_sb;
+      rstr[j] = P.ext_sr;
+    }
+  }
+  const size_t koff = (size_t)krow * N + x;
   Mac128 ab[BG], aa[BG];
-  int since = 0;
 #pragma unroll
   for (int b = 0; b < BG; ++b) {
     ab[b].zero();
     aa[b].zero();
   }
+  int since = 0;
   for (int rot = 0; rot < P.n_rot; ++rot) {
     const uint32_t src = auto_src((uint32_t)x, P.gal[rot], P.log_n);
-    for (int j = 0; j < P.beta; ++j) {
-      const uint64_t kb = __ldg(P.kb[rot][j] + (size_t)krow * N + x);
-      const uint64_t ka = __ldg(P.ka[rot][j] + (size_t)krow * N + x);
-      const int g0 = j * P.alpha;
-      const int g1 = min(g0 + P.alpha, P.level + 1);
-      const uint64_t* base;
-      int64_t bstr;
-      if (r >= g0 && r < g1) {
-        base = P.d + rot * P.d_sr + (size_t)r * N + src;
-        bstr = P.ds;
-      } else {
-        base = P.ext + rot * P.ext_sr + j * P.ext_sj +
-               (size_t)(r < g0 ? r : r - (g1 - g0)) * N + src;
-        bstr = P.ext_sb;
-      }
+    uint64_t kb[BETA], ka[BETA], v[BETA][BG];
 #pragma unroll
-      for (int b = 0; b < BG; ++b) {
-        if (b < nb) {
-          const uint64_t v = __ldg(base + (size_t)(b0 + b) * bstr);
-          ab[b].add(v, kb);
-          aa[b].add(v, ka);
-        }
+    for (int j = 0; j < BETA; ++j) {
+      if (j < P.beta) {
+        kb[j] = __ldg(P.kb[rot][j] + koff);
+        ka[j] = __ldg(P.ka[rot][j] + koff);
+        const uint64_t* bp = base[j] + rot * rstr[j] + src;
+#pragma unroll
+        for (int b = 0; b < BG; ++b) v[j][b] = b < nb ? __ldg(bp + (size_t)b * bstr[j]) : 0;
       }
-      if (++since == kMacFold) {
-        since = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      if (j < P.beta) {
 #pragma unroll
         for (int b = 0; b < BG; ++b) {
-          ab[b].fold(pc.q, pc.bar);
-          aa[b].fold(pc.q, pc.bar);
+          ab[b].add(v[j][b], kb[j]);
+          aa[b].add(v[j][b], ka[j]);
+        }
+        if (++since == kMacFold) {
+          since = 0;
+#pragma unroll
+          for (int b = 0; b < BG; ++b) {
+            ab[b].fold(pc.q, pc.bar);
+            aa[b].fold(pc.q, pc.bar);
+          }
         }
       }
     }
@@ -776,17 +796,32 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant_
   }
 }
 
+template <int BG>
+static void launch_ip_rot_bg(IpRotParams& P, dim3 grid, cudaStream_t st) {
+  if (P.beta <= 2)
+    k_ks_ip_rot<BG, 2><<<grid, kEwThreads, 0, st>>>(P);
+  else if (P.beta <= 4)
+    k_ks_ip_rot<BG, 4><<<grid, kEwThreads, 0, st>>>(P);
+  else
+    k_ks_ip_rot<BG, kMaxRotDigits><<<grid, kEwThreads, 0, st>>>(P);
+}
+
 void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
   if (P.beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
   if (P.n_rot < 1 || P.n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
-  constexpr int BG = 4;
-  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext, (P.n_batch + BG - 1) / BG);
+  const int bg = P.n_batch >= 4 ? 4 : P.n_batch >= 2 ? 2 : 1;
+  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext, (P.n_batch + bg - 1) / bg);
   const double ipn = (double)(1 << P.log_n) * P.n_ext;
   ProfScope ps(PROF_KS_IP, st,
                ipn * 8.0 * P.n_rot * (2.0 * P.beta + P.n_batch * P.beta) +
                    ipn * 8.0 * 2.0 * P.n_batch * (P.sum_mode ? 1 : P.n_rot),
                ipn * P.n_batch * P.n_rot * 2.0 * P.beta);
-  k_ks_ip_rot<BG><<<grid, kEwThreads, 0, st>>>(P);
+  if (bg == 4)
+    launch_ip_rot_bg<4>(P, grid, st);
+  else if (bg == 2)
+    launch_ip_rot_bg<2>(P, grid, st);
+  else
+    launch_ip_rot_bg<1>(P, grid, st);
   check_cuda(cudaGetLastError(), "ks rotation inner product launch");
 }
 
