@@ -580,7 +580,12 @@ def run_ours(args):
 
     prof_step = wl.profile_step if hasattr(wl, "profile_step") else wl.step
     _lib.profile_enable(True)
+    if os.environ.get("BENCH_NVTX"):  # lets ncu --nvtx-include "profile_step/" target one step
+        torch.cuda.nvtx.range_push("profile_step")
     prof_step()
+    if os.environ.get("BENCH_NVTX"):
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     # the reference op histogram in a separate pass: recording it may run the

@@ -77,10 +77,6 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
  * precompute (ring.py:81-177).  Primes must be < 2^62, = 1 mod 2N. */
 int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain,
                       const uint64_t* special, int n_special, hegpu_ring_t* out);
-/* Keep the ring's twiddle tables (n_primes * 4N words) resident in a
- * persisting L2 carve-out for kernels launched on `stream`. */
-int hegpu_l2_persist_twiddles(hegpu_ring_t ring, void* stream, double hit_ratio);
-
 int hegpu_ring_destroy(hegpu_ring_t ring);
 /* Copy the device twiddle tables of global prime p to host: 4N words,
  * interleaved (psi_rev[i], shoup(psi_rev[i])) pairs for i < N, then

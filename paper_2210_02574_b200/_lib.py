@@ -42,7 +42,6 @@ SIGNATURES = {
     "hegpu_automorphism": [_P, _I, _U64, _P, _I64, _P, _I64, _I, _I, _P, _P],
     "hegpu_tensor": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_apply": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _P, _I64, _I, _P],
-    "hegpu_l2_persist_twiddles": [_P, _P, ctypes.c_double],
     "hegpu_tensor_periodic": [_P, _P, _P, _I64, _I, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_rotsum": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _I64, _I64, _P],
     "hegpu_ks_apply_rescale": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _I64, _I64, _P, _I64,

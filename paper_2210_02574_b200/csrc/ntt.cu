@@ -255,6 +255,9 @@ constexpr int kRegMinBlocks = 8 / kRegWarps;  // scales the launch bounds below
 #define HEGPU_NTT_PPB 4
 #endif
 constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
+// conversion prologue: up to this many source limbs take the unrolled path
+// (all source words of a coefficient in flight at once)
+constexpr int kConvMaxSrc = 8;
 
 // Shared memory of the register passes (bytes): the cols pass holds its
 // S x 8 tile, the warp buffers and the S twiddle pairs of stages [0, LOGS);
@@ -263,7 +266,7 @@ constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
 template <int LOGS>
 constexpr size_t cols_r_smem() {
   return ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8 +
-         (size_t)(1 << LOGS) * 16;
+         (size_t)(1 << LOGS) * 16 + kConvMaxSrc * 3 * 8;
 }
 template <int LOGS>
 constexpr size_t blocks_r_smem() {
@@ -291,6 +294,17 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinB
   ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + S * TS + kRegWarps * Sh::PAD_S);
   // every column transform of this pass uses twiddles [1, S) of its table
   for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tw + i);
+  // conversion constants of this target limb: punc[i], fp32 weight, shift
+  uint64_t* s_conv = reinterpret_cast<uint64_t*>(stw + S);
+  const int nsrc = (!INV && sg.csrc != nullptr && sg.cmode != 1) ? sg.c_nsrc : 0;
+  for (int i = threadIdx.x; i < nsrc && i < kConvMaxSrc; i += blockDim.x) {
+    s_conv[i] = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
+    if (sg.cmode == 2) {
+      s_conv[kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfw) + i);
+      s_conv[2 * kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfs) + i);
+    }
+  }
+  __syncthreads();
   const int c0 = blockIdx.x * kRegWarps;
   const bool centered = sg.cmode == 2;
   const uint64_t negd = (!INV && centered) ? __ldg(sg.cnegd + limb) : 0;
@@ -316,6 +330,37 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinB
       // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
       const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
       const uint64_t q = pc.q;
+      if (nsrc <= kConvMaxSrc) {
+        // unrolled: the nsrc source words of each coefficient load together
+#pragma unroll 2
+        for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+          const int r = e / kRegWarps, c = e % kRegWarps;
+          const size_t x = c0 + c + (size_t)C * r;
+          uint64_t h[kConvMaxSrc];
+#pragma unroll
+          for (int i = 0; i < kConvMaxSrc; ++i) h[i] = i < nsrc ? __ldg(hs + (size_t)i * N + x) : 0;
+          Mac128 acc;
+          acc.zero();
+          float f = 0.f;
+#pragma unroll
+          for (int i = 0; i < kConvMaxSrc; ++i) {
+            if (i < nsrc) {
+              acc.add(h[i], s_conv[i]);
+              if (centered) {
+                const uint64_t wbits = s_conv[kConvMaxSrc + i];
+                const int sh = (int)s_conv[2 * kConvMaxSrc + i];
+                f = fmaf(__uint2float_rn(static_cast<uint32_t>(h[i] >> sh)),
+                         __uint_as_float(static_cast<uint32_t>(wbits)), f);
+              }
+            }
+          }
+          if (centered) {
+            if (nsrc == kConvMaxSrc) acc.fold(q, pc.bar);
+            acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
+          }
+          tile[r * TS + c] = acc.redc(pc);
+        }
+      } else
       for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
         const int r = e / kRegWarps, c = e % kRegWarps;
         const size_t x = c0 + c + (size_t)C * r;

@@ -61,11 +61,7 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
       uint64_t u = x[e];
       u = u >= q2 ? u - q2 : u;
       const ulonglong2 wp = tw[ti];
-#ifdef HEGPU_EXP_NOMUL
-      const uint64_t v = x[e + d] ^ wp.x;
-#else
       const uint64_t v = shoup_lazy(x[e + d], wp.x, wp.y, q);
-#endif
       x[e] = u + v;
       x[e + d] = u - v + q2;
     }

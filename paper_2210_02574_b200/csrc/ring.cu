@@ -1512,27 +1512,6 @@ int hegpu_profile_read(double* ms, long long* counts, double* bytes, double* mod
   })
 }
 
-int hegpu_l2_persist_twiddles(hegpu_ring_t ring, void* stream, double hit_ratio) {
-  HEGPU_TRY({
-    Ring& R = RR(ring);
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "get device");
-    cudaDeviceProp prop;
-    check_cuda(cudaGetDeviceProperties(&prop, dev), "device props");
-    const size_t bytes = (size_t)R.n_primes * 4 * R.n * 8;
-    const size_t carve = std::min<size_t>(bytes, prop.persistingL2CacheMaxSize);
-    check_cuda(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve), "persisting L2 limit");
-    cudaStreamAttrValue attr = {};
-    attr.accessPolicyWindow.base_ptr = R.dtw;
-    attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, prop.accessPolicyMaxWindowSize);
-    attr.accessPolicyWindow.hitRatio = (float)hit_ratio;
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    check_cuda(cudaStreamSetAttribute(S_(stream), cudaStreamAttributeAccessPolicyWindow, &attr),
-               "access policy window");
-  })
-}
-
 int hegpu_ring_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
                       int n_special, hegpu_ring_t* out) {
   HEGPU_TRY({

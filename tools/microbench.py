@@ -74,9 +74,6 @@ def bench_bsgs(params):
 
 def main():
     params = ckks.get_preset("p16")
-    if os.environ.get("PERSIST"):
-        _lib.call("hegpu_l2_persist_twiddles", params.ring.device(), _dev.stream(),
-                  float(os.environ["PERSIST"]))
     which = sys.argv[1:] or ["ntt", "bsgs"]
     if "ntt" in which:
         bench_ntt(params)
