@@ -258,6 +258,9 @@ constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
 // conversion prologue: up to this many source limbs take the unrolled path
 // (all source words of a coefficient in flight at once)
 constexpr int kConvMaxSrc = 8;
+#ifndef HEGPU_COLS_MINB
+#define HEGPU_COLS_MINB 5
+#endif
 
 // Shared memory of the register passes (bytes): the cols pass holds its
 // S x 8 tile, the warp buffers and the S twiddle pairs of stages [0, LOGS);
@@ -273,8 +276,13 @@ constexpr size_t blocks_r_smem() {
   return (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8 + (size_t)kRegWarps * (1 << LOGS) * 16;
 }
 
-template <int LOGS, bool INV>
-__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinBlocks) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+// CM: first-pass input -- 0 plain load, 1 centered lift of one limb
+// (rescale / ModRaise), 2 fast basis conversion, 3 conversion of the centered
+// representative (ModDown by q_l * P).  Compile-time so each variant carries
+// only its own prologue.
+template <int LOGS, bool INV, int CM>
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MINB) * kRegMinBlocks) k_ntt_cols_r(const __grid_constant__ NttParams P) {
+  static_assert(!INV || CM == 0, "prologues are forward-only");
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   constexpr int TS = kRegWarps + 1;  // padded tile row (conflict-free column reads)
@@ -296,18 +304,18 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinB
   for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tw + i);
   // conversion constants of this target limb: punc[i], fp32 weight, shift
   uint64_t* s_conv = reinterpret_cast<uint64_t*>(stw + S);
-  const int nsrc = (!INV && sg.csrc != nullptr && sg.cmode != 1) ? sg.c_nsrc : 0;
+  const int nsrc = CM >= 2 ? sg.c_nsrc : 0;
   for (int i = threadIdx.x; i < nsrc && i < kConvMaxSrc; i += blockDim.x) {
     s_conv[i] = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
-    if (sg.cmode == 2) {
+    if (CM == 3) {
       s_conv[kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfw) + i);
       s_conv[2 * kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfs) + i);
     }
   }
   __syncthreads();
   const int c0 = blockIdx.x * kRegWarps;
-  const bool centered = sg.cmode == 2;
-  const uint64_t negd = (!INV && centered) ? __ldg(sg.cnegd + limb) : 0;
+  constexpr bool centered = CM == 3;
+  const uint64_t negd = centered ? __ldg(sg.cnegd + limb) : 0;
   const ulonglong2 fs = P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh);
   const ulonglong2 fd = P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh);
 #pragma unroll 1
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinB
     const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
                               : (sg.in + poly * sg.in_stride + (size_t)limb * N);
     uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
-    if (!INV && sg.csrc != nullptr && sg.cmode == 1) {
+    if constexpr (CM == 1) {
       // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
       const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
       const uint64_t qs = sg.csrc_q;
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 5) * kRegMinB
         const int64_t v = u > (qs >> 1) ? (int64_t)u - (int64_t)qs : (int64_t)u;
         tile[r * TS + c] = signed_mod(v, pc);
       }
-    } else if (!INV && sg.csrc != nullptr) {
+    } else if constexpr (CM >= 2) {
       // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
       const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
       const uint64_t q = pc.q;
@@ -491,26 +499,46 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinB
   }
 }
 
+template <int LOGS, bool INV, int CM>
+static void launch_cols_r_cm(const NttParams& P, dim3 grid, cudaStream_t st) {
+  const size_t smem = cols_r_smem<LOGS>();
+  static bool attr_set = false;  // opt in to > 48 KiB dynamic shared memory once
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, INV, CM>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    attr_set = true;
+  }
+  k_ntt_cols_r<LOGS, INV, CM><<<grid, 32 * kRegWarps, smem, st>>>(P);
+}
+
+// the first-pass prologue every segment of the launch shares
+static int cols_mode(const NttParams& P) {
+  int cm = -1;
+  for (int g = 0; g < P.S.n_seg; ++g) {
+    const Seg& sg = P.S.seg[g];
+    const int m = sg.csrc == nullptr ? 0 : sg.cmode == 1 ? 1 : sg.cmode == 2 ? 3 : 2;
+    if (cm >= 0 && m != cm) throw HegpuError{HEGPU_E_ARG, "NTT segments mix prologue modes"};
+    cm = m;
+  }
+  return cm < 0 ? 0 : cm;
+}
+
 template <int LOGS>
 static void launch_cols_r(bool inverse, const NttParams& P, int n_units, int log_n,
                           cudaStream_t st) {
   const int C = (1 << log_n) >> LOGS;
   dim3 grid(C / kRegWarps, n_units);
-  const size_t smem = cols_r_smem<LOGS>();
-  static bool attr_set = false;  // opt in to > 48 KiB dynamic shared memory once
-  if (!attr_set) {
-    check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "smem attr");
-    check_cuda(cudaFuncSetAttribute(k_ntt_cols_r<LOGS, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "smem attr");
-    attr_set = true;
+  if (inverse) {
+    launch_cols_r_cm<LOGS, true, 0>(P, grid, st);
+    return;
   }
-  if (inverse)
-    k_ntt_cols_r<LOGS, true><<<grid, 32 * kRegWarps, smem, st>>>(P);
-  else
-    k_ntt_cols_r<LOGS, false><<<grid, 32 * kRegWarps, smem, st>>>(P);
+  switch (cols_mode(P)) {
+    case 1: launch_cols_r_cm<LOGS, false, 1>(P, grid, st); break;
+    case 2: launch_cols_r_cm<LOGS, false, 2>(P, grid, st); break;
+    case 3: launch_cols_r_cm<LOGS, false, 3>(P, grid, st); break;
+    default: launch_cols_r_cm<LOGS, false, 0>(P, grid, st); break;
+  }
 }
 
 template <int LOGS>
