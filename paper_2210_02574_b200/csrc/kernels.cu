@@ -1092,11 +1092,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_bsgs(const __grid_constant__ 
 // stored [term][run][giant]) per term.
 constexpr int kRunTile = 32;   // coefficients per CTA
 constexpr int kRunGiants = 32; // giants per CTA (grid.z covers more)
-constexpr int kRunChunk = 64;  // terms staged in shared memory at a time
+#ifndef HEGPU_RUN_CHUNK
+#define HEGPU_RUN_CHUNK 32
+#endif
+#ifndef HEGPU_RUN_GPT
+#define HEGPU_RUN_GPT 4
+#endif
+constexpr int kRunChunk = HEGPU_RUN_CHUNK;  // terms per shared-memory stage (double-buffered)
 
 constexpr size_t bsgs_run_smem(int n_terms, int rt) {
-  return (size_t)(n_terms < kRunChunk ? n_terms : kRunChunk) * (2 * kRunTile + kRunGiants * rt) *
-         8;
+  (void)n_terms;
+  return (size_t)2 * kRunChunk * (2 * kRunTile + kRunGiants * rt) * 8;  // two stage buffers
 }
 
 // RT = runs per tile (2 for pt_log_run 4, 1 for 5); one batch element per CTA.
@@ -1107,15 +1113,16 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
   extern __shared__ __align__(16) uint64_t sm[];
   constexpr int COLS = 2 * kRunTile;  // (c0, c1) x 32 coefficients
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
+  constexpr int BUF = kRunChunk * (COLS + kRunGiants * RT);  // words per stage buffer
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
   const int x0 = blockIdx.x * kRunTile;
   const int g0 = blockIdx.z * kRunGiants;
   const int T = P.n_terms;
-  // terms are staged kRunChunk at a time (babies [t][2][32], diagonals
-  // [t][RT][32 giants]); the accumulators carry over between chunks
-  uint64_t* bab = sm;
-  uint64_t* pts = sm + (size_t)(T < kRunChunk ? T : kRunChunk) * COLS;  // see bsgs_run_smem
+  const int nch = (T + kRunChunk - 1) / kRunChunk;
+  // terms are staged kRunChunk at a time into one of two buffers (babies
+  // [t][2][32], diagonals [t][RT][32 giants]), all by cp.async: chunk c + 1
+  // loads while chunk c is multiplied; accumulators carry across chunks
   constexpr int PAIRS = kRunTile;  // (c, x pair)
   const int p = threadIdx.x % PAIRS, gg = threadIdx.x / PAIRS;
   const int c = p / (kRunTile / 2), xl = (p % (kRunTile / 2)) * 2;
@@ -1130,13 +1137,11 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
     acc[g][1].zero();
   }
   const size_t pcol = ((size_t)limb * N + x0) >> LR;
-  const uint64_t* pt_g = pts + run * kRunGiants + gg * kRunGpt;
-  const uint64_t* bab_c = bab + c * kRunTile + xl;
-  int since = 0;
-#pragma unroll 1
-  for (int tc = 0; tc < T; tc += kRunChunk) {
+  auto stage = [&](int ch) {
+    uint64_t* bab = sm + (size_t)(ch & 1) * BUF;
+    uint64_t* pts = bab + (size_t)kRunChunk * COLS;
+    const int tc = ch * kRunChunk;
     const int nt = T - tc < kRunChunk ? T - tc : kRunChunk;
-    if (tc) __syncthreads();  // previous chunk consumed
     for (int e = threadIdx.x; e < nt * COLS / 2; e += blockDim.x) {
       const int t = e / (COLS / 2), rem = e - t * (COLS / 2);
       const int cc = rem / (kRunTile / 2), xx = (rem - cc * (kRunTile / 2)) * 2;
@@ -1150,10 +1155,31 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
       uint64_t* d = pts + (size_t)t * RT * kRunGiants + g;
       const uint64_t* srcp = P.pt_base + (size_t)(idx < 0 ? 0 : idx) * P.pt_stride + pcol;
 #pragma unroll
-      for (int r = 0; r < RT; ++r) d[r * kRunGiants] = idx < 0 ? 0 : __ldg(srcp + r);
+      for (int r = 0; r < RT; ++r) {
+        if (idx < 0)
+          d[r * kRunGiants] = 0;
+        else
+          cp_async8(d + r * kRunGiants, srcp + r);
+      }
     }
-    cp_async_wait_all();
+    cp_async_commit();
+  };
+  stage(0);
+  int since = 0;
+#pragma unroll 1
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage(ch + 1);
+      cp_async_wait_group<1>();  // chunk ch has landed, ch + 1 in flight
+    } else {
+      cp_async_wait_group<0>();
+    }
     __syncthreads();
+    const uint64_t* bab = sm + (size_t)(ch & 1) * BUF;
+    const uint64_t* pts = bab + (size_t)kRunChunk * COLS;
+    const uint64_t* pt_g = pts + run * kRunGiants + gg * kRunGpt;
+    const uint64_t* bab_c = bab + c * kRunTile + xl;
+    const int nt = T - ch * kRunChunk < kRunChunk ? T - ch * kRunChunk : kRunChunk;
 #pragma unroll 2
     for (int t = 0; t < nt; ++t) {
       const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(bab_c + (size_t)t * COLS);
@@ -1176,6 +1202,7 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
         }
       }
     }
+    __syncthreads();  // buffer ch & 1 is restaged for chunk ch + 2
   }
 #pragma unroll
   for (int g = 0; g < kRunGpt; ++g) {
@@ -1207,7 +1234,7 @@ static void launch_bsgs_run_g(const BsgsParams& P, int k, cudaStream_t st) {
 // the CtS shape; the register-only ceiling of Mac128 is 2.16 T/s.
 template <int RT>
 static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
-  launch_bsgs_run_g<RT, 4>(P, k, st);
+  launch_bsgs_run_g<RT, HEGPU_RUN_GPT>(P, k, st);
 }
 
 template <int NB>

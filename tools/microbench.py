@@ -65,7 +65,7 @@ def bench_bsgs(params):
             pts = rand_limbs(params, (2048, k, n >> lr), k)
             f = lambda: _lib.call("hegpu_bsgs", ring, ptrs, n_terms, k * n, 2 * k * n, nb,
                                   pts.data_ptr(), k * (n >> lr), lr, idx.data_ptr(), n_giants,
-                                  out.data_ptr(), nb * 2 * k * n, k, _dev.stream())
+                                  out.data_ptr(), nb * 2 * k * n, k, 0, _dev.stream())
             us = timeit(f, iters=5, warm=1)
             macs = n_giants * n_terms * nb * 2 * k * n
             print(f"bsgs nb={nb} lr={lr} k={k}: {us:9.1f} us  {macs / us / 1e6:6.3f} T mac/s")
