@@ -44,7 +44,7 @@ for it in range(3):
           f"refresh {t4.elapsed_time(t5):.1f} ms")
 for name, fn in (("gradient", lambda: logreg._batched_gradient(xb, yb, wl.w, layout, keys, sig,
                                                                 cfg.learning_rate, wl.batch_rows)),
-                 ("refresh", lambda: wl.refresher.refresh_many([wl.w, wl.u]))):
+                 ("refresh", lambda: wl.refresher.refresh_many([w2, u2]))):
     _lib.profile_enable(True)
     fn()
     prof = _lib.profile_read()
