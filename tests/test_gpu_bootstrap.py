@@ -152,3 +152,24 @@ def test_packed_pair_refresh(boot):
     for r, v in ((ra, va), (rb, vb)):
         assert r.level == ctx.output_level and r.scale == params.default_scale
         assert np.max(np.abs(ckks.decrypt_vector(r, keys) - np.tile(v, reps))) < 1e-2
+
+
+def test_captured_bootstrap_replays(boot):
+    """CapturedBootstrap (CUDA graph of one bootstrap) gives the same output
+    as the eager call on the same input and accepts new inputs of the same
+    shape (ciphertext or packed host tensor)."""
+    params, ctx, keys, _ = boot
+    rng = np.random.default_rng(23)
+    v1, v2 = rng.uniform(-1, 1, 64), rng.uniform(-1, 1, 64)
+    c1 = ckks.encrypt_vector(params, v1, keys, level=0, rng_seed=31)
+    c2 = ckks.encrypt_vector(params, v2, keys, level=0, rng_seed=32)
+    cap = bs.CapturedBootstrap(c1, ctx, keys)
+    out = cap.run(c1)
+    eager = bs.bootstrap(c1, ctx, keys)
+    assert np.array_equal(out.c0.limbs, eager.c0.limbs)
+    assert np.array_equal(out.c1.limbs, eager.c1.limbs)
+    import torch
+
+    host = torch.stack([c2.c0.data, c2.c1.data]).cpu()
+    out2 = cap.run(host.to("cuda"))
+    assert np.max(np.abs(ckks.decrypt_vector(out2, keys)[:64] - v2)) < 1e-2
