@@ -1100,20 +1100,20 @@ constexpr int kRunGiants = 32; // giants per CTA (grid.z covers more)
 #endif
 constexpr int kRunChunk = HEGPU_RUN_CHUNK;  // terms per shared-memory stage (double-buffered)
 
-constexpr size_t bsgs_run_smem(int n_terms, int rt) {
-  (void)n_terms;
-  return (size_t)2 * kRunChunk * (2 * kRunTile + kRunGiants * rt) * 8;  // two stage buffers
+constexpr size_t bsgs_run_smem(int ng, int rt) {
+  return (size_t)2 * kRunChunk * (2 * kRunTile + ng * rt) * 8;  // two stage buffers
 }
 
 // RT = runs per tile (2 for pt_log_run 4, 1 for 5); one batch element per CTA.
-template <int RT, int GPT>
-__global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
+template <int RT, int GPT, int NG>
+__global__ void __launch_bounds__(32 * (NG / GPT), GPT == 8 ? 3 : 2)
     k_bsgs_run(const __grid_constant__ BsgsParams P) {
   constexpr int kRunGpt = GPT;
+  constexpr int kRunGiants = NG;  // giants per CTA
   extern __shared__ __align__(16) uint64_t sm[];
   constexpr int COLS = 2 * kRunTile;  // (c0, c1) x 32 coefficients
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
-  constexpr int BUF = kRunChunk * (COLS + kRunGiants * RT);  // words per stage buffer
+  constexpr int BUF = kRunChunk * (COLS + NG * RT);  // words per stage buffer
   const int N = 1 << P.log_n;
   const int limb = blockIdx.y;
   const int x0 = blockIdx.x * kRunTile;
@@ -1214,27 +1214,31 @@ __global__ void __launch_bounds__(32 * (kRunGiants / GPT), GPT == 8 ? 3 : 2)
                                    (size_t)limb * N + x0 + xl) = make_ulonglong2(r0, r1);
   }
 }
-template <int RT, int GPT>
+template <int RT, int GPT, int NG>
 static void launch_bsgs_run_g(const BsgsParams& P, int k, cudaStream_t st) {
-  const size_t smem = bsgs_run_smem(P.n_terms, RT);
+  const size_t smem = bsgs_run_smem(NG, RT);
   static bool attr_set = false;
   if (!attr_set) {
-    check_cuda(cudaFuncSetAttribute(k_bsgs_run<RT, GPT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)bsgs_run_smem(kBsgsMaxTerms, RT)),
+    check_cuda(cudaFuncSetAttribute(k_bsgs_run<RT, GPT, NG>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "bsgs smem attr");
     attr_set = true;
   }
-  dim3 grid((1 << P.log_n) / kRunTile, k, (P.n_giants + kRunGiants - 1) / kRunGiants);
-  k_bsgs_run<RT, GPT><<<grid, 32 * (kRunGiants / GPT), smem, st>>>(P);
+  dim3 grid((1 << P.log_n) / kRunTile, k, (P.n_giants + NG - 1) / NG);
+  k_bsgs_run<RT, GPT, NG><<<grid, 32 * (NG / GPT), smem, st>>>(P);
 }
 
 // 4 giants x 2 columns per thread (8 accumulators, 256 threads): measured
 // 1.38 T products/s vs 1.19 (8 giants, 128 threads) and 1.00 (2 giants) on
 // the CtS shape; the register-only ceiling of Mac128 is 2.16 T/s.
+// a CTA covers 32 giants, or 16 when the transform has no more (its thread
+// groups would otherwise idle)
 template <int RT>
 static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
-  launch_bsgs_run_g<RT, HEGPU_RUN_GPT>(P, k, st);
+  if (P.n_giants <= 16)
+    launch_bsgs_run_g<RT, HEGPU_RUN_GPT, 16>(P, k, st);
+  else
+    launch_bsgs_run_g<RT, HEGPU_RUN_GPT, kRunGiants>(P, k, st);
 }
 
 template <int NB>
