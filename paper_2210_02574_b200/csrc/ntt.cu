@@ -255,6 +255,12 @@ constexpr int kRegMinBlocks = 8 / kRegWarps;  // scales the launch bounds below
 #define HEGPU_NTT_PPB 4
 #endif
 constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
+// HEGPU_NTT_PAIR=2: the block pass runs two polys of a limb per warp in
+// lockstep (2x ILP); measured no faster (the pipes, not latency, bound it)
+#ifndef HEGPU_NTT_PAIR
+#define HEGPU_NTT_PAIR 1
+#endif
+constexpr int kNttPair = HEGPU_NTT_PAIR;
 // conversion prologue: up to this many source limbs take the unrolled path
 // (all source words of a coefficient in flight at once)
 constexpr int kConvMaxSrc = 8;
@@ -273,7 +279,8 @@ constexpr size_t cols_r_smem() {
 }
 template <int LOGS>
 constexpr size_t blocks_r_smem() {
-  return (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8 + (size_t)kRegWarps * (1 << LOGS) * 16;
+  return (size_t)kNttPair * kRegWarps * RegShape<LOGS>::PAD_S * 8 +
+         (size_t)kRegWarps * (1 << LOGS) * 16;
 }
 
 // CM: first-pass input -- 0 plain load, 1 centered lift of one limb
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 2 ? 3 : 4)) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
@@ -436,7 +443,8 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinB
   const int blk = blockIdx.x * kRegWarps + warp;
   const size_t off = (size_t)limb * N + (size_t)blk * S;
   uint64_t* wbuf = sm + warp * Sh::PAD_S;
-  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kRegWarps * Sh::PAD_S);
+  uint64_t* wbuf2 = sm + (kRegWarps * (kNttPair - 1) + warp) * Sh::PAD_S;  // paired polys
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kNttPair * kRegWarps * Sh::PAD_S);
   constexpr int LO_S = LOGS - EB;
   {
     // stage st of blocks [blk0, blk0 + W) uses global twiddles
@@ -449,21 +457,15 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinB
     }
   }
   const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;
-  uint64_t x[E];
-#pragma unroll 1
-  for (int pi = 0; pi < U.np; ++pi) {
-    const int poly = U.p0 + pi;
+  auto load = [&](uint64_t (&x)[E], int poly) {
     const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + off)
                               : (sg.out + poly * sg.out_stride + off);
-    uint64_t* dst = sg.out + poly * sg.out_stride + off;
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
-    if (pi == 0) {
-      cp_async_wait_all();
-      __syncthreads();
-    }
+  };
+  auto finish = [&](uint64_t (&x)[E], int poly) {
+    uint64_t* dst = sg.out + poly * sg.out_stride + off;
     if (!INV) {
-      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
       if (P.epi) {
         const uint64_t* other = sg.other + poly * sg.other_stride + off;
         uint64_t* eout = sg.eout + poly * sg.eout_stride + off;
@@ -489,12 +491,39 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : 4) * kRegMinB
         }
       }
     } else {
-      // re-based table: log_n' = LOGS + log2(warps) (the last-stage scaling
-      // is never in this pass)
-      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw, pc,
-                    make_ulonglong2(pc.ninv, pc.ninv_sh), make_ulonglong2(pc.ilast, pc.ilast_sh));
 #pragma unroll
       for (int e = 0; e < E; ++e) dst[lane + 32 * e] = x[e];
+    }
+  };
+  // re-based twiddle table for the inverse: log_n' = LOGS + log2(warps) (the
+  // last-stage scaling is never in this pass)
+  const ulonglong2 fs = make_ulonglong2(pc.ninv, pc.ninv_sh);
+  const ulonglong2 fd = make_ulonglong2(pc.ilast, pc.ilast_sh);
+  uint64_t x[E], x2[E];
+#pragma unroll 1
+  for (int pi = 0; pi < U.np; pi += kNttPair) {
+    const bool pair = kNttPair == 2 && pi + 1 < U.np;
+    load(x, U.p0 + pi);
+    if (pair) load(x2, U.p0 + pi + 1);
+    if (pi == 0) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (pair) {
+      // two polys of this limb in lockstep: shared twiddles, 2x ILP
+      if (!INV)
+        fwd_sub2<LOGS>(x, x2, wbuf, wbuf2, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
+      else
+        inv_sub2<LOGS>(x, x2, wbuf, wbuf2, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw,
+                       pc, fs, fd);
+      finish(x, U.p0 + pi);
+      finish(x2, U.p0 + pi + 1);
+    } else {
+      if (!INV)
+        fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
+      else
+        inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw, pc, fs, fd);
+      finish(x, U.p0 + pi);
     }
   }
 }

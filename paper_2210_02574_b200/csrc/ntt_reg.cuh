@@ -162,4 +162,72 @@ __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
   reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
 }
 
+// Two independent sub-transforms in lockstep (the same twiddles: the same
+// limb of two polys): each round runs both register sets back to back so the
+// scheduler interleaves two independent butterfly streams (2x ILP), and the
+// two re-distributions share one pair of __syncwarp.
+template <int LOGS>
+__device__ __forceinline__ void reg_shuffle2(uint64_t (&x0)[RegShape<LOGS>::E],
+                                             uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
+                                             uint64_t* b1, int lane, int lo_from, int lo_to) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  if (lo_from == lo_to) return;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = padi(reg_j(lane, e, lo_from, EB));
+    b0[j] = x0[e];
+    b1[j] = x1[e];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = padi(reg_j(lane, e, lo_to, EB));
+    x0[e] = b0[j];
+    x1[e] = b1[j];
+  }
+  __syncwarp();
+}
+
+template <int LOGS>
+__device__ __forceinline__ void fwd_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
+                                         uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
+                                         uint64_t* b1, int lane, int lo_in, int lo_out, int g0,
+                                         int blk, const ulonglong2* tw, uint64_t q) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int phi = LOGS - 1 - r * EB;
+    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
+    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
+    reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo);
+    cur = lo;
+    fwd_round<LOGS>(x0, lane, lo, phi, plo, g0, blk, tw, q);
+    fwd_round<LOGS>(x1, lane, lo, phi, plo, g0, blk, tw, q);
+  }
+  reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo_out);
+}
+
+template <int LOGS>
+__device__ __forceinline__ void inv_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
+                                         uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
+                                         uint64_t* b1, int lane, int lo_in, int lo_out, int log_n,
+                                         int gshift, int blk, const ulonglong2* tw,
+                                         const PrimeConst& pc, const ulonglong2 fin_s,
+                                         const ulonglong2 fin_d) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int plo = r * EB;
+    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
+    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
+    reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo);
+    cur = lo;
+    inv_round<LOGS>(x0, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
+    inv_round<LOGS>(x1, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
+  }
+  reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo_out);
+}
+
 }  // namespace hegpu
