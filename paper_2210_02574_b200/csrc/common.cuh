@@ -32,7 +32,53 @@ struct PrimeConst {
   uint64_t ninv_sh;
   uint64_t ilast;     // ipsi_rev[1] * N^{-1} mod q (fused last inverse stage)
   uint64_t ilast_sh;
+  // FP64-pipe twiddles (w, w/q) for primes below kFpMaxBits bits, forward
+  // [0, N) then inverse [N, 2N); nullptr: this prime takes the integer path
+  const double2* twf;
+  uint64_t pad_;
 };
+
+// ---------------------------------------------------------------------------
+// FP64 modular arithmetic for primes q < 2^kFpMaxBits (sm_100a runs DFMA at
+// 64 lanes/clk/SM; a modmul below is 6 FP64 ops, ~2.7x the measured rate of
+// the 64-bit integer Shoup product, tools/fpmodpeak.cu).  Residues are
+// integers held exactly in doubles, in signed lazy ranges.
+//   h = a*w, l = fma(a, w, -h)     exact: a*w = h + l
+//   t = rint(a * (w/q))            quotient estimate, |a*w/q - t| < 0.75
+//   r = fma(-t, q, h) + l          exact (|r| < q < 2^53), r in (-q, q)
+// Valid for |a| < 2^51 and w < q; results identical as residues to the
+// integer path, so the transforms stay bit-exact once normalised.
+// ---------------------------------------------------------------------------
+constexpr int kFpMaxBits = 46;
+constexpr double kFpMagic = 6755399441055744.0;  // 1.5 * 2^52: rint by addition
+constexpr long long kFpMagicBits = 0x4338000000000000LL;
+
+__device__ __forceinline__ double fp_mulmod(double a, double w, double wq, double q) {
+  const double h = a * w;
+  const double l = fma(a, w, -h);
+  const double t = fma(a, wq, kFpMagic) - kFpMagic;
+  return fma(-t, q, h) + l;
+}
+// centered reduction: |result| <= q/2 (+1), for |x| < 2^51
+__device__ __forceinline__ double fp_reduce(double x, double q, double qinv) {
+  const double t = fma(x, qinv, kFpMagic) - kFpMagic;
+  return fma(-t, q, x);
+}
+// signed 64-bit integer <-> double, exact for |x| < 2^51
+__device__ __forceinline__ double fp_from_s64(uint64_t x) {
+  return __longlong_as_double(static_cast<long long>(x) + kFpMagicBits) - kFpMagic;
+}
+__device__ __forceinline__ uint64_t fp_to_s64(double x) {
+  return static_cast<uint64_t>(__double_as_longlong(x + kFpMagic) - kFpMagicBits);
+}
+// x in (-q, q) -> residue in [0, q)
+__device__ __forceinline__ uint64_t fp_to_residue_small(double x, double q) {
+  return fp_to_s64(x < 0.0 ? x + q : x);
+}
+// any |x| < 2^51 -> residue in [0, q)
+__device__ __forceinline__ uint64_t fp_to_residue(double x, double q, double qinv) {
+  return fp_to_residue_small(fp_reduce(x, q, qinv), q);
+}
 
 // ---------------------------------------------------------------------------
 // scalar helpers

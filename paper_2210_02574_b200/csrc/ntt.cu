@@ -307,8 +307,12 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
   ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + S * TS + kRegWarps * Sh::PAD_S);
+  // FP64 path for primes below 2^kFpMaxBits: (w, w/q) twiddles, same layout
+  const bool fpp = pc.twf != nullptr;
+  const ulonglong2* tws =
+      fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + (INV ? N : 0)) : tw;
   // every column transform of this pass uses twiddles [1, S) of its table
-  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tw + i);
+  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tws + i);
   // conversion constants of this target limb: punc[i], fp32 weight, shift
   uint64_t* s_conv = reinterpret_cast<uint64_t*>(stw + S);
   const int nsrc = CM >= 2 ? sg.c_nsrc : 0;
@@ -409,7 +413,28 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
     uint64_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
-    if (!INV)
+    if (fpp) {
+      // forward: [0, q) in, signed lazy intermediate out; inverse: the
+      // signed intermediate in, fully reduced out
+      const double qd = (double)pc.q, qinv = 1.0 / qd;
+      double xf[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) xf[e] = fp_from_s64(x[e]);
+      const double2* stwf = reinterpret_cast<const double2*>(stw);
+      double* wbf = reinterpret_cast<double*>(wbuf);
+      if (!INV) {
+        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, 0, 0, stwf, qd);
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = fp_to_s64(xf[e]);
+      } else {
+        const double2 fsf = make_double2((double)fs.x, (double)fs.x / qd);
+        const double2 fdf = make_double2((double)fd.x, (double)fd.x / qd);
+        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stwf, qd, qinv, fsf,
+                         fdf);
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = fp_to_residue_small(xf[e], qd);
+      }
+    } else if (!INV)
       fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, stw, pc.q);
     else
       inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc, fs, fd);
@@ -446,14 +471,17 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
   uint64_t* wbuf2 = sm + (kRegWarps * (kNttPair - 1) + warp) * Sh::PAD_S;  // paired polys
   ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kNttPair * kRegWarps * Sh::PAD_S);
   constexpr int LO_S = LOGS - EB;
+  const bool fpp = pc.twf != nullptr;  // FP64 path (common.cuh)
   {
+    const ulonglong2* tws =
+        fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + (INV ? N : 0)) : tw;
     // stage st of blocks [blk0, blk0 + W) uses global twiddles
     // (1 << (a + st)) + (blk0 << st) + [0, W << st)  ->  smem (W << st) + ...
     const int blk0 = blockIdx.x * kRegWarps;
     for (int v = kRegWarps + threadIdx.x; v < kRegWarps * S; v += blockDim.x) {
       const int st = 31 - __clz(v) - kRegWarpsLog;
       const int i = v - (kRegWarps << st);
-      cp_async16(stw + v, tw + (1 << (a + st)) + (blk0 << st) + i);
+      cp_async16(stw + v, tws + (1 << (a + st)) + (blk0 << st) + i);
     }
   }
   const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;
@@ -500,9 +528,11 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
   const ulonglong2 fs = make_ulonglong2(pc.ninv, pc.ninv_sh);
   const ulonglong2 fd = make_ulonglong2(pc.ilast, pc.ilast_sh);
   uint64_t x[E], x2[E];
+  int step = 1;
 #pragma unroll 1
-  for (int pi = 0; pi < U.np; pi += kNttPair) {
-    const bool pair = kNttPair == 2 && pi + 1 < U.np;
+  for (int pi = 0; pi < U.np; pi += step) {
+    const bool pair = kNttPair == 2 && pi + 1 < U.np && !fpp;
+    step = pair ? 2 : 1;
     load(x, U.p0 + pi);
     if (pair) load(x2, U.p0 + pi + 1);
     if (pi == 0) {
@@ -518,6 +548,27 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
                        pc, fs, fd);
       finish(x, U.p0 + pi);
       finish(x2, U.p0 + pi + 1);
+    } else if (fpp) {
+      // forward: signed intermediate in, fully reduced out; inverse: [0, q)
+      // in, signed intermediate (|x| < q) out
+      const double qd = (double)q, qinv = 1.0 / qd;
+      double xf[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) xf[e] = fp_from_s64(x[e]);
+      const double2* stwf = reinterpret_cast<const double2*>(stw);
+      double* wbf = reinterpret_cast<double*>(wbuf);
+      if (!INV) {
+        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, kRegWarpsLog, warp, stwf, qd);
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = fp_to_residue(xf[e], qd, qinv);
+      } else {
+        const double2 one = make_double2(1.0, 1.0 / qd);  // never used: no final stage here
+        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stwf, qd, qinv,
+                         one, one);
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = fp_to_s64(xf[e]);
+      }
+      finish(x, U.p0 + pi);
     } else {
       if (!INV)
         fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);

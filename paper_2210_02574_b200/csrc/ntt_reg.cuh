@@ -110,8 +110,8 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
 }
 
 // Re-distribute the warp's elements from window lo_from to window lo_to.
-template <int LOGS>
-__device__ __forceinline__ void reg_shuffle(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+template <int LOGS, typename T>
+__device__ __forceinline__ void reg_shuffle(T (&x)[RegShape<LOGS>::E], T* buf,
                                             int lane, int lo_from, int lo_to) {
   constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
   if (lo_from == lo_to) return;
@@ -228,6 +228,108 @@ __device__ __forceinline__ void inv_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
     inv_round<LOGS>(x1, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
   }
   reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo_out);
+}
+
+// ---------------------------------------------------------------------------
+// FP64-pipe variants (primes q < 2^kFpMaxBits, common.cuh): elements are
+// integers held in doubles in signed lazy ranges, twiddles are (w, w/q).
+// Forward CT: u + v, u - v with v = w*x in (-q, q): the bound grows by q per
+// stage (<= (stages + 1) q, < 2^51 over both passes of N <= 2^17).
+// Inverse GS: the sum doubles per stage, so it is centred-reduced after every
+// 4th stage and at the end of a non-final pass (bound <= 16 q < 2^50).
+// ---------------------------------------------------------------------------
+template <int LOGS>
+__device__ __forceinline__ void fwd_round_fp(double (&x)[RegShape<LOGS>::E], int lane, int lo,
+                                             int phi, int plo, int g0, int blk,
+                                             const double2* __restrict__ tw, double q) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+#pragma unroll
+  for (int p = LOGS - 1; p >= 0; --p) {
+    if (p > phi || p < plo) continue;
+    const int st = LOGS - 1 - p;
+    const int d = 1 << (p - lo);
+    const int base = (1 << (g0 + st)) + (blk << st);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & d) continue;
+      const int j = reg_j(lane, e, lo, EB);
+      const double2 wp = tw[base + (j >> (p + 1))];
+      const double v = fp_mulmod(x[e + d], wp.x, wp.y, q);
+      const double u = x[e];
+      x[e] = u + v;
+      x[e + d] = u - v;
+    }
+  }
+}
+
+template <int LOGS>
+__device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E], int lane, int lo,
+                                             int plo, int phi, int log_n, int gshift, int blk,
+                                             const double2* __restrict__ tw, double q,
+                                             double qinv, const double2 fin_s,
+                                             const double2 fin_d) {
+  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+#pragma unroll
+  for (int p = 0; p < LOGS; ++p) {
+    if (p < plo || p > phi) continue;
+    const int d = 1 << (p - lo);
+    const bool last = (gshift + p == log_n - 1);
+    const bool red = (p & 3) == 3 || p == LOGS - 1;
+    const int base = (1 << (log_n - gshift - p - 1)) + (blk << (LOGS - p - 1));
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & d) continue;
+      const double a = x[e], b = x[e + d];
+      double s = a + b;
+      const double df = a - b;
+      if (!last) {
+        const int j = reg_j(lane, e, lo, EB);
+        const double2 wp = tw[base + (j >> (p + 1))];
+        x[e] = red ? fp_reduce(s, q, qinv) : s;
+        x[e + d] = fp_mulmod(df, wp.x, wp.y, q);
+      } else {
+        x[e] = fp_mulmod(s, fin_s.x, fin_s.y, q);
+        x[e + d] = fp_mulmod(df, fin_d.x, fin_d.y, q);
+      }
+    }
+  }
+}
+
+template <int LOGS>
+__device__ __forceinline__ void fwd_sub_fp(double (&x)[RegShape<LOGS>::E], double* buf, int lane,
+                                           int lo_in, int lo_out, int g0, int blk,
+                                           const double2* tw, double q) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int phi = LOGS - 1 - r * EB;
+    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
+    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
+    cur = lo;
+    fwd_round_fp<LOGS>(x, lane, lo, phi, plo, g0, blk, tw, q);
+  }
+  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+}
+
+template <int LOGS>
+__device__ __forceinline__ void inv_sub_fp(double (&x)[RegShape<LOGS>::E], double* buf, int lane,
+                                           int lo_in, int lo_out, int log_n, int gshift, int blk,
+                                           const double2* tw, double q, double qinv,
+                                           const double2 fin_s, const double2 fin_d) {
+  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
+  int cur = lo_in;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int plo = r * EB;
+    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
+    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
+    cur = lo;
+    inv_round_fp<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, q, qinv, fin_s, fin_d);
+  }
+  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
 }
 
 }  // namespace hegpu

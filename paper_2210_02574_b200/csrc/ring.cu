@@ -136,7 +136,40 @@ PrimeConst make_prime_const(uint64_t q, int log_n, uint64_t ipsi1) {
   c.ninv_sh = h_shoup(c.ninv, q);
   c.ilast = h_mulmod(ipsi1, c.ninv, q);
   c.ilast_sh = h_shoup(c.ilast, q);
+  c.twf = nullptr;
+  c.pad_ = 0;
   return c;
+}
+
+// FP64 twiddles (w, w/q) of every prime below 2^kFpMaxBits, built from the
+// integer Shoup tables (layout [prime][4N]: forward pairs, inverse pairs).
+// Sets pc[i].twf to the prime's device table; returns the allocation (or
+// nullptr when no prime qualifies or HEGPU_NTT_FP=0).
+static void* attach_fp_twiddles(std::vector<PrimeConst>& pc, const uint64_t* tw, int n) {
+  const char* env = getenv("HEGPU_NTT_FP");
+  if (env && atoi(env) == 0) return nullptr;
+  std::vector<int> fp;
+  for (int i = 0; i < (int)pc.size(); ++i)
+    if (pc[i].q < (1ull << kFpMaxBits)) fp.push_back(i);
+  if (fp.empty()) return nullptr;
+  std::vector<double> h((size_t)fp.size() * 4 * n);
+  for (size_t f = 0; f < fp.size(); ++f) {
+    const int i = fp[f];
+    const double qd = (double)pc[i].q;
+    const uint64_t* t = tw + (size_t)i * 4 * n;
+    double* o = h.data() + f * 4 * n;
+    for (int j = 0; j < 2 * n; ++j) {  // forward then inverse
+      const double w = (double)t[2 * j];
+      o[2 * j] = w;
+      o[2 * j + 1] = w / qd;
+    }
+  }
+  void* d = nullptr;
+  check_cuda(cudaMalloc(&d, h.size() * 8), "alloc fp twiddles");
+  check_cuda(cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice), "copy fp twiddles");
+  for (size_t f = 0; f < fp.size(); ++f)
+    pc[fp[f]].twf = reinterpret_cast<const double2*>(static_cast<double*>(d) + f * 4 * n);
+  return d;
 }
 
 // Twiddles of one prime, natural form, bit-reversed order, as interleaved
@@ -168,6 +201,7 @@ Ring::~Ring() {
     if (kv.second->dmem) cudaFree(kv.second->dmem);
   if (dpc) cudaFree(dpc);
   if (dtw) cudaFree(dtw);
+  if (dtwf) cudaFree(dtwf);
 }
 
 static uint64_t prod_mod(const std::vector<uint64_t>& ps, int skip, uint64_t m) {
@@ -365,6 +399,7 @@ static Ring* create_ring(int log_n, const uint64_t* chain, int n_chain, const ui
     make_twiddles(R->primes[i], log_n, t);
     R->hpc[i] = make_prime_const(R->primes[i], log_n, t[2 * n + 2]);  // ipsi_rev[1]
   }
+  R->dtwf = attach_fp_twiddles(R->hpc, tw.data(), (int)n);
   check_cuda(cudaMalloc(&R->dpc, R->hpc.size() * sizeof(PrimeConst)), "alloc consts");
   check_cuda(cudaMemcpy(R->dpc, R->hpc.data(), R->hpc.size() * sizeof(PrimeConst),
                         cudaMemcpyHostToDevice),
@@ -1407,6 +1442,8 @@ static void shim_ntt(bool inverse, uint64_t* a, int k, int n, const uint64_t* tw
     }
   }
   const size_t bytes = (size_t)k * n * 8;
+  DevBuf dtwf(0);
+  if (log_n >= 12) dtwf.p = attach_fp_twiddles(pc, tw.data(), n);
   DevBuf dpc(pc.size() * sizeof(PrimeConst)), dtw(tw.size() * 8), da(bytes);
   h2d(dpc.p, pc.data(), pc.size() * sizeof(PrimeConst));
   h2d(dtw.p, tw.data(), tw.size() * 8);

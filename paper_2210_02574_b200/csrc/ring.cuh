@@ -52,6 +52,7 @@ struct Ring {
   std::vector<PrimeConst> hpc;
   PrimeConst* dpc = nullptr;
   uint64_t* dtw = nullptr;  // [n_primes][4][N]: psi, psi_sh, ipsi, ipsi_sh
+  void* dtwf = nullptr;     // FP64 twiddles of the primes < 2^kFpMaxBits (PrimeConst::twf)
   std::mutex mu;
   std::map<std::pair<int, int>, std::unique_ptr<KsLevel>> ks;
   // rescale constants: level -> (q_level^-1 mod q_i, shoup) for i < level
