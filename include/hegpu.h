@@ -127,6 +127,20 @@ int hegpu_lift_centered(hegpu_ring_t ring, const uint64_t* src, int64_t src_stri
                         int src_prime, uint64_t* out, int64_t out_stride, int n_polys,
                         int k, const int32_t* primes, void* stream);
 
+/* Full-slot bootstrap diagonals, generated and encoded on the device: for
+ * i < n_diags the slot vector of diagonal d[i] of the CoeffToSlot (kind 0,
+ * bootstrap.py:174-184) or SlotToCoeff (kind 1, bootstrap.py:187-197) map of
+ * output/input half `half`, times `fold`, rolled by g0[i] and conjugated when
+ * conj[i] (the BSGS plaintexts of bootstrap.py:219-236), encoded at `scale`
+ * like encoding.encode (encoding.py:62-97): out[i*N + k] = rounded int64
+ * coefficient k.  d, g0, conj are host arrays; scratch is a device buffer of
+ * min(n_diags, 256) * N * 16 bytes.  Coefficients >= 2^62 in magnitude set a
+ * sticky flag read (and cleared) by hegpu_encode_overflow (synchronizes). */
+int hegpu_encode_diags(hegpu_ring_t ring, int kind, int half, double fold, double scale,
+                       int n_diags, const int32_t* d, const int32_t* g0, const uint8_t* conj,
+                       void* scratch, int64_t* out, void* stream);
+int hegpu_encode_overflow(hegpu_ring_t ring, int* flag);
+
 /* X -> X^g.  eval_form=1: slot permutation on bit-reversed evaluation form
  * (poly_automorphism_eval, ring.py:471-482); eval_form=0: signed coefficient
  * permutation (poly_automorphism, ring.py:426-437).  in != out. */

@@ -40,6 +40,9 @@ SIGNATURES = {
     "hegpu_lift_signed": [_P, _P, _I64, _P, _I64, _I, _I, _P, _P],
     "hegpu_lift_centered": [_P, _P, _I64, _I, _P, _I64, _I, _I, _P, _P],
     "hegpu_automorphism": [_P, _I, _U64, _P, _I64, _P, _I64, _I, _I, _P, _P],
+    "hegpu_encode_diags": [_P, _I, _I, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P, _P,
+                           _P, _P],
+    "hegpu_encode_overflow": [_P, _P],
     "hegpu_tensor": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_apply": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _P, _I64, _I, _P],
     "hegpu_tensor_periodic": [_P, _P, _P, _I64, _I, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
@@ -70,7 +73,7 @@ _RESTYPES = {
     "hegpu_launch_count": ctypes.c_longlong,
 }
 PROF_CLASSES = ("ntt", "elementwise", "lift", "automorphism", "tensor", "conv", "ks_ip",
-                "diag_mac", "encrypt",
+                "diag_mac", "encrypt", "encode",
                 # subsets of "ntt" by the step that issued them (not additive)
                 "ntt_modup", "ntt_moddown", "ntt_rescale")
 

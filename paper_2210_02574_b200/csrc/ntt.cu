@@ -264,6 +264,9 @@ constexpr int kNttPair = HEGPU_NTT_PAIR;
 // conversion prologue: up to this many source limbs take the unrolled path
 // (all source words of a coefficient in flight at once)
 constexpr int kConvMaxSrc = 8;
+#ifndef HEGPU_BLOCKS_MINB
+#define HEGPU_BLOCKS_MINB 4
+#endif
 #ifndef HEGPU_COLS_MINB
 #define HEGPU_COLS_MINB 5
 #endif
@@ -304,6 +307,12 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
   const ulonglong2* tw =
       reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + (INV ? 2 * (size_t)N : 0));
   uint64_t* tile = sm;
+  // tile slot of (row r, column c): with 8 columns an XOR swizzle makes both
+  // the row-wise fill and the column-wise register load conflict-free
+  auto tix = [](int r, int c) {
+    if constexpr (kRegWarps == 8) return r * 8 + (c ^ ((r >> 1) & 7));
+    else return r * TS + c;
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* wbuf = sm + S * TS + warp * Sh::PAD_S;
   ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + S * TS + kRegWarps * Sh::PAD_S);
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
   const ulonglong2* tws =
       fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + (INV ? N : 0)) : tw;
   // every column transform of this pass uses twiddles [1, S) of its table
-  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + i, tws + i);
+  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + tw_sw(i), tws + i);
   // conversion constants of this target limb: punc[i], fp32 weight, shift
   uint64_t* s_conv = reinterpret_cast<uint64_t*>(stw + S);
   const int nsrc = CM >= 2 ? sg.c_nsrc : 0;
@@ -343,7 +352,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
         const int r = e / kRegWarps, c = e % kRegWarps;
         const uint64_t u = __ldg(hs + c0 + c + (size_t)C * r);
         const int64_t v = u > (qs >> 1) ? (int64_t)u - (int64_t)qs : (int64_t)u;
-        tile[r * TS + c] = signed_mod(v, pc);
+        tile[tix(r, c)] = signed_mod(v, pc);
       }
     } else if constexpr (CM >= 2) {
       // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
             if (nsrc == kConvMaxSrc) acc.fold(q, pc.bar);
             acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
           }
-          tile[r * TS + c] = acc.redc(pc);
+          tile[tix(r, c)] = acc.redc(pc);
         }
       } else
       for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
@@ -399,12 +408,12 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
           if (sg.c_nsrc % kMacFold == 0) acc.fold(q, pc.bar);
           acc.add(static_cast<uint64_t>(__float2int_rn(f)), negd);
         }
-        tile[r * TS + c] = acc.redc(pc);
+        tile[tix(r, c)] = acc.redc(pc);
       }
     } else {
       for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
         const int r = e / kRegWarps, c = e % kRegWarps;
-        tile[r * TS + c] = src[c0 + c + (size_t)C * r];
+        tile[tix(r, c)] = src[c0 + c + (size_t)C * r];
       }
     }
     if (pi == 0) cp_async_wait_all();
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
     constexpr int LO_S = LOGS - EB;  // strided window: j = lane + 32 e
     uint64_t x[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = tile[reg_j(lane, e, LO_S, EB) * TS + warp];
+    for (int e = 0; e < E; ++e) x[e] = tile[tix(reg_j(lane, e, LO_S, EB), warp)];
     if (fpp) {
       // forward: [0, q) in, signed lazy intermediate out; inverse: the
       // signed intermediate in, fully reduced out
@@ -439,18 +448,18 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
     else
       inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc, fs, fd);
 #pragma unroll
-    for (int e = 0; e < E; ++e) tile[reg_j(lane, e, LO_S, EB) * TS + warp] = x[e];
+    for (int e = 0; e < E; ++e) tile[tix(reg_j(lane, e, LO_S, EB), warp)] = x[e];
     __syncthreads();
     for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
       const int r = e / kRegWarps, c = e % kRegWarps;
-      dst[c0 + c + (size_t)C * r] = tile[r * TS + c];
+      dst[c0 + c + (size_t)C * r] = tile[tix(r, c)];
     }
     if (pi + 1 < U.np) __syncthreads();  // the tile is reloaded for the next poly
   }
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 2 ? 3 : 4)) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 2 ? 3 : HEGPU_BLOCKS_MINB)) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
     for (int v = kRegWarps + threadIdx.x; v < kRegWarps * S; v += blockDim.x) {
       const int st = 31 - __clz(v) - kRegWarpsLog;
       const int i = v - (kRegWarps << st);
-      cp_async16(stw + v, tws + (1 << (a + st)) + (blk0 << st) + i);
+      cp_async16(stw + tw_sw(v), tws + (1 << (a + st)) + (blk0 << st) + i);
     }
   }
   const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;

@@ -35,6 +35,22 @@ __device__ __forceinline__ int reg_j(int lane, int e, int lo, int eb) {
   return (lane & ((1 << lo) - 1)) | (e << lo) | ((lane >> lo) << (lo + eb));
 }
 __device__ __forceinline__ int padi(int j) { return j + (j >> 4); }
+// warp-buffer slot of element j: 64-bit accesses are served per half-warp, so
+// a half-warp's 16 words must hit 16 distinct bank pairs.  For the round
+// windows of S = 128 / 256 the XOR swizzle j ^ ((j >> 3) & 15) is
+// conflict-free in every round (1 padded word per 16 leaves 2-way conflicts);
+// for S = 512 the padding is.
+template <int LOGS>
+__device__ __forceinline__ int shf_idx(int j) {
+  if constexpr (LOGS == 7 || LOGS == 8)
+    return j ^ ((j >> 3) & 15);
+  else
+    return padi(j);
+}
+// shared-memory slot of staged twiddle i (16-byte entries, served per quarter
+// warp): late stages read twiddles at a lane stride of 2..8 entries, which the
+// swizzle spreads over the 8 bank groups (4x fewer wavefronts at stride 4)
+__device__ __forceinline__ int tw_sw(int i) { return i ^ ((i >> 3) & 7); }
 
 
 // Forward CT butterflies on register window [lo, lo+EB) for bit positions
@@ -60,7 +76,7 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
       const int ti = base + (j >> (p + 1));
       uint64_t u = x[e];
       u = u >= q2 ? u - q2 : u;
-      const ulonglong2 wp = tw[ti];
+      const ulonglong2 wp = tw[tw_sw(ti)];
       const uint64_t v = shoup_lazy(x[e + d], wp.x, wp.y, q);
       x[e] = u + v;
       x[e + d] = u - v + q2;
@@ -99,7 +115,7 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
         const int j = reg_j(lane, e, lo, EB);
         const int ti = base + (j >> (p + 1));
         x[e] = s;
-        const ulonglong2 wp = tw[ti];
+        const ulonglong2 wp = tw[tw_sw(ti)];
         x[e + d] = shoup_lazy(df, wp.x, wp.y, q);
       } else {
         x[e] = shoup(s, fin_s.x, fin_s.y, q);
@@ -116,10 +132,10 @@ __device__ __forceinline__ void reg_shuffle(T (&x)[RegShape<LOGS>::E], T* buf,
   constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
   if (lo_from == lo_to) return;
 #pragma unroll
-  for (int e = 0; e < E; ++e) buf[padi(reg_j(lane, e, lo_from, EB))] = x[e];
+  for (int e = 0; e < E; ++e) buf[shf_idx<LOGS>(reg_j(lane, e, lo_from, EB))] = x[e];
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = buf[padi(reg_j(lane, e, lo_to, EB))];
+  for (int e = 0; e < E; ++e) x[e] = buf[shf_idx<LOGS>(reg_j(lane, e, lo_to, EB))];
   __syncwarp();
 }
 
@@ -174,14 +190,14 @@ __device__ __forceinline__ void reg_shuffle2(uint64_t (&x0)[RegShape<LOGS>::E],
   if (lo_from == lo_to) return;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int j = padi(reg_j(lane, e, lo_from, EB));
+    const int j = shf_idx<LOGS>(reg_j(lane, e, lo_from, EB));
     b0[j] = x0[e];
     b1[j] = x1[e];
   }
   __syncwarp();
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int j = padi(reg_j(lane, e, lo_to, EB));
+    const int j = shf_idx<LOGS>(reg_j(lane, e, lo_to, EB));
     x0[e] = b0[j];
     x1[e] = b1[j];
   }
@@ -253,7 +269,7 @@ __device__ __forceinline__ void fwd_round_fp(double (&x)[RegShape<LOGS>::E], int
     for (int e = 0; e < E; ++e) {
       if (e & d) continue;
       const int j = reg_j(lane, e, lo, EB);
-      const double2 wp = tw[base + (j >> (p + 1))];
+      const double2 wp = tw[tw_sw(base + (j >> (p + 1)))];
       const double v = fp_mulmod(x[e + d], wp.x, wp.y, q);
       const double u = x[e];
       x[e] = u + v;
@@ -284,7 +300,7 @@ __device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E], int
       const double df = a - b;
       if (!last) {
         const int j = reg_j(lane, e, lo, EB);
-        const double2 wp = tw[base + (j >> (p + 1))];
+        const double2 wp = tw[tw_sw(base + (j >> (p + 1)))];
         x[e] = red ? fp_reduce(s, q, qinv) : s;
         x[e + d] = fp_mulmod(df, wp.x, wp.y, q);
       } else {

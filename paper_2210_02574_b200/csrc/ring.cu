@@ -202,6 +202,9 @@ Ring::~Ring() {
   if (dpc) cudaFree(dpc);
   if (dtw) cudaFree(dtw);
   if (dtwf) cudaFree(dtwf);
+  if (enc.dlog) cudaFree(enc.dlog);
+  if (enc.pow5) cudaFree(enc.pow5);
+  if (enc.overflow) cudaFree(enc.overflow);
 }
 
 static uint64_t prod_mod(const std::vector<uint64_t>& ps, int skip, uint64_t m) {
@@ -1615,6 +1618,23 @@ int hegpu_lift_centered(hegpu_ring_t ring, const uint64_t* src, int64_t src_stri
     if (src_prime < 0 || src_prime >= R.n_primes) throw HegpuError{HEGPU_E_ARG, "bad src prime"};
     launch_lift_centered(R.dpc, R.log_n, src, src_stride, R.primes[src_prime], out, out_stride,
                          n_polys, k, primes, S_(stream));
+  })
+}
+
+int hegpu_encode_diags(hegpu_ring_t ring, int kind, int half, double fold, double scale,
+                       int n_diags, const int32_t* d, const int32_t* g0, const uint8_t* conj,
+                       void* scratch, int64_t* out, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    launch_encode_diags(R, kind, half, fold, scale, n_diags, d, g0, conj,
+                        static_cast<double2*>(scratch), out, S_(stream));
+  })
+}
+
+int hegpu_encode_overflow(hegpu_ring_t ring, int* flag) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    *flag = encode_overflow_check(R) ? 1 : 0;
   })
 }
 

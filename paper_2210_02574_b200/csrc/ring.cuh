@@ -45,6 +45,14 @@ struct KsLevel {
   uint64_t p_mod_ql = 0;                  // P mod q_level
 };
 
+// device tables of the diagonal encoder (encode.cu), built on first use
+struct EncTables {
+  int32_t* dlog = nullptr;  // spectrum index -> slot | (conj << 30)
+  int32_t* pow5 = nullptr;  // 5^j mod 2N
+  int* overflow = nullptr;  // sticky |coefficient| >= 2^62 flag
+};
+constexpr int kEncMaxDiags = 256;  // diagonals per encode launch (kernel parameter space)
+
 struct Ring {
   int log_n = 0, n = 0, n_chain = 0, n_special = 0, n_primes = 0;
   int device = 0;
@@ -58,7 +66,10 @@ struct Ring {
   // rescale constants: level -> (q_level^-1 mod q_i, shoup) for i < level
   std::map<int, std::pair<std::vector<uint64_t>, std::vector<uint64_t>>> rescale;
 
+  EncTables enc;
+
   ~Ring();
+  const EncTables& enc_tables();
   const KsLevel& ks_level(int level, int alpha);
   const std::pair<std::vector<uint64_t>, std::vector<uint64_t>>& rescale_consts(int level);
   int special_prime(int i) const { return n_chain + i; }
@@ -109,6 +120,7 @@ enum ProfClass {
   PROF_KS_IP,
   PROF_DIAG_MAC,
   PROF_ENCRYPT,
+  PROF_ENCODE,
   PROF_NUM_CLASSES
 };
 // bytes / modmuls: ALGORITHMIC traffic and modular multiplications of the
@@ -276,5 +288,11 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
                  uint64_t* out, int64_t out_gstride, int k, cudaStream_t st, int kq,
                  int n_chain);
+
+// encode.cu: full-slot bootstrap diagonals -> rounded integer coefficients
+void launch_encode_diags(Ring& R, int kind, int half, double fold, double scale, int n_diags,
+                         const int32_t* d, const int32_t* g0, const uint8_t* conj,
+                         double2* scratch, int64_t* out, cudaStream_t st);
+bool encode_overflow_check(Ring& R);
 
 }  // namespace hegpu

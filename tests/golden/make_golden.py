@@ -193,6 +193,25 @@ def boot_fixture():
     return res
 
 
+def boot_full_fixture():
+    """Full-slot (4,096 slots) bootstrap at desk-boot, N = 2^13: the
+    reference's error on one seeded ciphertext (its diagonals are the ones
+    the GPU encoder generates, bootstrap.py:319-335)."""
+    params = ckks.get_preset("desk-boot")
+    ctx = bs.build_context(params, n_slots=params.slot_count)
+    steps = sorted(set(ctx.required_rotation_steps()))
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=11)
+    v = np.random.default_rng(1003).uniform(-1, 1, params.slot_count)
+    ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=22)
+    t0 = time.time()
+    out = bs.bootstrap(ct, ctx, keys)
+    tb = time.time() - t0
+    dec = ckks.decrypt_vector(out, keys)
+    np.savez_compressed(os.path.join(HERE, "boot_desk_full.npz"), v=v, dec=dec)
+    return {"steps": steps, "enc": ct_digest(ct), "out_level": out.level,
+            "bootstrap_seconds": tb, "err": float(np.max(np.abs(dec - v)))}
+
+
 def logreg_fixture():
     params = ckks.get_preset("desk")
     keys = ckks.keygen(params, rng_seed=7)
@@ -215,6 +234,14 @@ def logreg_fixture():
 
 def main():
     t0 = time.time()
+    if sys.argv[1:] == ["boot_full"]:  # add / refresh only this entry
+        path = os.path.join(HERE, "digests.json")
+        digests = json.load(open(path))
+        digests["boot_desk_full"] = boot_full_fixture()
+        with open(path, "w") as fh:
+            json.dump(digests, fh, indent=1, sort_keys=True)
+        print("boot_full written in %.1fs" % (time.time() - t0), file=sys.stderr)
+        return
     kernels_fixture()
     ring_fixture()
     digests = {}
@@ -227,6 +254,7 @@ def main():
         digests[name], _ = scheme_digests(params, name, [1], conj=False, full=(name == "p14"))
         print(name, "done", time.time() - t0, file=sys.stderr)
     digests["boot_desk64"] = boot_fixture()
+    digests["boot_desk_full"] = boot_full_fixture()
     ref_sig = os.path.join(os.path.dirname(minimax.__file__), "approximants", "sigmoid_deg15.txt")
     digests["sigmoid_ref"] = [float(c).hex() for c in
                               minimax.import_text(open(ref_sig).read()).cheb_coeffs]

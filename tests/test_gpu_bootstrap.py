@@ -173,3 +173,89 @@ def test_captured_bootstrap_replays(boot):
     host = torch.stack([c2.c0.data, c2.c1.data]).cpu()
     out2 = cap.run(host.to("cuda"))
     assert np.max(np.abs(ckks.decrypt_vector(out2, keys)[:64] - v2)) < 1e-2
+
+
+# ---------------------------------------------------------------------------
+# full-slot contexts: diagonals generated + encoded on the device
+# ---------------------------------------------------------------------------
+
+
+def test_gpu_diag_encode_matches_host_encode():
+    """hegpu_encode_diags reproduces the host encode (numpy FFT + rint,
+    encoding.py:62-97) of the closed-form diagonals (bootstrap.py:174-197),
+    rolled and conjugated as in the BSGS loop (bootstrap.py:219-236), up to
+    float rounding of the last bits."""
+    import ctypes
+
+    import torch
+
+    from paper_2210_02574_b200 import _dev, _lib
+
+    params = ckks.get_preset("desk-boot")
+    ctx = bs.build_context(params, n_slots=params.slot_count)
+    n, s = params.ring_degree, params.slot_count
+    s_in = params.default_scale
+    cases = [(bs.DIAG_KIND_CTS, 0, 0, 0, 0), (bs.DIAG_KIND_CTS, 1, 65, 64, 1),
+             (bs.DIAG_KIND_CTS, 0, s - 1, s - 64, 1), (bs.DIAG_KIND_STC, 0, 3, 0, 0),
+             (bs.DIAG_KIND_STC, 1, 130, 128, 0)]
+    for kind, half, d, g0, conj in cases:
+        if kind == bs.DIAG_KIND_CTS:
+            vals, fold, scale = bs._cts_diag_full(ctx, d, half, s_in), bs._cts_fold(ctx, s_in), \
+                float(params.ring.moduli_chain[params.max_level])
+        else:
+            vals, fold, scale = bs._stc_diag_full(ctx, d, half, s_in), \
+                params.ring.moduli_chain[0] / s_in, params.default_scale
+        if conj:
+            vals = np.conj(vals)
+        want = bs._coeffs_from_rows(n, np.roll(vals, g0)[None, :], scale)[0]
+        coeffs = _dev.empty(1, n)
+        scratch = torch.empty((1, n, 2), dtype=torch.float64, device="cuda")
+        dd, gg, cc = (np.array([x], dtype=t) for x, t in ((d, np.int32), (g0, np.int32),
+                                                           (conj, np.uint8)))
+        _lib.call("hegpu_encode_diags", params.ring.device(), kind, half, ctypes.c_double(fold),
+                  ctypes.c_double(scale), 1, dd.ctypes.data, gg.ctypes.data, cc.ctypes.data,
+                  scratch.data_ptr(), coeffs.data_ptr(), _dev.stream())
+        got = coeffs.cpu().numpy()[0].astype(np.float64)
+        tol = max(2.0, 1e-12 * np.max(np.abs(want)))
+        assert np.max(np.abs(got - want)) <= tol, (kind, half, d, g0, conj)
+
+
+@pytest.fixture(scope="module")
+def boot_full(digests):
+    params = ckks.get_preset("desk-boot")
+    ctx = bs.build_context(params, n_slots=params.slot_count)
+    d = digests["boot_desk_full"]
+    assert sorted(set(ctx.required_rotation_steps())) == d["steps"]
+    keys = ckks.keygen(params, rotation_steps=d["steps"], rng_seed=11)
+    return params, ctx, keys, d
+
+
+def test_full_slot_bootstrap_matches_reference(boot_full):
+    """Full-slot bootstrap (4,096 slots, bootstrap.py:319-335) with the
+    device-generated diagonals: reference tolerance, same quality as the
+    reference's own run on the same seeded ciphertext (golden fixture)."""
+    params, ctx, keys, d = boot_full
+    g = golden_npz("boot_desk_full.npz")
+    v = g["v"]
+    ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=22)
+    assert ct_digest(ct) == d["enc"]
+    out = bs.bootstrap(ct, ctx, keys)
+    assert out.level == ctx.output_level == d["out_level"]
+    assert out.scale == params.default_scale
+    dec = ckks.decrypt_vector(out, keys)
+    err = np.max(np.abs(dec - v))
+    assert err < 1e-2  # T/test_bootstrap.py:23
+    assert err <= max(2 * d["err"], 5e-3)
+    assert np.max(np.abs(dec - g["dec"])) < 1e-2
+
+
+def test_full_slot_bootstrap_batched(boot_full):
+    """Two ciphertexts refreshed by one batched full-slot bootstrap (the
+    ingest path): every diagonal is generated once for the batch."""
+    params, ctx, keys, _ = boot_full
+    rng = np.random.default_rng(41)
+    vs = [rng.uniform(-1, 1, params.slot_count) for _ in range(2)]
+    cts = [ckks.encrypt_vector(params, v, keys, level=0) for v in vs]
+    outs = bs.bootstrap_many(cts, ctx, keys)
+    for o, v in zip(outs, vs):
+        assert np.max(np.abs(ckks.decrypt_vector(o, keys) - v)) < 1e-2
