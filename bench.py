@@ -341,6 +341,83 @@ class BootstrapWorkload:
                 "diag_cache_gib": round(diag_gib(self.ctx), 2)}
 
 
+class BootstrapFullWorkload:
+    """cfg3 (full): full-slot bootstrap (32,768 slots) at N=2^16, B ciphertexts
+    per step (BENCH_FULL_BATCH, default 1; B > 1 is the batched data-ingest
+    refresh of logreg.py:338).  Its 196,609 diagonals are generated and encoded
+    on the GPU every step (the reference encodes them on the host, ~2 h per
+    bootstrap at N=2^16).  Metric: ms per refreshed ciphertext."""
+
+    metric = "CKKS bootstrap ms (N=2^16)"
+    unit = "ms"
+    higher = False
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_2210_02574_b200 import bootstrap as bs, ckks
+        from paper_2210_02574_b200.ckks import ops
+
+        self.params = p16()
+        slots = self.params.slot_count
+        self.ctx = bs.build_context(self.params, n_slots=slots)
+        steps = self.ctx.required_rotation_steps()
+        t0 = time.time()
+        self.keys = ckks.keygen(self.params, rotation_steps=steps, rng_seed=7)
+        self.keygen_s = time.time() - t0
+        self.batch = int(os.environ.get("BENCH_FULL_BATCH", "1"))
+        self.ms_div = self.batch
+        rng = np.random.default_rng(1002)
+        self.vs = [rng.uniform(-1, 1, slots) for _ in range(self.batch)]
+        self.cts = [ckks.encrypt_vector(self.params, v, self.keys, level=0, rng_seed=5 + i)
+                    for i, v in enumerate(self.vs)]
+        self.ct = self.cts[0] if self.batch == 1 else ops.stack(self.cts)
+        self.host = torch.stack([self.ct.c0.data, self.ct.c1.data]).cpu().pin_memory()
+        self.h2d = self.host.numel() * 8
+        self.d2h = 0
+        self.units = 1
+        self.config = {"workload": "cfg3 full-slot bootstrap (32768 slots)", "preset": "p16",
+                       "N": self.params.ring_degree, "n_slots": slots,
+                       "ciphertexts_per_step": self.batch, "rotation_keys": len(steps),
+                       "unit_note": "ms per refreshed ciphertext (step time / batch)",
+                       "diagonals": "generated + encoded on the GPU every step"}
+
+    def _boot(self, ct):
+        from paper_2210_02574_b200 import bootstrap as bs
+        from paper_2210_02574_b200.ckks import ops
+
+        if ct.batch is None:
+            return [bs.bootstrap(ct, self.ctx, self.keys)]
+        return bs.bootstrap_many(ops.unstack(ct), self.ctx, self.keys)
+
+    def step(self):
+        self.outs = self._boot(self.ct)
+        return self.outs
+
+    def e2e_step(self):
+        from paper_2210_02574_b200.ckks import ops
+
+        lead = () if self.ct.batch is None else (self.ct.batch,)
+        t = ops._packed(self.params, lead, 0)
+        t.copy_(self.host.to("cuda", non_blocking=True).transpose(0, 1) if lead
+                else self.host.to("cuda", non_blocking=True))
+        ct = ops._ct(t, 0, self.ct.scale, self.ct.slot_count, self.params)
+        outs = self._boot(ct)
+        self.d2h = sum(o.c0.data.numel() * 16 for o in outs)
+        return [torch_stack_host(o) for o in outs]
+
+    def oracle_sample(self):
+        return cost_model_sample(self.params, self.histogram, 1, "ms")
+
+    def check(self):
+        from paper_2210_02574_b200 import ckks
+
+        errs = [float(np.max(np.abs(ckks.decrypt_vector(o, self.keys) - v)))
+                for o, v in zip(self.outs, self.vs)]
+        return {"max_abs_err": max(errs), "output_level": self.outs[0].level,
+                "keygen_s": round(self.keygen_s, 1)}
+
+
 def logreg_rotation_steps(layout):
     """Rotation steps of the gradient pipeline (logreg.py:202-229): the
     reference's doubling steps plus the multiples the hoisted radix-4 rounds
@@ -521,7 +598,8 @@ class TrainWorkload:
                 "diag_cache_gib": round(diag_gib(self.ctx), 2)}
 
 
-WORKLOADS = {"train": TrainWorkload, "ks": KsWorkload, "bootstrap": BootstrapWorkload}
+WORKLOADS = {"train": TrainWorkload, "ks": KsWorkload, "bootstrap": BootstrapWorkload,
+             "bootstrap_full": BootstrapFullWorkload}
 
 
 # ---------------------------------------------------------------------------
@@ -605,9 +683,9 @@ def run_ours(args):
     if wl.higher:
         value = wl.units / (ms_step / 1e3)
         e2e_value = wl.units / (e2e_ms / 1e3)
-    else:
-        value = ms_step
-        e2e_value = e2e_ms
+    else:  # time per unit (a full-slot step refreshes `ms_div` ciphertexts)
+        value = ms_step / getattr(wl, "ms_div", 1)
+        e2e_value = e2e_ms / getattr(wl, "ms_div", 1)
     peak, peak_kind = measured_peaks()
     dom = max(prof, key=lambda c: prof[c]["ms"])
     dp = prof[dom]
@@ -680,7 +758,7 @@ def run_reference(args):
             return self.text
 
     wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", "p16.preset"))
-    if args.config in ("train", "bootstrap"):
+    if args.config in ("train", "bootstrap", "bootstrap_full"):
         wl.histogram = load_histogram(args.config)
         wl.units = TrainWorkload.batch_rows if args.config == "train" else 1
     vals = []

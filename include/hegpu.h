@@ -141,6 +141,13 @@ int hegpu_encode_diags(hegpu_ring_t ring, int kind, int half, double fold, doubl
                        void* scratch, int64_t* out, void* stream);
 int hegpu_encode_overflow(hegpu_ring_t ring, int* flag);
 
+/* Forward NTT of signed int64 coefficient rows into k eval-form limbs: the
+ * lift of poly_from_signed (ring.py:381-393) fused into the NTT's first pass.
+ * src poly p at src + p*src_stride, out poly p at out + p*out_stride. */
+int hegpu_ntt_from_signed(hegpu_ring_t ring, const int64_t* src, int64_t src_stride,
+                          uint64_t* out, int64_t out_stride, int n_polys, int k,
+                          const int32_t* primes, void* stream);
+
 /* X -> X^g.  eval_form=1: slot permutation on bit-reversed evaluation form
  * (poly_automorphism_eval, ring.py:471-482); eval_form=0: signed coefficient
  * permutation (poly_automorphism, ring.py:426-437).  in != out. */

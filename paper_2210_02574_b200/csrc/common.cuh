@@ -254,6 +254,8 @@ struct Seg {
   int64_t ein_stride;
   // cmode 1: the prologue instead lifts one coefficient-form limb (modulus
   // csrc_q, at csrc + p*csrc_stride) centered into every limb (rescale/ModRaise)
+  // cmode 3: the prologue reads signed int64 coefficients (csrc + p*csrc_stride)
+  // and reduces them into every limb (numpy np.mod semantics)
   // cmode 2: conversion of the CENTERED representative: the overflow count
   // e = round(sum_i hat_i / d_i) is estimated in fp32 from (hat_i >> cfs[i]) *
   // cfw[i] (cfw = 2^cfs / d_i; both read at stride 2, one per 64-bit word)

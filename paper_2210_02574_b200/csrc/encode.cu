@@ -36,6 +36,7 @@ struct DiagEncParams {
   double fold, scale;
   const int32_t* dlog;  // spectrum index m -> slot j | (conj << 30)
   const int32_t* pow5;  // j -> 5^j mod 2N, j < N/2
+  const double2* eroot; // e -> exp(i pi e / N), e < 2N (every root the encoder needs)
   double2* y;           // pass A -> pass B scratch [diag][N]
   int64_t* out;         // [diag][N] rounded coefficients
   int* overflow;
@@ -60,9 +61,8 @@ __device__ __forceinline__ double2 diag_value(const DiagEncParams& P, int i, int
     e = ((long long)P.pow5[src] * col) % two_n2;
   }
   if (e < 0) e += two_n2;
-  double sn, cs;
-  sincospi((double)e / (double)n, &sn, &cs);  // exp(i pi e / N)
-  return make_double2(cs * P.fold, (conj ? -sn : sn) * P.fold);
+  const double2 r = P.eroot[e];  // exp(i pi e / N)
+  return make_double2(r.x * P.fold, (conj ? -r.y : r.y) * P.fold);
 }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -91,13 +91,11 @@ __device__ void smem_dft(double2* buf, const double2* tw, int log_l) {
 
 __device__ __forceinline__ int bitrev(int x, int bits) { return __brev(x) >> (32 - bits); }
 
-__device__ void fill_twiddles(double2* tw, int log_l) {
-  const int L = 1 << log_l;
-  for (int t = threadIdx.x; t < L / 2; t += blockDim.x) {
-    double sn, cs;
-    sincospi(-2.0 * t / L, &sn, &cs);
-    tw[t] = make_double2(cs, sn);
-  }
+// tw[t] = e^{-2 pi i t / L} = eroot[-2 t N / L mod 2N]
+__device__ void fill_twiddles(double2* tw, int log_l, const double2* eroot, int log_n) {
+  const int L = 1 << log_l, two_n = 2 << log_n;
+  for (int t = threadIdx.x; t < L / 2; t += blockDim.x)
+    tw[t] = eroot[(two_n - ((2 * t) << (log_n - log_l))) & (two_n - 1)];
 }
 
 // pass A: columns m2 of x[N2 m1 + m2], DFT over m1, twiddle e^{-2 pi i m2 k1 / N},
@@ -109,7 +107,7 @@ __global__ void __launch_bounds__(256) k_enc_pass_a(const __grid_constant__ Diag
   double2* tw = esm + kEncCols * n1;
   const int i = blockIdx.y;
   const int m2_0 = blockIdx.x * kEncCols;
-  fill_twiddles(tw, a);
+  fill_twiddles(tw, a, P.eroot, P.log_n);
   for (int e = threadIdx.x; e < kEncCols * n1; e += blockDim.x) {
     const int c = e / n1, m1 = e - c * n1;
     const int m = n2 * m1 + m2_0 + c;
@@ -126,9 +124,9 @@ __global__ void __launch_bounds__(256) k_enc_pass_a(const __grid_constant__ Diag
   for (int e = threadIdx.x; e < kEncCols * n1; e += blockDim.x) {
     const int k1 = e / kEncCols, c = e - k1 * kEncCols;
     const int m2 = m2_0 + c;
-    double sn, cs;
-    sincospi(-2.0 * (double)((m2 * k1) & (n - 1)) / n, &sn, &cs);
-    y[(size_t)k1 * n2 + m2] = cmul(buf[c * n1 + k1], make_double2(cs, sn));
+    // e^{-2 pi i m2 k1 / N} = eroot[-2 (m2 k1 mod N) mod 2N]
+    const double2 w = P.eroot[(2 * n - 2 * ((m2 * k1) & (n - 1))) & (2 * n - 1)];
+    y[(size_t)k1 * n2 + m2] = cmul(buf[c * n1 + k1], w);
   }
 }
 
@@ -142,7 +140,7 @@ __global__ void __launch_bounds__(256) k_enc_pass_b(const __grid_constant__ Diag
   double2* tw = esm + kEncCols * n2;
   const int i = blockIdx.y;
   const int k1_0 = blockIdx.x * kEncCols;
-  fill_twiddles(tw, b);
+  fill_twiddles(tw, b, P.eroot, P.log_n);
   const double2* y = P.y + (size_t)i * n;
   for (int e = threadIdx.x; e < kEncCols * n2; e += blockDim.x) {
     const int c = e / n2, m2 = e - c * n2;
@@ -155,10 +153,9 @@ __global__ void __launch_bounds__(256) k_enc_pass_b(const __grid_constant__ Diag
   for (int e = threadIdx.x; e < kEncCols * n2; e += blockDim.x) {
     const int k2 = e / kEncCols, c = e - k2 * kEncCols;
     const int k = k1_0 + c + n1 * k2;
-    double sn, cs;
-    sincospi((double)k / n, &sn, &cs);  // zeta^k = exp(i pi k / N)
+    const double2 z = P.eroot[k];  // zeta^k = exp(i pi k / N)
     const double2 x = buf[c * n2 + k2];
-    const double v = rint((x.x * cs + x.y * sn) * inv_n);
+    const double v = rint((x.x * z.x + x.y * z.y) * inv_n);
     if (!(fabs(v) < 4611686018427387904.0)) atomicExch(P.overflow, 1);  // 2^62
     out[k] = (int64_t)v;
   }
@@ -170,6 +167,11 @@ const EncTables& Ring::enc_tables() {
   const int s = n / 2;
   const uint64_t two_n = 2ull * n;
   std::vector<int32_t> pw(s), dl(n, -1);
+  std::vector<double2> er(2 * (size_t)n);
+  for (int e = 0; e < 2 * n; ++e) {  // exp(i pi e / N) in long double
+    const long double ang = 3.141592653589793238462643383279503L * e / n;
+    er[e] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
   uint64_t g = 1;
   for (int j = 0; j < s; ++j) {
     pw[j] = (int32_t)g;
@@ -180,6 +182,9 @@ const EncTables& Ring::enc_tables() {
   check_cuda(cudaMalloc(&enc.dlog, n * sizeof(int32_t)), "alloc dlog");
   check_cuda(cudaMalloc(&enc.pow5, s * sizeof(int32_t)), "alloc pow5");
   check_cuda(cudaMalloc(&enc.overflow, sizeof(int)), "alloc flag");
+  check_cuda(cudaMalloc(&enc.eroot, er.size() * sizeof(double2)), "alloc roots");
+  check_cuda(cudaMemcpy(enc.eroot, er.data(), er.size() * sizeof(double2),
+                        cudaMemcpyHostToDevice), "roots");
   check_cuda(cudaMemcpy(enc.dlog, dl.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice), "dlog");
   check_cuda(cudaMemcpy(enc.pow5, pw.data(), s * sizeof(int32_t), cudaMemcpyHostToDevice), "pow5");
   check_cuda(cudaMemset(enc.overflow, 0, sizeof(int)), "flag");
@@ -215,6 +220,7 @@ void launch_encode_diags(Ring& R, int kind, int half, double fold, double scale,
     P.scale = scale;
     P.dlog = T.dlog;
     P.pow5 = T.pow5;
+    P.eroot = T.eroot;
     P.y = scratch;
     P.out = out + (size_t)c0 * n;
     P.overflow = T.overflow;

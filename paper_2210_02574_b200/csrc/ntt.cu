@@ -288,7 +288,8 @@ constexpr size_t blocks_r_smem() {
 
 // CM: first-pass input -- 0 plain load, 1 centered lift of one limb
 // (rescale / ModRaise), 2 fast basis conversion, 3 conversion of the centered
-// representative (ModDown by q_l * P).  Compile-time so each variant carries
+// representative (ModDown by q_l * P), 4 signed int64 coefficients
+// (limbs_from_signed, ring.py:381-387: encoded plaintexts).  Compile-time so each variant carries
 // only its own prologue.
 template <int LOGS, bool INV, int CM>
 __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MINB) * kRegMinBlocks) k_ntt_cols_r(const __grid_constant__ NttParams P) {
@@ -344,7 +345,13 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
     const uint64_t* src = INV ? (sg.out + poly * sg.out_stride + (size_t)limb * N)
                               : (sg.in + poly * sg.in_stride + (size_t)limb * N);
     uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
-    if constexpr (CM == 1) {
+    if constexpr (CM == 4) {
+      const int64_t* hs = reinterpret_cast<const int64_t*>(sg.csrc + poly * sg.csrc_stride);
+      for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+        const int r = e / kRegWarps, c = e % kRegWarps;
+        tile[tix(r, c)] = signed_mod(__ldg(hs + c0 + c + (size_t)C * r), pc);
+      }
+    } else if constexpr (CM == 1) {
       // fused centered lift: v = src > q_s/2 ? src - q_s : src, then mod q
       const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
       const uint64_t qs = sg.csrc_q;
@@ -606,7 +613,11 @@ static int cols_mode(const NttParams& P) {
   int cm = -1;
   for (int g = 0; g < P.S.n_seg; ++g) {
     const Seg& sg = P.S.seg[g];
-    const int m = sg.csrc == nullptr ? 0 : sg.cmode == 1 ? 1 : sg.cmode == 2 ? 3 : 2;
+    const int m = sg.csrc == nullptr ? 0
+                  : sg.cmode == 1   ? 1
+                  : sg.cmode == 2   ? 3
+                  : sg.cmode == 3   ? 4
+                                    : 2;
     if (cm >= 0 && m != cm) throw HegpuError{HEGPU_E_ARG, "NTT segments mix prologue modes"};
     cm = m;
   }
@@ -626,6 +637,7 @@ static void launch_cols_r(bool inverse, const NttParams& P, int n_units, int log
     case 1: launch_cols_r_cm<LOGS, false, 1>(P, grid, st); break;
     case 2: launch_cols_r_cm<LOGS, false, 2>(P, grid, st); break;
     case 3: launch_cols_r_cm<LOGS, false, 3>(P, grid, st); break;
+    case 4: launch_cols_r_cm<LOGS, false, 4>(P, grid, st); break;
     default: launch_cols_r_cm<LOGS, false, 0>(P, grid, st); break;
   }
 }

@@ -205,6 +205,7 @@ Ring::~Ring() {
   if (enc.dlog) cudaFree(enc.dlog);
   if (enc.pow5) cudaFree(enc.pow5);
   if (enc.overflow) cudaFree(enc.overflow);
+  if (enc.eroot) cudaFree(enc.eroot);
 }
 
 static uint64_t prod_mod(const std::vector<uint64_t>& ps, int skip, uint64_t m) {
@@ -1360,6 +1361,26 @@ static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* ou
   ntt_simple(R, false, out, os, out, os, P, to_level + 1, chain.data(), st);
 }
 
+// Eval-form limbs of signed int64 coefficient rows: lift (np.mod into every
+// limb) fused into the forward NTT's first pass.
+void ntt_from_signed(Ring& R, const int64_t* src, int64_t ss, uint64_t* out, int64_t os, int P,
+                     int k, const int32_t* primes, cudaStream_t st) {
+  if (P <= 0 || k <= 0) return;
+  if (R.log_n >= 12) {
+    SegSet S;
+    S.n_seg = 0;
+    S.n_rows = 0;
+    add_seg(S, nullptr, 0, out, os, P, k, primes);
+    S.seg[0].csrc = reinterpret_cast<const uint64_t*>(src);
+    S.seg[0].csrc_stride = ss;
+    S.seg[0].cmode = 3;
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    return;
+  }
+  launch_lift_signed(R.dpc, R.log_n, src, ss, out, os, P, k, primes, st);
+  ntt_simple(R, false, out, os, out, os, P, k, primes, st);
+}
+
 // --- host-array kernel-table shims (hebert._kernels) -----------------------
 
 struct DevBuf {
@@ -1628,6 +1649,18 @@ int hegpu_encode_diags(hegpu_ring_t ring, int kind, int half, double fold, doubl
     Ring& R = RR(ring);
     launch_encode_diags(R, kind, half, fold, scale, n_diags, d, g0, conj,
                         static_cast<double2*>(scratch), out, S_(stream));
+  })
+}
+
+int hegpu_ntt_from_signed(hegpu_ring_t ring, const int64_t* src, int64_t src_stride,
+                          uint64_t* out, int64_t out_stride, int n_polys, int k,
+                          const int32_t* primes, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    for (int l = 0; l < k; ++l)
+      if (primes[l] < 0 || primes[l] >= R.n_primes)
+        throw HegpuError{HEGPU_E_ARG, "prime index out of range"};
+    ntt_from_signed(R, src, src_stride, out, out_stride, n_polys, k, primes, S_(stream));
   })
 }
 

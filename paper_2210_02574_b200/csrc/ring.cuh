@@ -50,6 +50,7 @@ struct EncTables {
   int32_t* dlog = nullptr;  // spectrum index -> slot | (conj << 30)
   int32_t* pow5 = nullptr;  // 5^j mod 2N
   int* overflow = nullptr;  // sticky |coefficient| >= 2^62 flag
+  double2* eroot = nullptr; // exp(i pi e / N), e < 2N
 };
 constexpr int kEncMaxDiags = 256;  // diagonals per encode launch (kernel parameter space)
 
