@@ -19,6 +19,9 @@
 // N = 2^16 is 16 tiles, so every launch has (16 x limbs x polys) CTAs.
 // Intermediate values stay in Harvey lazy ranges ([0,4q) forward, [0,2q)
 // inverse); outputs are fully reduced.
+#include <mutex>
+#include <vector>
+
 #include "ntt_reg.cuh"
 #include "ring.cuh"
 
@@ -255,12 +258,6 @@ constexpr int kRegMinBlocks = 8 / kRegWarps;  // scales the launch bounds below
 #define HEGPU_NTT_PPB 4
 #endif
 constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
-// HEGPU_NTT_PAIR=2: the block pass runs two polys of a limb per warp in
-// lockstep (2x ILP); measured no faster (the pipes, not latency, bound it)
-#ifndef HEGPU_NTT_PAIR
-#define HEGPU_NTT_PAIR 1
-#endif
-constexpr int kNttPair = HEGPU_NTT_PAIR;
 // conversion prologue: up to this many source limbs take the unrolled path
 // (all source words of a coefficient in flight at once)
 constexpr int kConvMaxSrc = 8;
@@ -270,6 +267,39 @@ constexpr int kConvMaxSrc = 8;
 #ifndef HEGPU_COLS_MINB
 #define HEGPU_COLS_MINB 5
 #endif
+
+// slot -> (st << 16 | local) of TwLayout<6 + li, inv>, filled once by the host
+// (the staging loops then do one table read per twiddle instead of a decode)
+__device__ int32_t g_tw_slot[2][4][512];
+
+template <int LOGS, bool INV>
+__device__ __forceinline__ int tw_slot_index(int i, int blk_shift_base) {
+  const int code = g_tw_slot[INV][LOGS - 6][i];
+  const int st = code >> 16, local = code & 0xffff;
+  return (1 << (blk_shift_base + st)) + local;
+}
+
+template <int LOGS, bool INV>
+static void fill_tw_slots(std::vector<int32_t>& h) {
+  for (int i = 0; i < (1 << LOGS) - 1; ++i) {
+    int st, local;
+    TwLayout<LOGS, INV>::decode(i, st, local);
+    h[((INV ? 1 : 0) * 4 + (LOGS - 6)) * 512 + i] = (st << 16) | local;
+  }
+}
+
+void ensure_tw_slots() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    std::vector<int32_t> h(2 * 4 * 512, 0);
+    fill_tw_slots<6, false>(h); fill_tw_slots<7, false>(h);
+    fill_tw_slots<8, false>(h); fill_tw_slots<9, false>(h);
+    fill_tw_slots<6, true>(h); fill_tw_slots<7, true>(h);
+    fill_tw_slots<8, true>(h); fill_tw_slots<9, true>(h);
+    check_cuda(cudaMemcpyToSymbol(g_tw_slot, h.data(), h.size() * sizeof(int32_t)),
+               "twiddle slot table");
+  });
+}
 
 // Shared memory of the register passes (bytes): the cols pass holds its
 // S x 8 tile, the warp buffers and the S twiddle pairs of stages [0, LOGS);
@@ -282,7 +312,7 @@ constexpr size_t cols_r_smem() {
 }
 template <int LOGS>
 constexpr size_t blocks_r_smem() {
-  return (size_t)kNttPair * kRegWarps * RegShape<LOGS>::PAD_S * 8 +
+  return (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8 +
          (size_t)kRegWarps * (1 << LOGS) * 16;
 }
 
@@ -321,8 +351,10 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
   const bool fpp = pc.twf != nullptr;
   const ulonglong2* tws =
       fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + (INV ? N : 0)) : tw;
-  // every column transform of this pass uses twiddles [1, S) of its table
-  for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(stw + tw_sw(i), tws + i);
+  // every column transform of this pass uses twiddles [1, S) of its table,
+  // staged in consumption order (TwLayout)
+  for (int i = threadIdx.x; i < S - 1; i += blockDim.x)
+    cp_async16(stw + i, tws + tw_slot_index<LOGS, INV>(i, 0));
   // conversion constants of this target limb: punc[i], fp32 weight, shift
   uint64_t* s_conv = reinterpret_cast<uint64_t*>(stw + S);
   const int nsrc = CM >= 2 ? sg.c_nsrc : 0;
@@ -430,30 +462,29 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = tile[tix(reg_j(lane, e, LO_S, EB), warp)];
     if (fpp) {
-      // forward: [0, q) in, signed lazy intermediate out; inverse: the
-      // signed intermediate in, fully reduced out
+      // forward: [0, q) in, lazy double intermediate (raw bits) out; inverse:
+      // the double intermediate in, fully reduced out
       const double qd = (double)pc.q, qinv = 1.0 / qd;
       double xf[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) xf[e] = fp_from_s64(x[e]);
+      for (int e = 0; e < E; ++e) xf[e] = INV ? __longlong_as_double(x[e]) : fp_from_s64(x[e]);
       const double2* stwf = reinterpret_cast<const double2*>(stw);
       double* wbf = reinterpret_cast<double*>(wbuf);
       if (!INV) {
-        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, 0, 0, stwf, qd);
+        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, stwf, qd);
 #pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = fp_to_s64(xf[e]);
+        for (int e = 0; e < E; ++e) x[e] = __double_as_longlong(xf[e]);
       } else {
         const double2 fsf = make_double2((double)fs.x, (double)fs.x / qd);
         const double2 fdf = make_double2((double)fd.x, (double)fd.x / qd);
-        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stwf, qd, qinv, fsf,
-                         fdf);
+        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, LOGS - 1, stwf, qd, qinv, fsf, fdf);
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = fp_to_residue_small(xf[e], qd);
       }
     } else if (!INV)
-      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, 0, 0, stw, pc.q);
+      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, stw, pc.q);
     else
-      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, log_n, log_n - LOGS, 0, stw, pc, fs, fd);
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS - 1, stw, pc, fs, fd);
 #pragma unroll
     for (int e = 0; e < E; ++e) tile[tix(reg_j(lane, e, LO_S, EB), warp)] = x[e];
     __syncthreads();
@@ -466,7 +497,7 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
 }
 
 template <int LOGS, bool INV>
-__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 2 ? 3 : HEGPU_BLOCKS_MINB)) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_BLOCKS_MINB) * kRegMinBlocks) k_ntt_blocks_r(const __grid_constant__ NttParams P) {
   using Sh = RegShape<LOGS>;
   constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
   extern __shared__ uint64_t sm[];
@@ -484,20 +515,21 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
   const int blk = blockIdx.x * kRegWarps + warp;
   const size_t off = (size_t)limb * N + (size_t)blk * S;
   uint64_t* wbuf = sm + warp * Sh::PAD_S;
-  uint64_t* wbuf2 = sm + (kRegWarps * (kNttPair - 1) + warp) * Sh::PAD_S;  // paired polys
-  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kNttPair * kRegWarps * Sh::PAD_S);
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(sm + kRegWarps * Sh::PAD_S);
   constexpr int LO_S = LOGS - EB;
   const bool fpp = pc.twf != nullptr;  // FP64 path (common.cuh)
   {
     const ulonglong2* tws =
         fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + (INV ? N : 0)) : tw;
-    // stage st of blocks [blk0, blk0 + W) uses global twiddles
-    // (1 << (a + st)) + (blk0 << st) + [0, W << st)  ->  smem (W << st) + ...
+    // warp w's sub-transform (block blk0 + w) uses global twiddles
+    // (1 << (a + st)) + ((blk0 + w) << st) + local, staged per warp in
+    // consumption order (TwLayout): smem run w * (S - 1) + slot
     const int blk0 = blockIdx.x * kRegWarps;
-    for (int v = kRegWarps + threadIdx.x; v < kRegWarps * S; v += blockDim.x) {
-      const int st = 31 - __clz(v) - kRegWarpsLog;
-      const int i = v - (kRegWarps << st);
-      cp_async16(stw + tw_sw(v), tws + (1 << (a + st)) + (blk0 << st) + i);
+    for (int v = threadIdx.x; v < kRegWarps * (S - 1); v += blockDim.x) {
+      const int w = v / (S - 1), i = v - w * (S - 1);
+      const int code = g_tw_slot[INV][LOGS - 6][i];
+      const int st = code >> 16, local = code & 0xffff;
+      cp_async16(stw + v, tws + (1 << (a + st)) + ((blk0 + w) << st) + local);
     }
   }
   const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;
@@ -543,55 +575,40 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : (kNttPair == 
   // last-stage scaling is never in this pass)
   const ulonglong2 fs = make_ulonglong2(pc.ninv, pc.ninv_sh);
   const ulonglong2 fd = make_ulonglong2(pc.ilast, pc.ilast_sh);
-  uint64_t x[E], x2[E];
-  int step = 1;
+  const ulonglong2* tab = stw + warp * (S - 1);  // this warp's consumption-order run
+  uint64_t x[E];
 #pragma unroll 1
-  for (int pi = 0; pi < U.np; pi += step) {
-    const bool pair = kNttPair == 2 && pi + 1 < U.np && !fpp;
-    step = pair ? 2 : 1;
+  for (int pi = 0; pi < U.np; ++pi) {
     load(x, U.p0 + pi);
-    if (pair) load(x2, U.p0 + pi + 1);
     if (pi == 0) {
       cp_async_wait_all();
       __syncthreads();
     }
-    if (pair) {
-      // two polys of this limb in lockstep: shared twiddles, 2x ILP
-      if (!INV)
-        fwd_sub2<LOGS>(x, x2, wbuf, wbuf2, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
-      else
-        inv_sub2<LOGS>(x, x2, wbuf, wbuf2, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw,
-                       pc, fs, fd);
-      finish(x, U.p0 + pi);
-      finish(x2, U.p0 + pi + 1);
-    } else if (fpp) {
-      // forward: signed intermediate in, fully reduced out; inverse: [0, q)
-      // in, signed intermediate (|x| < q) out
+    if (fpp) {
+      // forward: double intermediate (raw bits) in, fully reduced out;
+      // inverse: [0, q) in, double intermediate (|x| < q) out
       const double qd = (double)q, qinv = 1.0 / qd;
       double xf[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) xf[e] = fp_from_s64(x[e]);
-      const double2* stwf = reinterpret_cast<const double2*>(stw);
+      for (int e = 0; e < E; ++e) xf[e] = INV ? fp_from_s64(x[e]) : __longlong_as_double(x[e]);
+      const double2* tabf = reinterpret_cast<const double2*>(tab);
       double* wbf = reinterpret_cast<double*>(wbuf);
       if (!INV) {
-        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, kRegWarpsLog, warp, stwf, qd);
+        fwd_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, tabf, qd);
 #pragma unroll
         for (int e = 0; e < E; ++e) x[e] = fp_to_residue(xf[e], qd, qinv);
       } else {
         const double2 one = make_double2(1.0, 1.0 / qd);  // never used: no final stage here
-        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stwf, qd, qinv,
-                         one, one);
+        inv_sub_fp<LOGS>(xf, wbf, lane, LO_S, LO_S, -1, tabf, qd, qinv, one, one);
 #pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = fp_to_s64(xf[e]);
+        for (int e = 0; e < E; ++e) x[e] = __double_as_longlong(xf[e]);
       }
-      finish(x, U.p0 + pi);
+    } else if (!INV) {
+      fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, tab, q);
     } else {
-      if (!INV)
-        fwd_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, kRegWarpsLog, warp, stw, q);
-      else
-        inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS + kRegWarpsLog, 0, warp, stw, pc, fs, fd);
-      finish(x, U.p0 + pi);
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, -1, tab, pc, fs, fd);
     }
+    finish(x, U.p0 + pi);
   }
 }
 
@@ -695,8 +712,13 @@ static inline int ilog2(int x) {
 }
 
 void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inverse,
-                SegSet& S, const NttEpilogue* epi, cudaStream_t st) {
+                SegSet& S, const NttEpilogue* epi, cudaStream_t st, const uint64_t* fp_mask) {
+  // one kernel per pass serves both arithmetic classes (a per-CTA uniform
+  // branch on PrimeConst::twf): measured faster than a launch per class,
+  // whose integer-limb launches are too small to fill the GPU
+  (void)fp_mask;
   if (S.n_rows == 0) return;
+  ensure_tw_slots();
   if (S.n_rows > 65535) throw HegpuError{1, "NTT batch exceeds 65535 limbs"};
   NttParams local;
   local.S = S;

@@ -13,10 +13,10 @@
 // (hebert/_kernels.py:152-203) expressed in global stage/group terms, so the
 // output is bit-identical to the CT/GS transforms.
 //
-// The kernels stage the twiddles a CTA needs in shared memory first (the
-// round functions index `tw` with the same formulas, on a re-based table),
-// so the butterflies' twiddle reads are shared-memory loads instead of
-// long-latency global loads on the dependency chain.
+// The kernels stage the twiddles a CTA needs in shared memory first, in the
+// order the lanes consume them (TwLayout), so the butterflies' twiddle reads
+// are shared-memory loads at compile-time offsets instead of long-latency
+// global loads on the dependency chain.
 #pragma once
 #include "common.cuh"
 
@@ -47,36 +47,89 @@ __device__ __forceinline__ int shf_idx(int j) {
   else
     return padi(j);
 }
-// shared-memory slot of staged twiddle i (16-byte entries, served per quarter
-// warp): late stages read twiddles at a lane stride of 2..8 entries, which the
-// swizzle spreads over the 8 bank groups (4x fewer wavefronts at stride 4)
-__device__ __forceinline__ int tw_sw(int i) { return i ^ ((i >> 3) & 7); }
 
 
-// Forward CT butterflies on register window [lo, lo+EB) for bit positions
-// p = phi down to plo (t = 2^p within the sub-transform).  Twiddle index of
-// the butterfly whose lower element is j at local stage st (t = 2^(LOGS-1-st))
-// is tw_base(st) + (j >> (p + 1)), tw_base(st) = (1 << (g0 + st)) + (blk << st).
-template <int LOGS>
-__device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
-                                          int phi, int plo, int g0, int blk,
+// ---------------------------------------------------------------------------
+// Twiddles in consumption order.  Round r of a sub-transform works on register
+// window [lo, lo + EB); its butterfly at bit p (lower element j) uses twiddle
+// tree index (1 << st) + (j >> (p + 1)), st = LOGS - 1 - p, and
+//   j >> (p + 1) = (e >> (p + 1 - lo)) | (g << (lo + EB - p - 1)),  g = lane >> lo,
+// so a lane's twiddles of a round depend only on its group g.  The CTA stages
+// them (once) as [round][group][stage][u]: a lane then reads its round's
+// twiddles from one base address with compile-time offsets (no per-butterfly
+// index arithmetic), and the 8 lanes of a quarter warp with distinct groups
+// read slots cnt(r) apart, which spreads them over the bank groups.
+// ---------------------------------------------------------------------------
+template <int LOGS, bool INV>
+struct TwLayout {
+  static constexpr int EB = LOGS - 5, E = 1 << EB, R = (LOGS + EB - 1) / EB;
+  static constexpr int plo(int r) {
+    return INV ? r * EB : (LOGS - 1 - r * EB - EB + 1 < 0 ? 0 : LOGS - r * EB - EB);
+  }
+  static constexpr int phi(int r) {
+    return INV ? (r * EB + EB - 1 > LOGS - 1 ? LOGS - 1 : r * EB + EB - 1) : LOGS - 1 - r * EB;
+  }
+  static constexpr int lo(int r) {
+    return INV ? (r * EB + EB > LOGS ? LOGS - EB : r * EB)
+               : (LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB);
+  }
+  // distinct twiddles per group at bit p of round r
+  static constexpr int kp(int r, int p) { return E >> (p + 1 - lo(r)); }
+  static constexpr int cnt(int r) {
+    int c = 0;
+    for (int p = plo(r); p <= phi(r); ++p) c += kp(r, p);
+    return c;
+  }
+  // offset of bit p inside a group's run (stages in execution order)
+  static constexpr int pre(int r, int p) {
+    int c = 0;
+    if (INV) {
+      for (int q = plo(r); q < p; ++q) c += kp(r, q);
+    } else {
+      for (int q = phi(r); q > p; --q) c += kp(r, q);
+    }
+    return c;
+  }
+  static constexpr int groups(int r) { return 32 >> lo(r); }
+  static constexpr int off(int r) {
+    int c = 0;
+    for (int q = 0; q < r; ++q) c += groups(q) * cnt(q);
+    return c;
+  }
+  static constexpr int total() { return off(R); }  // == S - 1
+  // slot -> (st, local index within the stage); host/device, any slot < total()
+  __host__ __device__ static void decode(int s, int& st, int& local) {
+    int r = 0;
+    while (r + 1 < R && s >= off(r + 1)) ++r;
+    const int rel = s - off(r), g = rel / cnt(r);
+    int rem = rel - g * cnt(r);
+    int p = INV ? plo(r) : phi(r);
+    while (rem >= kp(r, p)) {
+      rem -= kp(r, p);
+      p += INV ? 1 : -1;
+    }
+    st = LOGS - 1 - p;
+    local = rem | (g << (lo(r) + EB - p - 1));
+  }
+};
+
+// Forward CT butterflies of round r (bits phi down to plo); tw = this lane's
+// twiddle run of the round.
+template <int LOGS, int r>
+__device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E],
                                           const ulonglong2* __restrict__ tw, uint64_t q) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  using L = TwLayout<LOGS, false>;
+  constexpr int E = RegShape<LOGS>::E, lo = L::lo(r);
   const uint64_t q2 = q << 1;
 #pragma unroll
-  for (int p = LOGS - 1; p >= 0; --p) {
-    if (p > phi || p < plo) continue;
-    const int st = LOGS - 1 - p;
+  for (int p = L::phi(r); p >= L::plo(r); --p) {
     const int d = 1 << (p - lo);
-    const int base = (1 << (g0 + st)) + (blk << st);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & d) continue;
-      const int j = reg_j(lane, e, lo, EB);
-      const int ti = base + (j >> (p + 1));
       uint64_t u = x[e];
       u = u >= q2 ? u - q2 : u;
-      const ulonglong2 wp = tw[tw_sw(ti)];
+      const ulonglong2 wp = tw[L::pre(r, p) + (e >> (p + 1 - lo))];
       const uint64_t v = shoup_lazy(x[e + d], wp.x, wp.y, q);
       x[e] = u + v;
       x[e + d] = u - v + q2;
@@ -84,26 +137,22 @@ __device__ __forceinline__ void fwd_round(uint64_t (&x)[RegShape<LOGS>::E], int 
   }
 }
 
-// Inverse GS butterflies for bit positions p = plo up to phi.  Twiddle index
-// is hbase(p) + (blk << (LOGS - p - 1)) + (j >> (p + 1)) with
-// hbase(p) = N >> (gshift + p + 1), gshift the global bit offset of this pass.
-// The final stage (global t = N/2) multiplies the sum by fin_s and the
-// difference by fin_d: (N^-1, ipsi_rev[1] N^-1), optionally times a per-limb
-// post-scale (the ModUp / ModDown punctured-product inverse).
-template <int LOGS>
-__device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int lane, int lo,
-                                          int plo, int phi, int log_n, int gshift, int blk,
-                                          const ulonglong2* __restrict__ tw,
+// Inverse GS butterflies of round r (bits plo up to phi).  The final stage
+// (global t = N/2, `last_p` = its bit, -1 if not in this pass) multiplies the
+// sum by fin_s and the difference by fin_d: (N^-1, ipsi_rev[1] N^-1),
+// optionally times a per-limb post-scale (ModUp / ModDown).
+template <int LOGS, int r>
+__device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E],
+                                          const ulonglong2* __restrict__ tw, int last_p,
                                           const PrimeConst& pc, const ulonglong2 fin_s,
                                           const ulonglong2 fin_d) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  using L = TwLayout<LOGS, true>;
+  constexpr int E = RegShape<LOGS>::E, lo = L::lo(r);
   const uint64_t q = pc.q, q2 = q << 1;
 #pragma unroll
-  for (int p = 0; p < LOGS; ++p) {
-    if (p < plo || p > phi) continue;
+  for (int p = L::plo(r); p <= L::phi(r); ++p) {
     const int d = 1 << (p - lo);
-    const bool last = (gshift + p == log_n - 1);
-    const int base = (1 << (log_n - gshift - p - 1)) + (blk << (LOGS - p - 1));
+    const bool last = p == last_p;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & d) continue;
@@ -112,10 +161,8 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E], int 
       s = s >= q2 ? s - q2 : s;
       const uint64_t df = a - b + q2;
       if (!last) {
-        const int j = reg_j(lane, e, lo, EB);
-        const int ti = base + (j >> (p + 1));
         x[e] = s;
-        const ulonglong2 wp = tw[tw_sw(ti)];
+        const ulonglong2 wp = tw[L::pre(r, p) + (e >> (p + 1 - lo))];
         x[e + d] = shoup_lazy(df, wp.x, wp.y, q);
       } else {
         x[e] = shoup(s, fin_s.x, fin_s.y, q);
@@ -139,111 +186,57 @@ __device__ __forceinline__ void reg_shuffle(T (&x)[RegShape<LOGS>::E], T* buf,
   __syncwarp();
 }
 
-// Full S-point forward sub-transform in registers; input layout window
-// lo_in, output layout window lo_out.
+// lane's twiddle run of round r in the staged table
+template <int LOGS, bool INV, int r, typename TW>
+__device__ __forceinline__ const TW* tw_run(const TW* tab, int lane) {
+  using L = TwLayout<LOGS, INV>;
+  return tab + L::off(r) + (lane >> L::lo(r)) * L::cnt(r);
+}
+
+template <int LOGS, int r = 0>
+__device__ __forceinline__ void fwd_rounds(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+                                           int lane, int cur, const ulonglong2* tab, uint64_t q,
+                                           int lo_out) {
+  using L = TwLayout<LOGS, false>;
+  if constexpr (r < L::R) {
+    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    fwd_round<LOGS, r>(x, tw_run<LOGS, false, r>(tab, lane), q);
+    fwd_rounds<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, q, lo_out);
+  } else {
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+  }
+}
+
+template <int LOGS, int r = 0>
+__device__ __forceinline__ void inv_rounds(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
+                                           int lane, int cur, const ulonglong2* tab, int last_p,
+                                           const PrimeConst& pc, const ulonglong2 fin_s,
+                                           const ulonglong2 fin_d, int lo_out) {
+  using L = TwLayout<LOGS, true>;
+  if constexpr (r < L::R) {
+    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    inv_round<LOGS, r>(x, tw_run<LOGS, true, r>(tab, lane), last_p, pc, fin_s, fin_d);
+    inv_rounds<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, last_p, pc, fin_s, fin_d, lo_out);
+  } else {
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+  }
+}
+
+// Full S-point sub-transforms in registers; input / output layout windows
+// lo_in / lo_out; tab = the staged consumption-order twiddles (TwLayout).
 template <int LOGS>
 __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
-                                        int lane, int lo_in, int lo_out, int g0, int blk,
-                                        const ulonglong2* tw, uint64_t q) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int phi = LOGS - 1 - r * EB;
-    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
-    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
-    cur = lo;
-    fwd_round<LOGS>(x, lane, lo, phi, plo, g0, blk, tw, q);
-  }
-  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+                                        int lane, int lo_in, int lo_out, const ulonglong2* tab,
+                                        uint64_t q) {
+  fwd_rounds<LOGS>(x, buf, lane, lo_in, tab, q, lo_out);
 }
 
 template <int LOGS>
 __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
-                                        int lane, int lo_in, int lo_out, int log_n, int gshift,
-                                        int blk, const ulonglong2* tw, const PrimeConst& pc,
+                                        int lane, int lo_in, int lo_out, int last_p,
+                                        const ulonglong2* tab, const PrimeConst& pc,
                                         const ulonglong2 fin_s, const ulonglong2 fin_d) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int plo = r * EB;
-    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
-    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
-    cur = lo;
-    inv_round<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
-  }
-  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
-}
-
-// Two independent sub-transforms in lockstep (the same twiddles: the same
-// limb of two polys): each round runs both register sets back to back so the
-// scheduler interleaves two independent butterfly streams (2x ILP), and the
-// two re-distributions share one pair of __syncwarp.
-template <int LOGS>
-__device__ __forceinline__ void reg_shuffle2(uint64_t (&x0)[RegShape<LOGS>::E],
-                                             uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
-                                             uint64_t* b1, int lane, int lo_from, int lo_to) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
-  if (lo_from == lo_to) return;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int j = shf_idx<LOGS>(reg_j(lane, e, lo_from, EB));
-    b0[j] = x0[e];
-    b1[j] = x1[e];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int j = shf_idx<LOGS>(reg_j(lane, e, lo_to, EB));
-    x0[e] = b0[j];
-    x1[e] = b1[j];
-  }
-  __syncwarp();
-}
-
-template <int LOGS>
-__device__ __forceinline__ void fwd_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
-                                         uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
-                                         uint64_t* b1, int lane, int lo_in, int lo_out, int g0,
-                                         int blk, const ulonglong2* tw, uint64_t q) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int phi = LOGS - 1 - r * EB;
-    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
-    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
-    reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo);
-    cur = lo;
-    fwd_round<LOGS>(x0, lane, lo, phi, plo, g0, blk, tw, q);
-    fwd_round<LOGS>(x1, lane, lo, phi, plo, g0, blk, tw, q);
-  }
-  reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo_out);
-}
-
-template <int LOGS>
-__device__ __forceinline__ void inv_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
-                                         uint64_t (&x1)[RegShape<LOGS>::E], uint64_t* b0,
-                                         uint64_t* b1, int lane, int lo_in, int lo_out, int log_n,
-                                         int gshift, int blk, const ulonglong2* tw,
-                                         const PrimeConst& pc, const ulonglong2 fin_s,
-                                         const ulonglong2 fin_d) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int plo = r * EB;
-    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
-    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
-    reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo);
-    cur = lo;
-    inv_round<LOGS>(x0, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
-    inv_round<LOGS>(x1, lane, lo, plo, phi, log_n, gshift, blk, tw, pc, fin_s, fin_d);
-  }
-  reg_shuffle2<LOGS>(x0, x1, b0, b1, lane, cur, lo_out);
+  inv_rounds<LOGS>(x, buf, lane, lo_in, tab, last_p, pc, fin_s, fin_d, lo_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -254,22 +247,18 @@ __device__ __forceinline__ void inv_sub2(uint64_t (&x0)[RegShape<LOGS>::E],
 // Inverse GS: the sum doubles per stage, so it is centred-reduced after every
 // 4th stage and at the end of a non-final pass (bound <= 16 q < 2^50).
 // ---------------------------------------------------------------------------
-template <int LOGS>
-__device__ __forceinline__ void fwd_round_fp(double (&x)[RegShape<LOGS>::E], int lane, int lo,
-                                             int phi, int plo, int g0, int blk,
+template <int LOGS, int r>
+__device__ __forceinline__ void fwd_round_fp(double (&x)[RegShape<LOGS>::E],
                                              const double2* __restrict__ tw, double q) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  using L = TwLayout<LOGS, false>;
+  constexpr int E = RegShape<LOGS>::E, lo = L::lo(r);
 #pragma unroll
-  for (int p = LOGS - 1; p >= 0; --p) {
-    if (p > phi || p < plo) continue;
-    const int st = LOGS - 1 - p;
+  for (int p = L::phi(r); p >= L::plo(r); --p) {
     const int d = 1 << (p - lo);
-    const int base = (1 << (g0 + st)) + (blk << st);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & d) continue;
-      const int j = reg_j(lane, e, lo, EB);
-      const double2 wp = tw[tw_sw(base + (j >> (p + 1)))];
+      const double2 wp = tw[L::pre(r, p) + (e >> (p + 1 - lo))];
       const double v = fp_mulmod(x[e + d], wp.x, wp.y, q);
       const double u = x[e];
       x[e] = u + v;
@@ -278,29 +267,26 @@ __device__ __forceinline__ void fwd_round_fp(double (&x)[RegShape<LOGS>::E], int
   }
 }
 
-template <int LOGS>
-__device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E], int lane, int lo,
-                                             int plo, int phi, int log_n, int gshift, int blk,
-                                             const double2* __restrict__ tw, double q,
-                                             double qinv, const double2 fin_s,
+template <int LOGS, int r>
+__device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E],
+                                             const double2* __restrict__ tw, int last_p,
+                                             double q, double qinv, const double2 fin_s,
                                              const double2 fin_d) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
+  using L = TwLayout<LOGS, true>;
+  constexpr int E = RegShape<LOGS>::E, lo = L::lo(r);
 #pragma unroll
-  for (int p = 0; p < LOGS; ++p) {
-    if (p < plo || p > phi) continue;
+  for (int p = L::plo(r); p <= L::phi(r); ++p) {
     const int d = 1 << (p - lo);
-    const bool last = (gshift + p == log_n - 1);
+    const bool last = p == last_p;
     const bool red = (p & 3) == 3 || p == LOGS - 1;
-    const int base = (1 << (log_n - gshift - p - 1)) + (blk << (LOGS - p - 1));
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e & d) continue;
       const double a = x[e], b = x[e + d];
-      double s = a + b;
+      const double s = a + b;
       const double df = a - b;
       if (!last) {
-        const int j = reg_j(lane, e, lo, EB);
-        const double2 wp = tw[tw_sw(base + (j >> (p + 1)))];
+        const double2 wp = tw[L::pre(r, p) + (e >> (p + 1 - lo))];
         x[e] = red ? fp_reduce(s, q, qinv) : s;
         x[e + d] = fp_mulmod(df, wp.x, wp.y, q);
       } else {
@@ -311,41 +297,48 @@ __device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E], int
   }
 }
 
+template <int LOGS, int r = 0>
+__device__ __forceinline__ void fwd_rounds_fp(double (&x)[RegShape<LOGS>::E], double* buf,
+                                              int lane, int cur, const double2* tab, double q,
+                                              int lo_out) {
+  using L = TwLayout<LOGS, false>;
+  if constexpr (r < L::R) {
+    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    fwd_round_fp<LOGS, r>(x, tw_run<LOGS, false, r>(tab, lane), q);
+    fwd_rounds_fp<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, q, lo_out);
+  } else {
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+  }
+}
+
+template <int LOGS, int r = 0>
+__device__ __forceinline__ void inv_rounds_fp(double (&x)[RegShape<LOGS>::E], double* buf,
+                                              int lane, int cur, const double2* tab, int last_p,
+                                              double q, double qinv, const double2 fin_s,
+                                              const double2 fin_d, int lo_out) {
+  using L = TwLayout<LOGS, true>;
+  if constexpr (r < L::R) {
+    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    inv_round_fp<LOGS, r>(x, tw_run<LOGS, true, r>(tab, lane), last_p, q, qinv, fin_s, fin_d);
+    inv_rounds_fp<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, last_p, q, qinv, fin_s, fin_d,
+                               lo_out);
+  } else {
+    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+  }
+}
+
 template <int LOGS>
 __device__ __forceinline__ void fwd_sub_fp(double (&x)[RegShape<LOGS>::E], double* buf, int lane,
-                                           int lo_in, int lo_out, int g0, int blk,
-                                           const double2* tw, double q) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int phi = LOGS - 1 - r * EB;
-    const int plo = phi - EB + 1 < 0 ? 0 : phi - EB + 1;
-    const int lo = LOGS - (r + 1) * EB < 0 ? 0 : LOGS - (r + 1) * EB;
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
-    cur = lo;
-    fwd_round_fp<LOGS>(x, lane, lo, phi, plo, g0, blk, tw, q);
-  }
-  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+                                           int lo_in, int lo_out, const double2* tab, double q) {
+  fwd_rounds_fp<LOGS>(x, buf, lane, lo_in, tab, q, lo_out);
 }
 
 template <int LOGS>
 __device__ __forceinline__ void inv_sub_fp(double (&x)[RegShape<LOGS>::E], double* buf, int lane,
-                                           int lo_in, int lo_out, int log_n, int gshift, int blk,
-                                           const double2* tw, double q, double qinv,
-                                           const double2 fin_s, const double2 fin_d) {
-  constexpr int EB = RegShape<LOGS>::EB, R = RegShape<LOGS>::ROUNDS;
-  int cur = lo_in;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int plo = r * EB;
-    const int phi = plo + EB - 1 > LOGS - 1 ? LOGS - 1 : plo + EB - 1;
-    const int lo = plo + EB > LOGS ? LOGS - EB : plo;
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo);
-    cur = lo;
-    inv_round_fp<LOGS>(x, lane, lo, plo, phi, log_n, gshift, blk, tw, q, qinv, fin_s, fin_d);
-  }
-  reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+                                           int lo_in, int lo_out, int last_p, const double2* tab,
+                                           double q, double qinv, const double2 fin_s,
+                                           const double2 fin_d) {
+  inv_rounds_fp<LOGS>(x, buf, lane, lo_in, tab, last_p, q, qinv, fin_s, fin_d, lo_out);
 }
 
 }  // namespace hegpu

@@ -390,6 +390,7 @@ static Ring* create_ring(int log_n, const uint64_t* chain, int n_chain, const ui
       if (R->primes[j] == q) throw HegpuError{HEGPU_E_ARG, "duplicate modulus"};
   }
   check_cuda(cudaGetDevice(&R->device), "get device");
+  ensure_tw_slots();
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, R->device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
@@ -404,6 +405,8 @@ static Ring* create_ring(int log_n, const uint64_t* chain, int n_chain, const ui
     R->hpc[i] = make_prime_const(R->primes[i], log_n, t[2 * n + 2]);  // ipsi_rev[1]
   }
   R->dtwf = attach_fp_twiddles(R->hpc, tw.data(), (int)n);
+  for (size_t i = 0; i < R->hpc.size(); ++i)
+    if (R->hpc[i].twf) R->fp_mask |= 1ull << i;
   check_cuda(cudaMalloc(&R->dpc, R->hpc.size() * sizeof(PrimeConst)), "alloc consts");
   check_cuda(cudaMemcpy(R->dpc, R->hpc.data(), R->hpc.size() * sizeof(PrimeConst),
                         cudaMemcpyHostToDevice),
@@ -465,7 +468,7 @@ static void ntt_simple(Ring& R, bool inverse, const uint64_t* in, int64_t is, ui
   S.n_seg = 0;
   S.n_rows = 0;
   add_seg(S, in, is, out, os, n_polys, k, primes);
-  launch_ntt(R.dpc, R.dtw, R.log_n, inverse, S, nullptr, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, inverse, S, nullptr, st, &R.fp_mask);
 }
 
 // --- hybrid key switching (keys.py:278-339) --------------------------------
@@ -493,7 +496,7 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
       E0.fin_s[i] = L.mu_fin_s[i];
       E0.fin_d[i] = L.mu_fin_d[i];
     }
-    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st, &R.fp_mask);
     for (int j0 = 0; j0 < beta; j0 += kMaxSeg) {
       const int jn = std::min(kMaxSeg, beta - j0);
       SegSet S;
@@ -516,7 +519,7 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
         sg.c_nsrc = g;
         sg.cpunc_ld = n_ext;
       }
-      launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+      launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st, &R.fp_mask);
     }
     return;
   }
@@ -558,7 +561,7 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
         add_seg(S, J.dst, J.dst_stride, J.dst, J.dst_stride, B, n_dst, dsel.data());
     }
     launch_conv(C, st);
-    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st, &R.fp_mask);
   }
 }
 
@@ -623,7 +626,7 @@ static void ks_moddown(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr,
       E0.fin_s[i] = L.md_fin_s[i];
       E0.fin_d[i] = L.md_fin_d[i];
     }
-    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st, &R.fp_mask);
   } else if (K > 0) {
     const std::vector<int32_t> sp = range_primes(R.n_chain, K);
     ntt_simple(R, true, acc + (size_t)k * N, (int64_t)n_ext * N, acc + (size_t)k * N,
@@ -681,7 +684,7 @@ static void ks_moddown(Ring& R, const KsLevel& L, uint64_t* acc, uint64_t* corr,
     E.c[t] = L.pinv[t];
     E.csh[t] = L.pinv_sh[t];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st, &R.fp_mask);
 }
 
 
@@ -705,7 +708,7 @@ static void ks_moddown_polys(Ring& R, const KsLevel& L, uint64_t* in, int64_t is
     E0.fin_s[i] = L.md_fin_s[i];
     E0.fin_d[i] = L.md_fin_d[i];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st, &R.fp_mask);
   const std::vector<int32_t> chain = range_primes(0, k);
   SegSet S;
   S.n_seg = 0;
@@ -727,7 +730,7 @@ static void ks_moddown_polys(Ring& R, const KsLevel& L, uint64_t* in, int64_t is
     E.c[t] = L.pinv[t];
     E.csh[t] = L.pinv_sh[t];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st, &R.fp_mask);
 }
 
 static void ks_ipdown(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds,
@@ -809,7 +812,7 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
     E0.fin_s[i] = L.mdr_fin_s[i];
     E0.fin_d[i] = L.mdr_fin_d[i];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, true, S0, &E0, st, &R.fp_mask);
   const std::vector<int32_t> chain = range_primes(0, level);
   SegSet S;
   S.n_seg = 0;
@@ -843,7 +846,7 @@ static void ks_moddown_rescale(Ring& R, const KsLevel& L, uint64_t* acc, uint64_
     E.s[t] = L.qlinv[t];
     E.ssh[t] = L.qlinv_sh[t];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st, &R.fp_mask);
 }
 
 static void ks_apply_rescale_impl(Ring& R, int level, int alpha, const uint64_t* d, int64_t ds,
@@ -1331,7 +1334,7 @@ static void rescale_impl(Ring& R, int level, const uint64_t* in, int64_t is, uin
     E.c[i] = cs.first[i];
     E.csh[i] = cs.second[i];
   }
-  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st);
+  launch_ntt(R.dpc, R.dtw, R.log_n, false, S, &E, st, &R.fp_mask);
 }
 
 static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* out, int64_t os,
@@ -1353,7 +1356,7 @@ static void mod_raise_impl(Ring& R, const uint64_t* in, int64_t is, uint64_t* ou
     S.seg[0].csrc_stride = (int64_t)N;
     S.seg[0].cmode = 1;
     S.seg[0].csrc_q = R.primes[0];
-    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st, &R.fp_mask);
     return;
   }
   launch_lift_centered(R.dpc, R.log_n, ws.u64(), (int64_t)N, R.primes[0], out, os, P,
@@ -1374,7 +1377,7 @@ void ntt_from_signed(Ring& R, const int64_t* src, int64_t ss, uint64_t* out, int
     S.seg[0].csrc = reinterpret_cast<const uint64_t*>(src);
     S.seg[0].csrc_stride = ss;
     S.seg[0].cmode = 3;
-    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st);
+    launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st, &R.fp_mask);
     return;
   }
   launch_lift_signed(R.dpc, R.log_n, src, ss, out, os, P, k, primes, st);

@@ -62,6 +62,7 @@ struct Ring {
   PrimeConst* dpc = nullptr;
   uint64_t* dtw = nullptr;  // [n_primes][4][N]: psi, psi_sh, ipsi, ipsi_sh
   void* dtwf = nullptr;     // FP64 twiddles of the primes < 2^kFpMaxBits (PrimeConst::twf)
+  uint64_t fp_mask = 0;     // bit p: prime p has FP64 twiddles
   std::mutex mu;
   std::map<std::pair<int, int>, std::unique_ptr<KsLevel>> ks;
   // rescale constants: level -> (q_level^-1 mod q_i, shoup) for i < level
@@ -156,8 +157,14 @@ struct NttEpilogue {
 
 // NTT over a set of segments.  For the forward transform with an epilogue,
 // seg.eout receives (seg.other - NTT(x)) * c[limb] and seg.out is scratch.
+// device tables of the NTT kernels (idempotent; called at ring creation so it
+// never runs inside a stream capture)
+void ensure_tw_slots();
+// fp_mask: bit p set when prime p takes the FP64 path (PrimeConst::twf);
+// nullptr launches both arithmetic variants
 void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inverse,
-                SegSet& S, const NttEpilogue* epi, cudaStream_t st);
+                SegSet& S, const NttEpilogue* epi, cudaStream_t st,
+                const uint64_t* fp_mask = nullptr);
 
 struct EwArgs {
   int op;
