@@ -704,10 +704,12 @@ __device__ __forceinline__ uint32_t auto_src(uint32_t i, uint32_t g, int log_n) 
 template <int BG, int BETA>
 __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant__ IpRotParams P) {
   const int N = 1 << P.log_n;
-  const int r = blockIdx.y;
-  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  // grid (batch groups, coefficient blocks, rows): the groups sharing a key
+  // slice are scheduled back to back, so the key words hit L2 after the first
+  const int r = blockIdx.z;
+  const int x = blockIdx.y * kEwThreads + threadIdx.x;
   if (x >= N) return;
-  const int b0 = blockIdx.z * BG;
+  const int b0 = blockIdx.x * BG;
   const int nb = P.n_batch - b0 < BG ? P.n_batch - b0 : BG;
   const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
   const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
@@ -810,7 +812,7 @@ void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
   if (P.beta > kMaxRotDigits) throw HegpuError{HEGPU_E_ARG, "too many key-switch digits"};
   if (P.n_rot < 1 || P.n_rot > kMaxRot) throw HegpuError{HEGPU_E_ARG, "1..16 rotations"};
   const int bg = P.n_batch >= 4 ? 4 : P.n_batch >= 2 ? 2 : 1;
-  dim3 grid(((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext, (P.n_batch + bg - 1) / bg);
+  dim3 grid((P.n_batch + bg - 1) / bg, ((1 << P.log_n) + kEwThreads - 1) / kEwThreads, P.n_ext);
   const double ipn = (double)(1 << P.log_n) * P.n_ext;
   ProfScope ps(PROF_KS_IP, st,
                ipn * 8.0 * P.n_rot * (2.0 * P.beta + P.n_batch * P.beta) +
@@ -1115,9 +1117,11 @@ __global__ void __launch_bounds__(32 * (NG / GPT), GPT == 8 ? 3 : 2)
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
   constexpr int BUF = kRunChunk * (COLS + NG * RT);  // words per stage buffer
   const int N = 1 << P.log_n;
-  const int limb = blockIdx.y;
-  const int x0 = blockIdx.x * kRunTile;
-  const int g0 = blockIdx.z * kRunGiants;
+  // grid (giant groups, tiles, limbs): the groups staging the same baby tile
+  // run back to back, so all but the first read it from L2
+  const int limb = blockIdx.z;
+  const int x0 = blockIdx.y * kRunTile;
+  const int g0 = blockIdx.x * kRunGiants;
   const int T = P.n_terms;
   const int nch = (T + kRunChunk - 1) / kRunChunk;
   // terms are staged kRunChunk at a time into one of two buffers (babies
@@ -1224,7 +1228,7 @@ static void launch_bsgs_run_g(const BsgsParams& P, int k, cudaStream_t st) {
                "bsgs smem attr");
     attr_set = true;
   }
-  dim3 grid((1 << P.log_n) / kRunTile, k, (P.n_giants + NG - 1) / NG);
+  dim3 grid((P.n_giants + NG - 1) / NG, (1 << P.log_n) / kRunTile, k);
   k_bsgs_run<RT, GPT, NG><<<grid, 32 * (NG / GPT), smem, st>>>(P);
 }
 
