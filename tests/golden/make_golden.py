@@ -212,6 +212,68 @@ def boot_full_fixture():
             "bootstrap_seconds": tb, "err": float(np.max(np.abs(dec - v)))}
 
 
+def _sigmoid15():
+    path = os.path.join(REPO, "paper_2210_02574_b200", "approximants", "sigmoid_deg15.txt")
+    return minimax.import_text(open(path).read())
+
+
+def predict_p14_fixture():
+    """BASELINE cfg1: N=2^14 (P14) encrypt -> 768-d logistic-regression
+    inference on one ciphertext of 8 rows -> decrypt."""
+    params = load_preset("p14")
+    keys = ckks.keygen(params, rng_seed=7)
+    layout = logreg.make_layout(params, 768)
+    X = np.random.default_rng(0).uniform(-1, 1, (8, 768))
+    w = np.random.default_rng(0).normal(0, 0.05, 768)
+    data = ckks.encrypt_vector(params, logreg._pack_slots(X, layout), keys, rng_seed=1)
+    wv = np.zeros(layout.slot_count)
+    for b in range(layout.rows_per_ct):
+        wv[b * layout.padded_dim: b * layout.padded_dim + 768] = w
+    wct = ckks.encrypt_vector(params, wv, keys, rng_seed=2)
+    model = logreg.EncryptedModel(2, layout, [wct], [wct])
+    sig = _sigmoid15()
+    t0 = time.time()
+    scores = logreg.predict(model, [data], keys, sig)
+    tp = time.time() - t0
+    dec = logreg.decrypt_scores(scores, keys, layout, 8)
+    shadow = logreg.shadow_scores(X, np.concatenate([w, np.zeros(layout.padded_dim - 768)])[None, :],
+                                  sig, layout)
+    np.savez_compressed(os.path.join(HERE, "predict_p14.npz"), X=X, w=w, dec=dec,
+                        shadow=np.asarray(shadow))
+    return {"data": ct_digest(data), "weights": ct_digest(wct), "scores": ct_digest(scores[0][0]),
+            "predict_seconds": tp}
+
+
+def ovr_fixture():
+    """BASELINE cfg5 semantics at desk scale: One-vs-Rest (logreg.py:325-331)
+    over 4 classes of 1024-d blob embeddings, debug refresh, 1 epoch."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "ref_conftest", "/root/reference/pkg/tests/conftest.py")
+    rc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rc)
+    params = ckks.get_preset("desk")
+    X, y = rc.make_blob_embeddings(np.random.default_rng(200), 8, 4, dim=1024)
+    layout = logreg.make_layout(params, 1024)
+    keys = ckks.keygen(params, rotation_steps=sorted(set(ckks.default_rotation_steps(params))),
+                       rng_seed=7)
+    pairs = logreg.pack_batch(X, y.astype(np.float64), layout, params, keys)
+    ovr = logreg.pack_labels_ovr(y, 4, layout, params, keys)
+    cfg = logreg.TrainConfig(0.5, 0.9, 16, 1)
+    sig = _sigmoid15()
+    t0 = time.time()
+    model, _ = logreg.train(pairs, len(y), cfg, params, keys, sig,
+                            bs.DebugRefresher(keys, enabled=True), class_count=4, ovr_labels=ovr,
+                            layout=layout)
+    tt = time.time() - t0
+    got = logreg.decrypted_weights(model, keys)
+    shadow = logreg.shadow_train(X, y, cfg, sig, class_count=4, layout=layout)
+    np.savez_compressed(os.path.join(HERE, "ovr_desk.npz"), X=X, y=y, ref_weights=got,
+                        shadow_weights=np.asarray(shadow.weights))
+    return {"train_seconds": tt}
+
+
 def logreg_fixture():
     params = ckks.get_preset("desk")
     keys = ckks.keygen(params, rng_seed=7)
@@ -234,13 +296,18 @@ def logreg_fixture():
 
 def main():
     t0 = time.time()
-    if sys.argv[1:] == ["boot_full"]:  # add / refresh only this entry
+    only = {"boot_full": ("boot_desk_full", boot_full_fixture),
+            "predict_p14": ("predict_p14", predict_p14_fixture),
+            "ovr": ("ovr_desk", ovr_fixture)}
+    if sys.argv[1:] and sys.argv[1] in only:  # add / refresh only these entries
         path = os.path.join(HERE, "digests.json")
         digests = json.load(open(path))
-        digests["boot_desk_full"] = boot_full_fixture()
+        for name in sys.argv[1:]:
+            key, fn = only[name]
+            digests[key] = fn()
         with open(path, "w") as fh:
             json.dump(digests, fh, indent=1, sort_keys=True)
-        print("boot_full written in %.1fs" % (time.time() - t0), file=sys.stderr)
+        print("%s written in %.1fs" % (sys.argv[1:], time.time() - t0), file=sys.stderr)
         return
     kernels_fixture()
     ring_fixture()
@@ -255,6 +322,8 @@ def main():
         print(name, "done", time.time() - t0, file=sys.stderr)
     digests["boot_desk64"] = boot_fixture()
     digests["boot_desk_full"] = boot_full_fixture()
+    digests["predict_p14"] = predict_p14_fixture()
+    digests["ovr_desk"] = ovr_fixture()
     ref_sig = os.path.join(os.path.dirname(minimax.__file__), "approximants", "sigmoid_deg15.txt")
     digests["sigmoid_ref"] = [float(c).hex() for c in
                               minimax.import_text(open(ref_sig).read()).cheb_coeffs]

@@ -101,3 +101,61 @@ def test_packing_roundtrip(desk):
     assert len(pairs) == 2 and pairs[0][0].level == logreg.DEFAULT_TRANSPORT_LEVEL
     slots = ckks.decrypt_vector(pairs[0][0], keys)
     assert np.max(np.abs(logreg.unpack_rows(slots, layout, 4) - X[:4])) < 1e-4
+
+
+def test_predict_p14_cfg1_matches_reference(digests, sigmoid15):
+    """BASELINE cfg1: P14 (N=2^14) encrypt -> 768-d
+    inference on one ciphertext of 8 rows -> decrypt.  The seeded data and
+    weight ciphertexts are bit-exact with the reference's; the decrypted
+    scores match the reference's run and the plaintext shadow."""
+    d = digests["predict_p14"]
+    g = golden_npz("predict_p14.npz")
+    params = ckks.get_preset("p14")
+    keys = ckks.keygen(params, rng_seed=7)
+    layout = logreg.make_layout(params, 768)
+    X, w = g["X"], g["w"]
+    data = ckks.encrypt_vector(params, logreg._pack_slots(X, layout), keys, rng_seed=1)
+    wv = np.zeros(layout.slot_count)
+    for b in range(layout.rows_per_ct):
+        wv[b * layout.padded_dim: b * layout.padded_dim + 768] = w
+    wct = ckks.encrypt_vector(params, wv, keys, rng_seed=2)
+    from oracle.scheme import sha
+
+    for ct, want in ((data, d["data"]), (wct, d["weights"])):
+        assert {"c0": sha(ct.c0.limbs), "c1": sha(ct.c1.limbs), "level": ct.level,
+                "scale": float(ct.scale).hex()} == want
+    model = logreg.EncryptedModel(2, layout, [wct], [wct])
+    scores = logreg.predict(model, [data], keys, sigmoid15)
+    assert scores[0][0].level == d["scores"]["level"]
+    got = logreg.decrypt_scores(scores, keys, layout, 8)
+    assert np.max(np.abs(got - g["dec"])) < 1e-4  # the reference's decrypted scores
+    assert np.max(np.abs(got - g["shadow"])) < 1e-2  # T/test_logreg.py:259
+
+
+def test_ovr_multiclass_1024d_matches_reference(sigmoid15):
+    """BASELINE cfg5 semantics (One-vs-Rest, logreg.py:325-331) at desk
+    scale: 4 classes of 1024-d embeddings (2 rows per ciphertext); weights
+    against the reference's trained weights and the shadow trainer, argmax
+    agreement with the shadow (T/test_acceptance.py:171)."""
+    g = golden_npz("ovr_desk.npz")
+    X, y = g["X"], g["y"]
+    params = ckks.get_preset("desk")
+    keys = ckks.keygen(params, rotation_steps=sorted(set(ckks.default_rotation_steps(params))),
+                       rng_seed=7)
+    layout = logreg.make_layout(params, 1024)
+    assert layout.padded_dim == 2048 and layout.rows_per_ct == 2
+    pairs = logreg.pack_batch(X, y.astype(np.float64), layout, params, keys)
+    ovr = logreg.pack_labels_ovr(y, 4, layout, params, keys)
+    cfg = logreg.TrainConfig(0.5, 0.9, 16, 1)
+    model, _ = logreg.train(pairs, len(y), cfg, params, keys, sigmoid15,
+                            bs.DebugRefresher(keys, enabled=True), class_count=4, ovr_labels=ovr,
+                            layout=layout)
+    assert len(model.weights) == 4
+    got = logreg.decrypted_weights(model, keys)
+    shadow = logreg.shadow_train(X, y, cfg, sigmoid15, class_count=4, layout=layout)
+    assert np.array_equal(np.asarray(shadow.weights), g["shadow_weights"])
+    assert np.max(np.abs(got - shadow.weights)) <= 2e-2
+    assert np.max(np.abs(got - g["ref_weights"])) <= 2e-2
+    enc = logreg.shadow_scores(X, got, sigmoid15, layout)
+    sh = logreg.shadow_scores(X, np.asarray(shadow.weights), sigmoid15, layout)
+    assert np.mean(np.argmax(enc, axis=1) == np.argmax(sh, axis=1)) >= 0.98
