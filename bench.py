@@ -697,8 +697,11 @@ def run_ours(args):
     step_ms_prof = sum(p["ms"] for c, p in prof.items() if not c.startswith("ntt_"))
     try:
         int_peak = _lib.modmul_peak()
+        fp_peak = _lib.fp_modmul_peak()
     except Exception:
-        int_peak = None
+        int_peak = fp_peak = None
+    mm_rate = dp["modmuls"] / (dp["ms"] / 1e3) if dp["ms"] else 0
+    traffic, traffic_src = dram_traffic(args.config, dom)
     line = {
         "metric": wl.metric, "value": round(value, 4), "unit": wl.unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -710,14 +713,21 @@ def run_ours(args):
         "gpu_launches": int(launches) if launches else None,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": round(dp["bytes"] / dp["launches"])
+                     if dp["launches"] else None,
                      "share_of_step": round(dp["ms"] / step_ms_prof, 4) if step_ms_prof else None},
+        # the NTT is modmul-bound, not HBM-bound: its products run on the FP64
+        # pipe for primes < 2^46 and on the integer pipe (64-bit Shoup) for the
+        # 60-bit primes; both peaks are measured by the library on this GPU
         "int_roofline": {
             "kernel": dom,
-            "achieved_modmul_per_s": round(dp["modmuls"] / (dp["ms"] / 1e3), 1) if dp["ms"] else 0,
+            "achieved_modmul_per_s": round(mm_rate, 1),
             "peak_modmul_per_s": int_peak,
-            "frac": round(dp["modmuls"] / (dp["ms"] / 1e3) / int_peak, 4)
-            if (dp["ms"] and int_peak) else None},
+            "frac": round(mm_rate / int_peak, 4) if (mm_rate and int_peak) else None,
+            "fp64_peak_modmul_per_s": fp_peak,
+            "frac_of_fp64_peak": round(mm_rate / fp_peak, 4) if (mm_rate and fp_peak) else None},
         "kernel_profile_ms": {c: round(p["ms"], 3) for c, p in prof.items() if p["launches"]},
         "kernel_profile_gbs": {c: round(p["bytes"] / p["ms"] / 1e6, 1)
                                for c, p in prof.items() if p["launches"] and p["ms"]},
@@ -727,6 +737,24 @@ def run_ours(args):
     line.update(extra)
     line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line), flush=True)
+
+
+def dram_traffic(config, cls):
+    """Measured DRAM bytes per launch of kernel class `cls` in this workload's
+    step: profiles/<round>_dram_traffic_<config>.json, written by
+    tools/dram_summary.py from an ncu pass (dram__bytes_read/write.sum) over
+    one eager step of the same command (tools/profile_round.sh)."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_dram_traffic_{config}.json")))
+    if not paths:
+        return None, None
+    try:
+        with open(paths[-1]) as fh:
+            rec = json.load(fh)[cls]
+        return int(rec["dram_bytes_per_launch"]), os.path.relpath(paths[-1], REPO)
+    except (KeyError, ValueError, OSError):
+        return None, None
 
 
 def cpu_baseline(wl):

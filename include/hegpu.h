@@ -60,6 +60,9 @@ long long hegpu_launch_count(void);
 /* Measured 64-bit Shoup modular-multiplication throughput of this GPU
  * (modmul/s, 8 independent chains per thread, all SMs); synchronous. */
 int hegpu_bench_modmul_peak(int iters, double* modmul_per_s);
+/* The same for the FP64-pipe modmul the engine uses for primes < 2^46
+ * (exact double arithmetic, 6 FP64 ops per product); synchronous. */
+int hegpu_bench_fp_modmul_peak(int iters, double* modmul_per_s);
 /* Enable (1) / disable (0) per-launch CUDA-event timing; clears records. */
 int hegpu_profile_enable(int on);
 /* Synchronise the device, then report and clear, per kernel class, the

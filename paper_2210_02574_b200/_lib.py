@@ -30,6 +30,7 @@ SIGNATURES = {
     "hegpu_device_count": [],
     "hegpu_launch_count": [],
     "hegpu_bench_modmul_peak": [_I, _P],
+    "hegpu_bench_fp_modmul_peak": [_I, _P],
     "hegpu_profile_enable": [_I],
     "hegpu_profile_read": [_P, _P, _P, _P, _I],
     "hegpu_ring_create": [_I, _P, _I, _P, _I, _P],
@@ -164,4 +165,11 @@ def modmul_peak(iters=4096):
     """Measured INT64 Shoup modmul/s of the current GPU."""
     out = ctypes.c_double()
     call("hegpu_bench_modmul_peak", iters, ctypes.byref(out))
+    return out.value
+
+
+def fp_modmul_peak(iters=4096):
+    """Measured FP64-pipe modmul/s (primes < 2^46) of the current GPU."""
+    out = ctypes.c_double()
+    call("hegpu_bench_fp_modmul_peak", iters, ctypes.byref(out))
     return out.value

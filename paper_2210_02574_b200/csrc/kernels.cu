@@ -919,6 +919,47 @@ __global__ void __launch_bounds__(256) k_modmul_peak(uint64_t* sink, uint64_t q,
   if (acc == 0x123456789ull) sink[0] = acc;  // keep the chains alive
 }
 
+// FP64-pipe modmul (common.cuh fp_mulmod) on a 40-bit chain prime
+__global__ void __launch_bounds__(256) k_fp_modmul_peak(double* sink, double q, double w,
+                                                        double wq, int iters) {
+  double x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = (double)((threadIdx.x * 8 + c + blockIdx.x) % 100000);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = fp_mulmod(x[c], w, wq, q);
+  }
+  double acc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc += x[c];
+  if (acc == 0.5) sink[0] = acc;  // keep the chains alive
+}
+
+double bench_fp_modmul_peak(int iters) {
+  const uint64_t qi = 0xffffe80001ull;  // 40-bit prime of the P16 chain
+  const double q = (double)qi, w = (double)(0x123456789ull % qi), wq = w / q;
+  int dev = 0, sms = 0;
+  check_cuda(cudaGetDevice(&dev), "device");
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  double* sink = nullptr;
+  check_cuda(cudaMalloc(&sink, 8), "alloc");
+  const int blocks = sms * 8, threads = 256;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_fp_modmul_peak<<<blocks, threads>>>(sink, q, w, wq, 64);
+  cudaEventRecord(a);
+  k_fp_modmul_peak<<<blocks, threads>>>(sink, q, w, wq, iters);
+  cudaEventRecord(b);
+  check_cuda(cudaEventSynchronize(b), "fp modmul bench");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  return (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+}
+
 double bench_modmul_peak(int iters) {
   const uint64_t q = 0xffffffffffc0001ull;  // 60-bit prime of the P16 chain
   const uint64_t w = 0x123456789abcdull % q;

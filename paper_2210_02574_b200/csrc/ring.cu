@@ -1531,6 +1531,10 @@ int hegpu_device_count(void) {
 
 long long hegpu_launch_count(void) { return g_launches.load(); }
 
+int hegpu_bench_fp_modmul_peak(int iters, double* modmul_per_s) {
+  HEGPU_TRY(*modmul_per_s = bench_fp_modmul_peak(iters))
+}
+
 int hegpu_bench_modmul_peak(int iters, double* modmul_per_s) {
   HEGPU_TRY(*modmul_per_s = bench_modmul_peak(iters))
 }

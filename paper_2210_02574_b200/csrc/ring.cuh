@@ -291,6 +291,7 @@ void launch_diag_mac(const PrimeConst* dpc, int log_n, const uint64_t* const* ct
                      int64_t out_bstride, int k, int accumulate, cudaStream_t st);
 void launch_ks_ip(IpParams& P, cudaStream_t st);
 double bench_modmul_peak(int iters);
+double bench_fp_modmul_peak(int iters);
 void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies, int n_terms,
                  int64_t c1_off, int64_t bstride, int n_batch, const uint64_t* pt_base,
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
