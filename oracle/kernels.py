@@ -26,7 +26,7 @@ def build_c(verbose=False):
 
     os.makedirs(os.path.dirname(C_LIB_PATH), exist_ok=True)
     src = os.path.join(_HERE, "csrc", "hekernels.c")
-    cmd = ["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-o", C_LIB_PATH, src]
+    cmd = ["gcc", "-O3", "-march=x86-64-v3", "-fopenmp", "-fPIC", "-shared", "-o", C_LIB_PATH, src]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -1270,8 +1270,8 @@ static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials
     first = false;
   }
   if (!first) {  // sum += the giants' switched parts (both components, extended basis)
-    EwArgs A{HEGPU_OP_ADD, sum, (int64_t)n_ext * N, acc, (int64_t)n_ext * N, sum,
-             (int64_t)n_ext * N, 2 * B, n_ext, ext_rows.data(), nullptr};
+    EwArgs A{HEGPU_OP_ADD, sum, (int64_t)n_ext * (int64_t)N, acc, (int64_t)n_ext * (int64_t)N, sum,
+             (int64_t)n_ext * (int64_t)N, 2 * B, n_ext, ext_rows.data(), nullptr};
     launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
   }
   ks_moddown_rescale(R, L, sum, corr, B, nullptr, 0, 0, down, (int64_t)2 * level * N,
