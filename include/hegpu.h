@@ -144,6 +144,17 @@ int hegpu_encode_diags(hegpu_ring_t ring, int kind, int half, double fold, doubl
                        void* scratch, int64_t* out, void* stream);
 int hegpu_encode_overflow(hegpu_ring_t ring, int* flag);
 
+/* numpy Generator(PCG64).integers(0, bounds[l], size=n, dtype=uint64) for
+ * l = 0..k-1 in order (the per-limb uniform sampling of ring.sample_poly,
+ * ring.py:494-498, and keygen, keys.py:133-151, 204-206), drawn on the device
+ * from the generator state (state, inc as 128-bit halves) into out + l *
+ * out_stride.  Bounds must exceed 2^32.  *consumed = 64-bit draws used
+ * (k*n plus rejections); the caller advances its generator by that much.
+ * Synchronizes the stream. */
+int hegpu_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        const uint64_t* bounds, int k, int n, uint64_t* out,
+                        int64_t out_stride, long long* consumed, void* stream);
+
 /* Forward NTT of signed int64 coefficient rows into k eval-form limbs: the
  * lift of poly_from_signed (ring.py:381-393) fused into the NTT's first pass.
  * src poly p at src + p*src_stride, out poly p at out + p*out_stride. */

@@ -45,6 +45,7 @@ SIGNATURES = {
                            _P, _P],
     "hegpu_encode_overflow": [_P, _P],
     "hegpu_ntt_from_signed": [_P, _P, _I64, _P, _I64, _I, _I, _P, _P],
+    "hegpu_pcg64_uniform": [_U64, _U64, _U64, _U64, _P, _I, _I, _P, _I64, _P, _P],
     "hegpu_tensor": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_apply": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _P, _I64, _I, _P],
     "hegpu_tensor_periodic": [_P, _P, _P, _I64, _I, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],

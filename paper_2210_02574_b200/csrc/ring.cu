@@ -1671,6 +1671,13 @@ int hegpu_ntt_from_signed(hegpu_ring_t ring, const int64_t* src, int64_t src_str
   })
 }
 
+int hegpu_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        const uint64_t* bounds, int k, int n, uint64_t* out,
+                        int64_t out_stride, long long* consumed, void* stream) {
+  HEGPU_TRY(*consumed = pcg64_uniform_fill(state_hi, state_lo, inc_hi, inc_lo, bounds, k, n, out,
+                                           out_stride, S_(stream)))
+}
+
 int hegpu_encode_overflow(hegpu_ring_t ring, int* flag) {
   HEGPU_TRY({
     Ring& R = RR(ring);

@@ -304,4 +304,9 @@ void launch_encode_diags(Ring& R, int kind, int half, double fold, double scale,
                          double2* scratch, int64_t* out, cudaStream_t st);
 bool encode_overflow_check(Ring& R);
 
+// rng.cu: numpy-compatible PCG64 bounded uniform draws; returns draws consumed
+long long pcg64_uniform_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                             uint64_t inc_lo, const uint64_t* bounds, int k, int n,
+                             uint64_t* out, int64_t out_stride, cudaStream_t st);
+
 }  // namespace hegpu

@@ -255,6 +255,7 @@ def ovr_fixture():
     spec.loader.exec_module(rc)
     params = ckks.get_preset("desk")
     X, y = rc.make_blob_embeddings(np.random.default_rng(200), 8, 4, dim=1024)
+    X = X * 0.25  # keeps every logit inside the sigmoid's fitted domain (|z| <= 12)
     layout = logreg.make_layout(params, 1024)
     keys = ckks.keygen(params, rotation_steps=sorted(set(ckks.default_rotation_steps(params))),
                        rng_seed=7)

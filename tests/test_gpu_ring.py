@@ -173,3 +173,26 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T):
         want = sum(int(pts_c[idx[g, t], l, x >> lr]) * int(bab[t, b, c, l, x])
                    for t in range(T) if idx[g, t] >= 0) % qs[l]
         assert int(outs[0][g, b, c, l, x]) == want
+
+
+def test_pcg64_uniform_device_matches_numpy():
+    """hegpu_pcg64_uniform reproduces numpy's Generator(PCG64).integers(0, q,
+    dtype=uint64) stream (keygen's uniform `a` draws) and leaves the generator
+    where numpy would: bit-exact on P16's 27 primes, and with bounds whose
+    Lemire rejection rate is ~1/4 (many rejected draws re-mapped)."""
+    from paper_2210_02574_b200 import _dev, ckks, ring as rg
+
+    params = ckks.get_preset("p16")
+    primes = list(params.ring.moduli_chain) + list(params.ring.special_moduli)
+    n = params.ring_degree
+    for bounds, m in ((primes, n), ([(1 << 62) + 1, (1 << 62) + 3, (1 << 63) - 25], 48)):
+        dev_rng, host_rng = np.random.default_rng(2024), np.random.default_rng(2024)
+        dev_rng.integers(-1, 2, size=17)  # leave a buffered uint32 behind, as keygen does
+        host_rng.integers(-1, 2, size=17)
+        out = _dev.empty(len(bounds), m)
+        rg.sample_uniform_dev(dev_rng, bounds, m, out)
+        want = np.stack([host_rng.integers(0, q, size=m, dtype=np.uint64) for q in bounds])
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want)
+        assert dev_rng.bit_generator.state == host_rng.bit_generator.state
+        assert np.array_equal(dev_rng.normal(size=5), host_rng.normal(size=5))
+        assert np.array_equal(dev_rng.integers(-1, 2, size=9), host_rng.integers(-1, 2, size=9))

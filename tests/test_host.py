@@ -172,3 +172,26 @@ def test_periodic_diagonal_run_compression():
         runs = ev.reshape(len(primes), n // r, r)
         assert (runs == runs[..., :1]).all()
         assert bs._run_log(type("P", (), {"ring_degree": n})(), period) == min(r.bit_length() - 1, 5)
+
+
+def test_pcg64_advance_matches_numpy():
+    """ring.pcg64_advance_state (the host half of hegpu_pcg64_uniform) is
+    numpy's PCG64 jump: the generator state after d draws."""
+    import numpy as np
+
+    from paper_2210_02574_b200 import ring as rg
+
+    for seed, d in ((7, 1), (11, 1_769_473), (3, 12345678901)):
+        g = np.random.default_rng(seed)
+        st = g.bit_generator.state["state"]
+        want = np.random.default_rng(seed)
+        want.bit_generator.advance(d)
+        assert rg.pcg64_advance_state(st["state"], st["inc"], d) == \
+            want.bit_generator.state["state"]["state"]
+    # one bounded uint64 draw = one 64-bit output: the stream position the
+    # device fill reports for k*n draws without rejections
+    g = np.random.default_rng(5)
+    st = g.bit_generator.state["state"]
+    g.integers(0, 0xffffe80001, size=1000, dtype=np.uint64)
+    assert rg.pcg64_advance_state(st["state"], st["inc"], 1000) == \
+        g.bit_generator.state["state"]["state"]
