@@ -64,6 +64,35 @@ __device__ __forceinline__ double fp_reduce(double x, double q, double qinv) {
   const double t = fma(x, qinv, kFpMagic) - kFpMagic;
   return fma(-t, q, x);
 }
+// Split products for primes q < 2^46: a residue x is held as (h, l) =
+// (rint(x / 2^23), x - 2^23 h), |h| <= 2^23, |l| <= 2^22, so
+//   x y = 2^46 h h' + 2^23 (h l' + l h') + l l'
+// with every partial product <= 2^46: three FP64 accumulators stay exact for
+// 64 products, each product costing 4 DFMA.
+struct FpSplitAcc {
+  double h, m, l;
+  __device__ __forceinline__ void zero() { h = m = l = 0.0; }
+  __device__ __forceinline__ void add(double2 x, double2 y) {
+    h = fma(x.x, y.x, h);
+    m = fma(x.x, y.y, m);
+    m = fma(x.y, y.x, m);
+    l = fma(x.y, y.y, l);
+  }
+};
+struct FpSplitConst {
+  double q, qinv, c23, c23q, c46, c46q;  // 2^23, 2^46 mod q and their quotients
+};
+__device__ __forceinline__ FpSplitConst fp_split_const(uint64_t qi) {
+  FpSplitConst c;
+  c.q = (double)qi;
+  c.qinv = 1.0 / c.q;
+  c.c23 = (double)((1ull << 23) % qi);
+  c.c46 = (double)((1ull << 46) % qi);
+  c.c23q = c.c23 / c.q;
+  c.c46q = c.c46 / c.q;
+  return c;
+}
+
 // signed 64-bit integer <-> double, exact for |x| < 2^51
 __device__ __forceinline__ double fp_from_s64(uint64_t x) {
   return __longlong_as_double(static_cast<long long>(x) + kFpMagicBits) - kFpMagic;
@@ -78,6 +107,19 @@ __device__ __forceinline__ uint64_t fp_to_residue_small(double x, double q) {
 // any |x| < 2^51 -> residue in [0, q)
 __device__ __forceinline__ uint64_t fp_to_residue(double x, double q, double qinv) {
   return fp_to_residue_small(fp_reduce(x, q, qinv), q);
+}
+// residue (< 2^46) -> (h, l) split
+__device__ __forceinline__ double2 fp_split23(uint64_t w) {
+  const double x = fp_from_s64(w);
+  const double h = fma(x, 0x1p-23, kFpMagic) - kFpMagic;
+  return make_double2(h, fma(-h, 0x1p23, x));
+}
+// value of a split accumulator, centred-reduced: |result| <= q/2 + 1
+__device__ __forceinline__ double fp_split_fold(const FpSplitAcc& a, const FpSplitConst& c) {
+  const double v = fp_mulmod(fp_reduce(a.h, c.q, c.qinv), c.c46, c.c46q, c.q) +
+                   fp_mulmod(fp_reduce(a.m, c.q, c.qinv), c.c23, c.c23q, c.q) +
+                   fp_reduce(a.l, c.q, c.qinv);
+  return fp_reduce(v, c.q, c.qinv);
 }
 
 // ---------------------------------------------------------------------------
@@ -261,6 +303,9 @@ struct Seg {
   // cfw[i] (cfw = 2^cfs / d_i; both read at stride 2, one per 64-bit word)
   // and e * cnegd[t] (= -D R mod p_t) is added
   int cmode;
+  // every conversion source prime is < 2^kFpMaxBits: the prologue may run
+  // part of its products on the FP64 pipe (split products, above)
+  int c_fp_src;
   uint64_t csrc_q;
   const uint64_t* cnegd;
   const float* cfw;

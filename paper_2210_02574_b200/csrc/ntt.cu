@@ -265,8 +265,13 @@ constexpr int kConvMaxSrc = 8;
 #ifndef HEGPU_BLOCKS_MINB
 #define HEGPU_BLOCKS_MINB 4
 #endif
+#ifndef HEGPU_CONV_HYBRID
+#define HEGPU_CONV_HYBRID 0
+#endif
+// column passes at 4 CTAs/SM (64 registers): measured 95.5 ms per training
+// step vs 96.9 at 5 (48 registers, the conversion prologues spilled)
 #ifndef HEGPU_COLS_MINB
-#define HEGPU_COLS_MINB 5
+#define HEGPU_COLS_MINB 4
 #endif
 
 // slot -> (st << 16 | local) of TwLayout<6 + li, inv>, filled once by the host
@@ -309,7 +314,7 @@ void ensure_tw_slots() {
 template <int LOGS>
 constexpr size_t cols_r_smem() {
   return ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8 +
-         (size_t)(1 << LOGS) * 16 + kConvMaxSrc * 3 * 8;
+         (size_t)(1 << LOGS) * 16 + kConvMaxSrc * 3 * 8 + kConvMaxSrc * 16;
 }
 template <int LOGS>
 constexpr size_t blocks_r_smem() {
@@ -361,6 +366,9 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
   const int nsrc = CM >= 2 ? sg.c_nsrc : 0;
   for (int i = threadIdx.x; i < nsrc && i < kConvMaxSrc; i += blockDim.x) {
     s_conv[i] = __ldg(sg.cpunc + i * sg.cpunc_ld + limb);
+    if (CM == 2 && pc.twf != nullptr && sg.c_fp_src)  // natural-form constant, split
+      reinterpret_cast<double2*>(s_conv + 3 * kConvMaxSrc)[i] =
+          fp_split23(mont_mul(s_conv[i], 1, pc.q, pc.qinv_neg));
     if (CM == 3) {
       s_conv[kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfw) + i);
       s_conv[2 * kConvMaxSrc + i] = __ldg(reinterpret_cast<const uint64_t*>(sg.cfs) + i);
@@ -398,7 +406,36 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_COLS_MI
       // fused fast basis conversion: out_t = REDC(sum_i hat_i * punc_mont[i][t])
       const uint64_t* hs = sg.csrc + poly * sg.csrc_stride;
       const uint64_t q = pc.q;
-      if (nsrc <= kConvMaxSrc) {
+      if (CM == 2 && nsrc <= kConvMaxSrc && HEGPU_CONV_HYBRID && pc.twf != nullptr &&
+          sg.c_fp_src) {
+        // hybrid: odd sources as FP64 split products (FP64 pipe), even ones
+        // in the 128-bit integer MAC (IMAD / ALU pipes); both exact
+        const double2* s_convf = reinterpret_cast<const double2*>(s_conv + 3 * kConvMaxSrc);
+        const FpSplitConst fc = fp_split_const(q);
+#pragma unroll 2
+        for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {
+          const int r = e / kRegWarps, c = e % kRegWarps;
+          const size_t x = c0 + c + (size_t)C * r;
+          uint64_t h[kConvMaxSrc];
+#pragma unroll
+          for (int i = 0; i < kConvMaxSrc; ++i) h[i] = i < nsrc ? __ldg(hs + (size_t)i * N + x) : 0;
+          Mac128 acc;
+          acc.zero();
+          FpSplitAcc fa;
+          fa.zero();
+#pragma unroll
+          for (int i = 0; i < kConvMaxSrc; ++i) {
+            if (i < nsrc) {
+              if (i & 1)
+                fa.add(fp_split23(h[i]), s_convf[i]);
+              else
+                acc.add(h[i], s_conv[i]);
+            }
+          }
+          tile[tix(r, c)] =
+              add_mod(acc.redc(pc), fp_to_residue_small(fp_split_fold(fa, fc), fc.q), q);
+        }
+      } else if (nsrc <= kConvMaxSrc) {
         // unrolled: the nsrc source words of each coefficient load together
 #pragma unroll 2
         for (int e = threadIdx.x; e < S * kRegWarps; e += blockDim.x) {

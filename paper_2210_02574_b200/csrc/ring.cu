@@ -439,6 +439,7 @@ static void add_seg(SegSet& S, const uint64_t* in, int64_t is, uint64_t* out, in
   g.ein = nullptr;
   g.ein_stride = 0;
   g.cmode = 0;
+  g.c_fp_src = 0;
   g.csrc_q = 0;
   g.cnegd = nullptr;
   g.cfw = nullptr;
@@ -518,6 +519,8 @@ static void ks_modup(Ring& R, const KsLevel& L, const uint64_t* d, int64_t ds, i
         sg.cpunc = L.mu_punc + (size_t)g0 * n_ext;
         sg.c_nsrc = g;
         sg.cpunc_ld = n_ext;
+        sg.c_fp_src = 1;
+        for (int i = g0; i < g1; ++i) sg.c_fp_src &= R.hpc[i].twf != nullptr ? 1 : 0;
       }
       launch_ntt(R.dpc, R.dtw, R.log_n, false, S, nullptr, st, &R.fp_mask);
     }
