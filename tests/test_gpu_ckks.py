@@ -296,3 +296,25 @@ def test_serialization_roundtrip(desk_keys):
     blob = ckks.serialize_ciphertext(ct)
     assert ckks.serialize_ciphertext(ckks.deserialize_ciphertext(blob, params)) == blob
     assert len(blob) == ckks.size_report(params, ct.level)
+
+
+def test_batched_ciphertext_ingest(desk_keys):
+    """deserialize_ciphertexts: several CKT1 buffers -> one batched device
+    ciphertext through one pinned H2D copy; each element re-serializes to its
+    own bytes, and mismatched buffers are refused like the single path."""
+    from paper_2210_02574_b200.errors import SerializationError
+
+    params, keys = desk_keys
+    rng = np.random.default_rng(4)
+    cts = [ckks.encrypt_vector(params, rng.uniform(-1, 1, 32), keys, level=3, rng_seed=i)
+           for i in range(3)]
+    blobs = [ckks.serialize_ciphertext(c) for c in cts]
+    batch = ckks.deserialize_ciphertexts(blobs, params)
+    assert batch.batch == 3 and batch.level == 3
+    for i, blob in enumerate(blobs):
+        assert ckks.serialize_ciphertext(batch[i]) == blob
+    other = ckks.serialize_ciphertext(ckks.encrypt_vector(params, np.zeros(4), keys, level=2))
+    with pytest.raises(SerializationError):
+        ckks.deserialize_ciphertexts(blobs + [other], params)
+    with pytest.raises(SerializationError):
+        ckks.deserialize_ciphertexts([blobs[0][:-8]], params)
