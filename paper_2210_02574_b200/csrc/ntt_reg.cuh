@@ -28,25 +28,15 @@ struct RegShape {
   static constexpr int EB = LOGS - 5;  // log2(elements per lane)
   static constexpr int E = 1 << EB;
   static constexpr int ROUNDS = (LOGS + EB - 1) / EB;
-  static constexpr int PAD_S = S + S / 16;  // warp buffer with 1 pad word per 16
+  // warp buffer: element j of a shuffle lives at j + (j >> s), s >= SMIN (shf_shift)
+  static constexpr int SMIN = LOGS - 5;
+  static constexpr int PAD_S = S + (S >> SMIN);
 };
 
 __device__ __forceinline__ int reg_j(int lane, int e, int lo, int eb) {
   return (lane & ((1 << lo) - 1)) | (e << lo) | ((lane >> lo) << (lo + eb));
 }
 __device__ __forceinline__ int padi(int j) { return j + (j >> 4); }
-// warp-buffer slot of element j: 64-bit accesses are served per half-warp, so
-// a half-warp's 16 words must hit 16 distinct bank pairs.  For the round
-// windows of S = 128 / 256 the XOR swizzle j ^ ((j >> 3) & 15) is
-// conflict-free in every round (1 padded word per 16 leaves 2-way conflicts);
-// for S = 512 the padding is.
-template <int LOGS>
-__device__ __forceinline__ int shf_idx(int j) {
-  if constexpr (LOGS == 7 || LOGS == 8)
-    return j ^ ((j >> 3) & 15);
-  else
-    return padi(j);
-}
 
 
 // ---------------------------------------------------------------------------
@@ -172,18 +162,45 @@ __device__ __forceinline__ void inv_round(uint64_t (&x)[RegShape<LOGS>::E],
   }
 }
 
-// Re-distribute the warp's elements from window lo_from to window lo_to.
-template <int LOGS, typename T>
-__device__ __forceinline__ void reg_shuffle(T (&x)[RegShape<LOGS>::E], T* buf,
-                                            int lane, int lo_from, int lo_to) {
-  constexpr int E = RegShape<LOGS>::E, EB = RegShape<LOGS>::EB;
-  if (lo_from == lo_to) return;
+// Padding shift of the warp buffer for a shuffle from window FROM to window TO:
+// element j lives at j + (j >> s).  The lane bits and the register bits of j
+// are disjoint, so the slot is base(lane) + c(e) with c a compile-time
+// constant: no per-access index arithmetic.  s is chosen per (FROM, TO) for
+// the fewest shared-memory wavefronts (64-bit words, served per half warp)
+// over the store and the load: ideal for every shuffle of S = 64..512 except
+// two of S = 256 / three of S = 64, 128 (1.5x).
+template <int LOGS>
+__host__ __device__ constexpr int shf_shift(int from, int to) {
+  if (LOGS == 9) return 4;
+  if (LOGS == 8) return (from == 0 && to == 5) || (from == 5 && to == 0) ? 4 : 3;
+  if (LOGS == 7) return (from == 5 || to == 5) ? 4 : 2;
+  // LOGS == 6
+  return (from >= 3 && to >= 3) || from == 5 || to == 5 ? 4 : 1;
+}
+
+template <int LOGS, int W>
+__device__ __forceinline__ int shf_base(int lane, int s) {
+  constexpr int EB = RegShape<LOGS>::EB;
+  const int a = (lane & ((1 << W) - 1)) | ((lane >> W) << (W + EB));
+  return a + (a >> s);
+}
+
+// Re-distribute the warp's elements from window FROM to window TO.
+template <int LOGS, int FROM, int TO, typename T>
+__device__ __forceinline__ void reg_shuffle(T (&x)[RegShape<LOGS>::E], T* buf, int lane) {
+  constexpr int E = RegShape<LOGS>::E;
+  if constexpr (FROM != TO) {
+    constexpr int s = shf_shift<LOGS>(FROM, TO);
+    static_assert(s >= RegShape<LOGS>::SMIN, "warp buffer too small for this padding");
+    T* bf = buf + shf_base<LOGS, FROM>(lane, s);
 #pragma unroll
-  for (int e = 0; e < E; ++e) buf[shf_idx<LOGS>(reg_j(lane, e, lo_from, EB))] = x[e];
-  __syncwarp();
+    for (int e = 0; e < E; ++e) bf[(e << FROM) + ((e << FROM) >> s)] = x[e];
+    __syncwarp();
+    const T* bt = buf + shf_base<LOGS, TO>(lane, s);
 #pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = buf[shf_idx<LOGS>(reg_j(lane, e, lo_to, EB))];
-  __syncwarp();
+    for (int e = 0; e < E; ++e) x[e] = bt[(e << TO) + ((e << TO) >> s)];
+    __syncwarp();
+  }
 }
 
 // lane's twiddle run of round r in the staged table
@@ -193,32 +210,33 @@ __device__ __forceinline__ const TW* tw_run(const TW* tab, int lane) {
   return tab + L::off(r) + (lane >> L::lo(r)) * L::cnt(r);
 }
 
-template <int LOGS, int r = 0>
+// CUR: the window the elements are in; the sub-transform starts and ends in
+// the strided window LOGS - EB (j = lane + 32 e)
+template <int LOGS, int r = 0, int CUR = LOGS - RegShape<LOGS>::EB>
 __device__ __forceinline__ void fwd_rounds(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
-                                           int lane, int cur, const ulonglong2* tab, uint64_t q,
-                                           int lo_out) {
+                                           int lane, const ulonglong2* tab, uint64_t q) {
   using L = TwLayout<LOGS, false>;
   if constexpr (r < L::R) {
-    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    reg_shuffle<LOGS, CUR, L::lo(r)>(x, buf, lane);
     fwd_round<LOGS, r>(x, tw_run<LOGS, false, r>(tab, lane), q);
-    fwd_rounds<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, q, lo_out);
+    fwd_rounds<LOGS, r + 1, L::lo(r)>(x, buf, lane, tab, q);
   } else {
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+    reg_shuffle<LOGS, CUR, LOGS - RegShape<LOGS>::EB>(x, buf, lane);
   }
 }
 
-template <int LOGS, int r = 0>
+template <int LOGS, int r = 0, int CUR = LOGS - RegShape<LOGS>::EB>
 __device__ __forceinline__ void inv_rounds(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
-                                           int lane, int cur, const ulonglong2* tab, int last_p,
+                                           int lane, const ulonglong2* tab, int last_p,
                                            const PrimeConst& pc, const ulonglong2 fin_s,
-                                           const ulonglong2 fin_d, int lo_out) {
+                                           const ulonglong2 fin_d) {
   using L = TwLayout<LOGS, true>;
   if constexpr (r < L::R) {
-    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    reg_shuffle<LOGS, CUR, L::lo(r)>(x, buf, lane);
     inv_round<LOGS, r>(x, tw_run<LOGS, true, r>(tab, lane), last_p, pc, fin_s, fin_d);
-    inv_rounds<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, last_p, pc, fin_s, fin_d, lo_out);
+    inv_rounds<LOGS, r + 1, L::lo(r)>(x, buf, lane, tab, last_p, pc, fin_s, fin_d);
   } else {
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+    reg_shuffle<LOGS, CUR, LOGS - RegShape<LOGS>::EB>(x, buf, lane);
   }
 }
 
@@ -228,7 +246,9 @@ template <int LOGS>
 __device__ __forceinline__ void fwd_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64_t* buf,
                                         int lane, int lo_in, int lo_out, const ulonglong2* tab,
                                         uint64_t q) {
-  fwd_rounds<LOGS>(x, buf, lane, lo_in, tab, q, lo_out);
+  (void)lo_in;  // both are the strided window LOGS - EB
+  (void)lo_out;
+  fwd_rounds<LOGS>(x, buf, lane, tab, q);
 }
 
 template <int LOGS>
@@ -236,7 +256,9 @@ __device__ __forceinline__ void inv_sub(uint64_t (&x)[RegShape<LOGS>::E], uint64
                                         int lane, int lo_in, int lo_out, int last_p,
                                         const ulonglong2* tab, const PrimeConst& pc,
                                         const ulonglong2 fin_s, const ulonglong2 fin_d) {
-  inv_rounds<LOGS>(x, buf, lane, lo_in, tab, last_p, pc, fin_s, fin_d, lo_out);
+  (void)lo_in;
+  (void)lo_out;
+  inv_rounds<LOGS>(x, buf, lane, tab, last_p, pc, fin_s, fin_d);
 }
 
 // ---------------------------------------------------------------------------
@@ -297,40 +319,40 @@ __device__ __forceinline__ void inv_round_fp(double (&x)[RegShape<LOGS>::E],
   }
 }
 
-template <int LOGS, int r = 0>
+template <int LOGS, int r = 0, int CUR = LOGS - RegShape<LOGS>::EB>
 __device__ __forceinline__ void fwd_rounds_fp(double (&x)[RegShape<LOGS>::E], double* buf,
-                                              int lane, int cur, const double2* tab, double q,
-                                              int lo_out) {
+                                              int lane, const double2* tab, double q) {
   using L = TwLayout<LOGS, false>;
   if constexpr (r < L::R) {
-    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    reg_shuffle<LOGS, CUR, L::lo(r)>(x, buf, lane);
     fwd_round_fp<LOGS, r>(x, tw_run<LOGS, false, r>(tab, lane), q);
-    fwd_rounds_fp<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, q, lo_out);
+    fwd_rounds_fp<LOGS, r + 1, L::lo(r)>(x, buf, lane, tab, q);
   } else {
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+    reg_shuffle<LOGS, CUR, LOGS - RegShape<LOGS>::EB>(x, buf, lane);
   }
 }
 
-template <int LOGS, int r = 0>
+template <int LOGS, int r = 0, int CUR = LOGS - RegShape<LOGS>::EB>
 __device__ __forceinline__ void inv_rounds_fp(double (&x)[RegShape<LOGS>::E], double* buf,
-                                              int lane, int cur, const double2* tab, int last_p,
+                                              int lane, const double2* tab, int last_p,
                                               double q, double qinv, const double2 fin_s,
-                                              const double2 fin_d, int lo_out) {
+                                              const double2 fin_d) {
   using L = TwLayout<LOGS, true>;
   if constexpr (r < L::R) {
-    reg_shuffle<LOGS>(x, buf, lane, cur, L::lo(r));
+    reg_shuffle<LOGS, CUR, L::lo(r)>(x, buf, lane);
     inv_round_fp<LOGS, r>(x, tw_run<LOGS, true, r>(tab, lane), last_p, q, qinv, fin_s, fin_d);
-    inv_rounds_fp<LOGS, r + 1>(x, buf, lane, L::lo(r), tab, last_p, q, qinv, fin_s, fin_d,
-                               lo_out);
+    inv_rounds_fp<LOGS, r + 1, L::lo(r)>(x, buf, lane, tab, last_p, q, qinv, fin_s, fin_d);
   } else {
-    reg_shuffle<LOGS>(x, buf, lane, cur, lo_out);
+    reg_shuffle<LOGS, CUR, LOGS - RegShape<LOGS>::EB>(x, buf, lane);
   }
 }
 
 template <int LOGS>
 __device__ __forceinline__ void fwd_sub_fp(double (&x)[RegShape<LOGS>::E], double* buf, int lane,
                                            int lo_in, int lo_out, const double2* tab, double q) {
-  fwd_rounds_fp<LOGS>(x, buf, lane, lo_in, tab, q, lo_out);
+  (void)lo_in;
+  (void)lo_out;
+  fwd_rounds_fp<LOGS>(x, buf, lane, tab, q);
 }
 
 template <int LOGS>
@@ -338,7 +360,9 @@ __device__ __forceinline__ void inv_sub_fp(double (&x)[RegShape<LOGS>::E], doubl
                                            int lo_in, int lo_out, int last_p, const double2* tab,
                                            double q, double qinv, const double2 fin_s,
                                            const double2 fin_d) {
-  inv_rounds_fp<LOGS>(x, buf, lane, lo_in, tab, last_p, q, qinv, fin_s, fin_d, lo_out);
+  (void)lo_in;
+  (void)lo_out;
+  inv_rounds_fp<LOGS>(x, buf, lane, tab, last_p, q, qinv, fin_s, fin_d);
 }
 
 }  // namespace hegpu
