@@ -70,14 +70,25 @@ def test_ntt_roundtrip_and_oracle(n):
     """Every supported size vs the oracle (reference T/test_ring.py:29-42)."""
     from oracle import scheme as S
 
-    primes = tuple(ring.generate_ntt_primes(60, 1, n) + ring.generate_ntt_primes(40, 2, n))
+    # 60-bit: integer Shoup path; 40- and 46-bit (just below 2^46, the widest
+    # lazy ranges): FP64 path (common.cuh kFpMaxBits)
+    primes = tuple(ring.generate_ntt_primes(60, 1, n) + ring.generate_ntt_primes(40, 2, n)
+                   + ring.generate_ntt_primes(46, 1, n))
     p = ring.RingParams("rt", n, primes)
-    a = ring.sample_poly(p, "uniform", 2, np.random.default_rng(1))
+    a = ring.sample_poly(p, "uniform", 3, np.random.default_rng(1))
     fwd = ring.ntt_transform(a, "forward")
     op = S.Params(n, primes, (), 2.0 ** 40, 1, None, 3.2)
     assert np.array_equal(fwd.limbs, S.ntt_fwd(op, a.limbs, primes))
     back = ring.ntt_transform(fwd, "inverse")
     assert np.array_equal(a.limbs, back.limbs)
+    # extreme residues (every coefficient q - 1, then alternating 0 / q - 1)
+    qv = np.array(primes, dtype=np.uint64)[:, None]
+    for lim in (np.broadcast_to(qv - np.uint64(1), (len(primes), n)),
+                (qv - np.uint64(1)) * (np.arange(n, dtype=np.uint64) % np.uint64(2))):
+        x = ring.RnsPoly(p, np.ascontiguousarray(lim, dtype=np.uint64), ring.COEFF, 3)
+        fx = ring.ntt_transform(x, "forward")
+        assert np.array_equal(fx.limbs, S.ntt_fwd(op, x.limbs, primes))
+        assert np.array_equal(ring.ntt_transform(fx, "inverse").limbs, x.limbs)
 
 
 def test_constant_and_wraparound():
