@@ -486,12 +486,17 @@ class TrainWorkload:
         self.w = logreg._zeros_ct(params, self.keys, top)
         self.u = logreg._zeros_ct(params, self.keys, top)
         self.it = 0
-        self.graph = None
-        if world == 1 and os.environ.get("BENCH_GRAPH", "1") == "1":
+        self.graph = self.sgraph = None
+        if os.environ.get("BENCH_GRAPH", "1") == "1":
             xb, yb = self.pool_dev[0]
-            self.graph = logreg.CapturedMinibatch(self.w, self.u, xb, yb, self.batch_rows,
-                                                  self.cfg, self.keys, self.sig, self.layout,
-                                                  self.refresher)
+            if world == 1 and os.environ.get("BENCH_SHARDED_GRAPH") != "1":
+                self.graph = logreg.CapturedMinibatch(self.w, self.u, xb, yb, self.batch_rows,
+                                                      self.cfg, self.keys, self.sig, self.layout,
+                                                      self.refresher)
+            else:  # per-rank gradient graph + owner refresh graphs, eager collectives
+                self.sgraph = logreg.CapturedShardedMinibatch(
+                    self.w, self.u, xb, yb, self.batch_rows, self.cfg, self.keys, self.sig,
+                    self.layout, self.refresher)
             # (the capture warm-up updated a throwaway copy; the state is still the initial one)
         self.units = self.batch_rows
         self.h2d = (self.host_x[0].numel() + self.host_y[0].numel()) * 8
@@ -538,6 +543,10 @@ class TrainWorkload:
             self.graph.load(xb, yb)
             self.w, self.u = self.graph.step()
             return self.w
+        if self.sgraph is not None:
+            self.sgraph.load(xb, yb)
+            self.w, self.u = self.sgraph.step()
+            return self.w
         self.w, self.u = logreg.train_minibatch(
             self.w, self.u, xb, yb, self.batch_rows, self.cfg, self.keys, self.sig, self.layout,
             self.refresher, local_shard=True)
@@ -569,6 +578,13 @@ class TrainWorkload:
             self._w_host[1].copy_(self.w.c1.data, non_blocking=True)
             self.d2h = self._w_host.numel() * 8
             return self._w_host
+        if self.sgraph is not None:
+            self.sgraph.load(self.host_x[i], self.host_y[i])  # H2D from pinned host memory
+            self.w, self.u = self.sgraph.step()
+            wh = self.w.c0.data.to("cpu")
+            wh1 = self.w.c1.data.to("cpu")
+            self.d2h = (wh.numel() + wh1.numel()) * 8
+            return wh, wh1
         xt = self.host_x[i].to("cuda", non_blocking=True)
         yt = self.host_y[i].to("cuda", non_blocking=True)
         x0, y0 = self.pool_dev[i]
@@ -594,11 +610,12 @@ class TrainWorkload:
         top = self.ctx.output_level
         zero_w = logreg._zeros_ct(self.params, self.keys, top)
         zero_u = logreg._zeros_ct(self.params, self.keys, top)
-        if self.graph is not None:
-            for dst, src in ((self.graph.w, zero_w), (self.graph.u, zero_u)):
+        g = self.graph if self.graph is not None else self.sgraph
+        if g is not None:
+            for dst, src in ((g.w, zero_w), (g.u, zero_u)):
                 dst.c0.data.copy_(src.c0.data)
                 dst.c1.data.copy_(src.c1.data)
-            self.w, self.u = self.graph.w, self.graph.u
+            self.w, self.u = g.w, g.u
         else:
             self.w, self.u = zero_w, zero_u
         self.it = 0
@@ -662,6 +679,9 @@ def run_ours(args):
     captured = getattr(wl, "captured", None)
     if captured is not None:
         launches += captured.kernels_per_run * args.steps
+    sgraph = getattr(wl, "sgraph", None)
+    if sgraph is not None:  # graph-replayed kernels (the eager ones are counted above)
+        launches += sgraph.kernels_per_step * args.steps
     ms = max_over_ranks(ms, world)
     ms_step = ms / args.steps
     # end to end through the public API with host buffers
