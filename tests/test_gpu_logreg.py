@@ -159,3 +159,48 @@ def test_ovr_multiclass_1024d_matches_reference(sigmoid15):
     enc = logreg.shadow_scores(X, got, sigmoid15, layout)
     sh = logreg.shadow_scores(X, np.asarray(shadow.weights), sigmoid15, layout)
     assert np.mean(np.argmax(enc, axis=1) == np.argmax(sh, axis=1)) >= 0.98
+
+
+def test_captured_minibatch_graphs_match_eager(sigmoid15):
+    """The bench's graph-replayed trainer steps (desk-boot, true bootstrap
+    refresh): CapturedMinibatch reproduces the eager train_minibatch limb for
+    limb; CapturedShardedMinibatch (the multi-GPU form: gradient graph, eager
+    collectives, per-owner refresh graphs), run at world size 1, decrypts like
+    it (w and u are bootstrapped separately there instead of packed)."""
+    from paper_2210_02574_b200.ckks import ops
+
+    params = ckks.get_preset("desk-boot")
+    layout = logreg.make_layout(params, 16)
+    ctx = bs.build_context(params, n_slots=layout.padded_dim, input_periodic=True)
+    steps = sorted(set(bs.refresh_rotation_steps(ctx)) | logreg.rotation_steps(layout))
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
+    ref = bs.BootstrapRefresher(ctx, keys)
+    cfg = logreg.TrainConfig(1.0, 0.9, 4 * layout.rows_per_ct, 1)
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-1, 1, (cfg.batch_size, 16))
+    y = (X @ rng.normal(size=16) > 0).astype(np.float64)
+    top = ctx.output_level
+    xs, ys = [], []
+    for c in range(4):
+        r0 = c * layout.rows_per_ct
+        xr, yr = X[r0: r0 + layout.rows_per_ct], y[r0: r0 + layout.rows_per_ct]
+        xs.append(ckks.encrypt(ckks.encode(params, logreg._pack_slots(xr, layout), top), keys,
+                               rng_seed=100 + c))
+        ys.append(ckks.encrypt(ckks.encode(params, logreg._pack_label_slots(yr, layout), 3), keys,
+                               rng_seed=200 + c))
+    xb, yb = ops.stack(xs), ops.stack(ys)
+    w0, u0 = logreg._zeros_ct(params, keys, top), logreg._zeros_ct(params, keys, top)
+    args = (cfg.batch_size, cfg, keys, sigmoid15, layout, ref)
+    we, ue = logreg.train_minibatch(w0, u0, xb, yb, *args, local_shard=True)
+    cm = logreg.CapturedMinibatch(w0, u0, xb, yb, *args)
+    cm.load(xb, yb)
+    wg, ug = cm.step()
+    assert np.array_equal(wg.c0.limbs, we.c0.limbs) and np.array_equal(ug.c1.limbs, ue.c1.limbs)
+    cs = logreg.CapturedShardedMinibatch(w0, u0, xb, yb, *args)
+    cs.load(xb, yb)
+    ws, us = cs.step()
+    for a, b in ((ws, we), (us, ue)):
+        assert a.level == b.level and a.scale == b.scale
+        # two independent bootstraps' errors (desk-boot: ~1e-3 each; the
+        # reference's bootstrap tolerance is 1e-2, T/test_bootstrap.py:23)
+        assert np.max(np.abs(ckks.decrypt_vector(a, keys) - ckks.decrypt_vector(b, keys))) < 5e-3
