@@ -418,6 +418,62 @@ class BootstrapFullWorkload:
                 "keygen_s": round(self.keygen_s, 1)}
 
 
+class PredictWorkload:
+    """cfg1: N=2^14 (P14) encrypted 768-d logistic-regression inference on one
+    ciphertext of 8 rows: step = encrypt the rows ->
+    predict (encrypted dot product + degree-15 sigmoid) -> decrypt the scores.
+    Metric: ms per inference (latency; the reference: 0.106 / 2.64 / 0.004 s)."""
+
+    metric = "encrypted LR inference ms (N=2^14, 8 rows)"
+    unit = "ms"
+    higher = False
+
+    def setup(self, rank, world):
+        from paper_2210_02574_b200 import ckks, logreg, minimax
+
+        self.params = ckks.get_preset("p14")
+        t0 = time.time()
+        self.keys = ckks.keygen(self.params, rng_seed=7)
+        self.keygen_s = time.time() - t0
+        self.layout = logreg.make_layout(self.params, 768)
+        self.sig = minimax.load_approximant("sigmoid_deg15")
+        self.X = np.random.default_rng(0).uniform(-1, 1, (8, 768))
+        w = np.random.default_rng(0).normal(0, 0.05, 768)
+        wv = np.zeros(self.layout.slot_count)
+        for b in range(self.layout.rows_per_ct):
+            wv[b * self.layout.padded_dim: b * self.layout.padded_dim + 768] = w
+        wct = ckks.encrypt_vector(self.params, wv, self.keys, rng_seed=2)
+        self.model = logreg.EncryptedModel(2, self.layout, [wct], [wct])
+        self.wpad = np.concatenate([w, np.zeros(self.layout.padded_dim - 768)])[None, :]
+        self.slots = logreg._pack_slots(self.X, self.layout)
+        self.units = 1
+        self.h2d = self.layout.slot_count * 8  # the packed rows (encoded and encrypted on device)
+        self.d2h = 0
+        self.config = {"workload": "cfg1 P14 encrypt -> 768-d LR inference -> decrypt, 1 ct",
+                       "preset": "p14", "N": self.params.ring_degree, "rows": 8}
+
+    def step(self):
+        from paper_2210_02574_b200 import ckks, logreg
+
+        ct = ckks.encrypt_vector(self.params, self.slots, self.keys, rng_seed=1)
+        self.scores = logreg.predict(self.model, [ct], self.keys, self.sig)
+        self.dec = logreg.decrypt_scores(self.scores, self.keys, self.layout, 8)
+        self.d2h = 2 * (self.scores[0][0].level + 1) * self.params.ring_degree * 8
+        return self.dec
+
+    e2e_step = step  # host rows in, host scores out: the step is already end to end
+
+    def oracle_sample(self):
+        return cost_model_sample(self.params, self.histogram, 1, "ms")
+
+    def check(self):
+        from paper_2210_02574_b200 import logreg
+
+        want = logreg.shadow_scores(self.X, self.wpad, self.sig, self.layout)
+        return {"max_abs_err_vs_shadow": float(np.max(np.abs(self.dec - want))),
+                "keygen_s": round(self.keygen_s, 1)}
+
+
 def logreg_rotation_steps(layout):
     """Rotation steps of the gradient pipeline (logreg.py:202-229): the
     reference's doubling steps plus the multiples the hoisted radix-4 rounds
@@ -632,7 +688,7 @@ class TrainWorkload:
 
 
 WORKLOADS = {"train": TrainWorkload, "ks": KsWorkload, "bootstrap": BootstrapWorkload,
-             "bootstrap_full": BootstrapFullWorkload}
+             "bootstrap_full": BootstrapFullWorkload, "predict": PredictWorkload}
 
 
 # ---------------------------------------------------------------------------
@@ -824,8 +880,9 @@ def run_reference(args):
         def to_config_text(self):
             return self.text
 
-    wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", "p16.preset"))
-    if args.config in ("train", "bootstrap", "bootstrap_full"):
+    preset = "p14" if args.config == "predict" else "p16"
+    wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", f"{preset}.preset"))
+    if args.config in ("train", "bootstrap", "bootstrap_full", "predict"):
         wl.histogram = load_histogram(args.config)
         wl.units = TrainWorkload.batch_rows if args.config == "train" else 1
     vals = []
@@ -838,7 +895,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": wl.higher, "impl": "reference", "data": "synthetic",
             "config": (wl.static_config(args.gpus) if hasattr(wl, "static_config")
-                       else {"workload": args.config, "preset": "p16"}),
+                       else {"workload": args.config, "preset": preset}),
             "cpu_baseline": {"value": round(value, 6), "unit": wl.unit,
                              "cores": os.cpu_count(), "kind": "port", "sample": sample},
             "e2e": {"value": round(value, 6), "unit": wl.unit, "h2d_bytes_per_step": 0,
