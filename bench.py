@@ -1,6 +1,7 @@
 """Benchmark of the B200 CKKS engine (driver contract: one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config train|bootstrap|ks]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--config train|ks|bootstrap|bootstrap_full|predict|ovr]
                     [--impl ours|reference]
 
 Workloads (BASELINE.json configs):
@@ -11,6 +12,11 @@ Workloads (BASELINE.json configs):
   bootstrap  cfg3: one sparse-1024 bootstrap at N=2^16.  metric: ms.
   ks         cfg2: NTT/iNTT + relinearisation key switch of 64 ciphertexts at
              the full P16 chain.  metric: key switches/sec.
+  bootstrap_full  cfg3 full-slot (ingest) bootstrap, batched.  metric: ms/ct.
+  predict    cfg1: P14 encrypt -> 768-d inference -> decrypt.  metric: ms.
+  ovr        cfg5: one One-vs-Rest minibatch of 4 class-models on 1024-d
+             embeddings (32 ciphertexts x 16 rows), each class's update and
+             sparse-2048 refresh.  metric: samples/sec (4 class-models).
 --impl reference times the reference algorithm's CPU path (the oracle port,
 oracle/, C+OpenMP kernels, all host cores) on a bounded sample.
 """
@@ -687,8 +693,182 @@ class TrainWorkload:
                 "diag_cache_gib": round(diag_gib(self.ctx), 2)}
 
 
+class OvrWorkload(TrainWorkload):
+    """cfg5 (AG-News-sized synthetic 1024-d embeddings, 4 classes, P16): one
+    minibatch of One-vs-Rest training (the reference's multi-class semantics,
+    logreg.py:325-331, 393-398) = the same 32 data ciphertexts x 16 rows
+    (batch 512) against the 4 classes' label ciphertexts, each class's
+    Nesterov update and its packed sparse-2048 bootstrap refresh of w and u.
+    A step updates all 4 class-models; samples/s counts rows (each row
+    updates every class).  Classes are independent (no exchange): under
+    torchrun the classes are dealt round-robin to the ranks (N <= 4)."""
+
+    metric = "encrypted OvR train samples/sec (4 class-models)"
+    n_pool = 2
+    n_classes = 4
+    dim = 1024
+
+    def setup(self, rank, world):
+        import torch
+
+        from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg, minimax
+        from paper_2210_02574_b200.ckks import ops
+        from paper_2210_02574_b200.synth import make_blob_embeddings
+
+        if world > self.n_classes:
+            raise SystemExit(f"ovr: classes are the sharded axis, at most {self.n_classes} ranks")
+        self.params = params = p16()
+        self.sig = minimax.load_approximant("sigmoid_deg15")
+        self.layout = logreg.make_layout(params, self.dim)
+        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True)
+        steps = sorted(set(bs.refresh_rotation_steps(self.ctx)) | logreg_rotation_steps(self.layout))
+        t0 = time.time()
+        self.keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
+        self.keygen_s = time.time() - t0
+        self.refresher = bs.BootstrapRefresher(self.ctx, self.keys)
+        self.cfg = logreg.TrainConfig(0.5, 0.9, self.batch_rows, 1)  # T/test_acceptance.py:151-154
+        self.mine = [c for c in range(self.n_classes) if c % world == rank]
+        rpc = self.layout.rows_per_ct
+        n_per_class = self.batch_rows * self.n_pool // self.n_classes
+        X, y = make_blob_embeddings(np.random.default_rng(200), n_per_class, self.n_classes,
+                                    dim=self.dim)
+        self.X, self.y = X, y
+        top = self.ctx.output_level
+        self.pool_dev = []
+        for b in range(self.n_pool):
+            xs, ys = [], {c: [] for c in self.mine}
+            for i in range(self.batch_rows // rpc):
+                r0 = b * self.batch_rows + i * rpc
+                xs.append(ckks.encrypt(
+                    ckks.encode(params, logreg._pack_slots(X[r0 : r0 + rpc], self.layout), top),
+                    self.keys, rng_seed=30_000 + b * 1000 + i))
+                for c in self.mine:
+                    yc = (y[r0 : r0 + rpc] == c).astype(np.float64)
+                    ys[c].append(ckks.encrypt(
+                        ckks.encode(params, logreg._pack_label_slots(yc, self.layout), 3),
+                        self.keys, rng_seed=40_000 + b * 1000 + c * 100 + i))
+            self.pool_dev.append((ops.stack(xs), {c: ops.stack(ys[c]) for c in self.mine}))
+        self.host_x = [torch.stack([xb.c0.data, xb.c1.data], dim=1).cpu().pin_memory()
+                       for xb, _ in self.pool_dev]
+        self.host_y = [{c: torch.stack([yb[c].c0.data, yb[c].c1.data], dim=1).cpu().pin_memory()
+                        for c in self.mine} for _, yb in self.pool_dev]
+        self.w = {c: logreg._zeros_ct(params, self.keys, top) for c in self.mine}
+        self.u = {c: logreg._zeros_ct(params, self.keys, top) for c in self.mine}
+        self.it = 0
+        xb, yb = self.pool_dev[0]
+        # one captured minibatch per class (independent state, same data shape)
+        # (replayed in capture order every step, so they share one graph pool)
+        self.graphs, pool = {}, None
+        for c in self.mine:
+            g = logreg.CapturedMinibatch(self.w[c], self.u[c], xb, yb[c], self.batch_rows,
+                                         self.cfg, self.keys, self.sig, self.layout,
+                                         self.refresher, pool=pool)
+            self.graphs[c], pool = g, g.pool
+        self.graph = self.sgraph = None
+        import types
+
+        self.captured = types.SimpleNamespace(
+            kernels_per_run=sum(g.kernels_per_step for g in self.graphs.values()))
+        self.units = self.batch_rows
+        self.h2d = (self.host_x[0].numel() + sum(t.numel() for t in self.host_y[0].values())) * 8
+        self.d2h = 0
+        self.config = self.static_config(world)
+        self.config["rotation_keys"] = len(steps)
+        self.config["classes_on_this_rank"] = self.mine
+
+    @classmethod
+    def static_config(cls, world):
+        return {
+            "workload": "cfg5 encrypted One-vs-Rest training minibatch (AG-News-shaped "
+                        "synthetic 1024-d, 4 classes)",
+            "preset": "p16", "N": 65536, "batch_rows": cls.batch_rows,
+            "classes": cls.n_classes, "ciphertexts_per_minibatch": cls.batch_rows // 16,
+            "rows_per_ct": 16,
+            "refresh": "per class: w and u refreshed together, one packed sparse bootstrap "
+                       "of period 4096 (two of period 2048 in the reference)",
+            "parallelism": f"classes dealt round-robin over {world} GPU(s), no exchange",
+            "l2": "keys and diagonals exceed L2"}
+
+    def profile_step(self):
+        from paper_2210_02574_b200 import logreg
+
+        import torch
+
+        torch.cuda.empty_cache()  # the eager step allocates outside the graph pool
+        xb, yb = self.pool_dev[self.it % self.n_pool]
+        self.it += 1
+        for c, g in self.graphs.items():
+            w, u = logreg.train_minibatch(g.w, g.u, xb, yb[c], self.batch_rows, self.cfg,
+                                          self.keys, self.sig, self.layout, self.refresher,
+                                          local_shard=True)
+            for dst, src in ((g.w, w), (g.u, u)):
+                dst.c0.data.copy_(src.c0.data)
+                dst.c1.data.copy_(src.c1.data)
+
+    def step(self):
+        xb, yb = self.pool_dev[self.it % self.n_pool]
+        self.it += 1
+        for c, g in self.graphs.items():
+            g.load(xb, yb[c])
+            self.w[c], self.u[c] = g.step()
+        return self.w
+
+    def e2e_step(self):
+        """Public-API step from pinned host buffers: the data ciphertexts are
+        copied H2D once (into the first class's graph, then device-to-device
+        into the others), each class's labels once; every class's refreshed w
+        is read back."""
+        import torch
+
+        i = self.it % self.n_pool
+        self.it += 1
+        first = None
+        for c, g in self.graphs.items():
+            if first is None:
+                g.load(self.host_x[i], self.host_y[i][c])
+                first = g
+            else:
+                g.load(first.x, self.host_y[i][c])
+            self.w[c], self.u[c] = g.step()
+        if getattr(self, "_w_host", None) is None:
+            w0 = next(iter(self.w.values()))
+            self._w_host = torch.empty((len(self.w), 2) + tuple(w0.c0.data.shape),
+                                       dtype=w0.c0.data.dtype, pin_memory=True)
+        for k, c in enumerate(self.mine):
+            self._w_host[k, 0].copy_(self.w[c].c0.data, non_blocking=True)
+            self._w_host[k, 1].copy_(self.w[c].c1.data, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.d2h = self._w_host.numel() * 8
+        return self._w_host
+
+    def check(self):
+        """From w = u = 0 every class applies the first minibatch; decrypted
+        weights against the plaintext OvR shadow trainer (T/test_acceptance.py:
+        151-171 protocol)."""
+        from paper_2210_02574_b200 import ckks, logreg
+
+        top = self.ctx.output_level
+        for g in self.graphs.values():
+            for dst in (g.w, g.u):
+                z = logreg._zeros_ct(self.params, self.keys, top)
+                dst.c0.data.copy_(z.c0.data)
+                dst.c1.data.copy_(z.c1.data)
+        self.it = 0
+        self.step()
+        sh = logreg.shadow_train(self.X[: self.batch_rows], self.y[: self.batch_rows], self.cfg,
+                                 self.sig, class_count=self.n_classes, layout=self.layout)
+        err = 0.0
+        for c in self.mine:
+            w = ckks.decrypt_vector(self.w[c], self.keys)[: self.layout.padded_dim]
+            err = max(err, float(np.max(np.abs(w - sh.weights[c]))))
+        return {"weights_vs_shadow_max_abs": err, "validation_minibatches": 1,
+                "keygen_s": round(self.keygen_s, 1),
+                "diag_cache_gib": round(diag_gib(self.ctx), 2)}
+
+
 WORKLOADS = {"train": TrainWorkload, "ks": KsWorkload, "bootstrap": BootstrapWorkload,
-             "bootstrap_full": BootstrapFullWorkload, "predict": PredictWorkload}
+             "bootstrap_full": BootstrapFullWorkload, "predict": PredictWorkload,
+             "ovr": OvrWorkload}
 
 
 # ---------------------------------------------------------------------------
@@ -882,9 +1062,9 @@ def run_reference(args):
 
     preset = "p14" if args.config == "predict" else "p16"
     wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", f"{preset}.preset"))
-    if args.config in ("train", "bootstrap", "bootstrap_full", "predict"):
+    if args.config in ("train", "bootstrap", "bootstrap_full", "predict", "ovr"):
         wl.histogram = load_histogram(args.config)
-        wl.units = TrainWorkload.batch_rows if args.config == "train" else 1
+        wl.units = TrainWorkload.batch_rows if args.config in ("train", "ovr") else 1
     vals = []
     for i in range(args.warmup + args.steps):
         v, sample = wl.oracle_sample()

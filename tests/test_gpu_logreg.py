@@ -196,6 +196,25 @@ def test_captured_minibatch_graphs_match_eager(sigmoid15):
     cm.load(xb, yb)
     wg, ug = cm.step()
     assert np.array_equal(wg.c0.limbs, we.c0.limbs) and np.array_equal(ug.c1.limbs, ue.c1.limbs)
+    # the OvR bench form: a second class's graph shares the first one's pool
+    # (replayed in capture order); each stays bit-exact with its eager update
+    yb2 = ops.stack([ckks.encrypt(ckks.encode(params, logreg._pack_label_slots(
+        1.0 - y[c * layout.rows_per_ct: (c + 1) * layout.rows_per_ct], layout), 3), keys,
+        rng_seed=300 + c) for c in range(4)])
+    we2, ue2 = logreg.train_minibatch(w0, u0, xb, yb2, *args, local_shard=True)
+    cm2 = logreg.CapturedMinibatch(w0, u0, xb, yb2, *args, pool=cm.pool)
+    for _ in range(2):  # the second round replays over the first round's intermediates
+        for g in (cm, cm2):
+            for dst, src in ((g.w, w0), (g.u, u0)):
+                dst.c0.data.copy_(src.c0.data)
+                dst.c1.data.copy_(src.c1.data)
+        cm.load(xb, yb)
+        wg, ug = cm.step()
+        cm2.load(cm.x, yb2)
+        wg2, ug2 = cm2.step()
+        assert np.array_equal(wg.c0.limbs, we.c0.limbs) and np.array_equal(ug.c1.limbs, ue.c1.limbs)
+        assert np.array_equal(wg2.c0.limbs, we2.c0.limbs)
+        assert np.array_equal(ug2.c1.limbs, ue2.c1.limbs)
     cs = logreg.CapturedShardedMinibatch(w0, u0, xb, yb, *args)
     cs.load(xb, yb)
     ws, us = cs.step()
