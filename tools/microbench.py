@@ -61,7 +61,7 @@ def bench_bsgs(params):
         ptrs = (ctypes.c_void_p * n_terms)(*[babies[t].data_ptr() for t in range(n_terms)])
         idx = torch.arange(n_giants * n_terms, dtype=torch.int32, device="cuda") % 2048
         out = torch.empty((n_giants, nb, 2, k, n), dtype=torch.int64, device="cuda")
-        for lr in (0, 4):
+        for lr in (0, 3, 4):
             pts = rand_limbs(params, (2048, k, n >> lr), k)
             f = lambda: _lib.call("hegpu_bsgs", ring, ptrs, n_terms, k * n, 2 * k * n, nb,
                                   pts.data_ptr(), k * (n >> lr), lr, idx.data_ptr(), n_giants,
