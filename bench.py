@@ -698,7 +698,8 @@ class OvrWorkload(TrainWorkload):
     minibatch of One-vs-Rest training (the reference's multi-class semantics,
     logreg.py:325-331, 393-398) = the same 32 data ciphertexts x 16 rows
     (batch 512) against the 4 classes' label ciphertexts, each class's
-    Nesterov update and its packed sparse-2048 bootstrap refresh of w and u.
+    Nesterov update and its sparse-2048 bootstrap refresh of w and u (one
+    batch of two).
     A step updates all 4 class-models; samples/s counts rows (each row
     updates every class).  Classes are independent (no exchange): under
     torchrun the classes are dealt round-robin to the ranks (N <= 4)."""
@@ -784,8 +785,8 @@ class OvrWorkload(TrainWorkload):
             "preset": "p16", "N": 65536, "batch_rows": cls.batch_rows,
             "classes": cls.n_classes, "ciphertexts_per_minibatch": cls.batch_rows // 16,
             "rows_per_ct": 16,
-            "refresh": "per class: w and u refreshed together, one packed sparse bootstrap "
-                       "of period 4096 (two of period 2048 in the reference)",
+            "refresh": "per class: w and u refreshed as one batch of two sparse-2048 "
+                       "bootstraps (pair packing stops at period 1024: bootstrap.PACKED_PAIR_MAX_SLOTS)",
             "parallelism": f"classes dealt round-robin over {world} GPU(s), no exchange",
             "l2": "keys and diagonals exceed L2"}
 

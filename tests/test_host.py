@@ -195,3 +195,20 @@ def test_pcg64_advance_matches_numpy():
     g.integers(0, 0xffffe80001, size=1000, dtype=np.uint64)
     assert rg.pcg64_advance_state(st["state"], st["inc"], 1000) == \
         g.bit_generator.state["state"]["state"]
+
+
+def test_pair_packing_stops_at_period_1024():
+    """refresh_many packs w and u into one bootstrap of twice the period only
+    up to n = 1024 slots (cfg4); at n = 2048 (cfg5 OvR) the packed transforms
+    cost more than a batch of two (bootstrap.PACKED_PAIR_MAX_SLOTS)."""
+    from types import SimpleNamespace
+
+    from paper_2210_02574_b200 import bootstrap as bs
+
+    params = SimpleNamespace(slot_count=32768)
+    def ctx(n, **kw):
+        return SimpleNamespace(params=params, n_slots=n, is_full=kw.get("full", False),
+                               input_periodic=kw.get("periodic", True))
+    assert bs._pair_packable_ctx(ctx(64)) and bs._pair_packable_ctx(ctx(1024))
+    assert not bs._pair_packable_ctx(ctx(2048))
+    assert not bs._pair_packable_ctx(ctx(1024, periodic=False))
