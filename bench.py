@@ -101,7 +101,31 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        """NVML queries take microseconds (an nvidia-smi process ~100 ms), so
+        even a sub-second timed region gets many samples.  Same row format."""
+        import pynvml as nv
+
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(smax), ""] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.02)
+        finally:
+            nv.nvmlShutdown()
+
     def _run(self):
+        try:
+            return self._run_nvml()
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
