@@ -112,6 +112,7 @@ class ClockSampler:
             smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
             bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                     nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self._ready.set()  # NVML is up: sampling starts with the timed region
             while not self._stop.is_set():
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
@@ -126,6 +127,7 @@ class ClockSampler:
             return self._run_nvml()
         except Exception:
             pass
+        self._ready.set()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -139,8 +141,10 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        self._ready = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=10)  # short timed regions: NVML init happens before them
         return self
 
     def __exit__(self, *exc):
