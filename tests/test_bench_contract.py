@@ -33,3 +33,20 @@ def test_reference_arm_nonzero_rank_is_silent():
         capture_output=True, text=True, timeout=120, cwd=REPO, env=env,
     )
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_clock_summary_flags_throttle_reasons():
+    """The clocks object of the bench line: median SM clock under load, max
+    clock, and every throttle reason seen in any sample (rows as the NVML and
+    nvidia-smi samplers record them)."""
+    sys.path.insert(0, REPO)
+    import bench
+
+    c = bench.ClockSampler(0)
+    c.samples = [["1965", "1965", "", "Not Active", "Not Active", "Not Active", "Not Active"],
+                 ["1950", "1965", "", "Not Active", "Not Active", "Not Active", "Active"],
+                 ["1965", "1965", "", "Active", "Not Active", "Not Active", "Not Active"]]
+    s = c.summary()
+    assert s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0 and s["samples"] == 3
+    assert s["reasons"] == ["hw_slowdown", "sw_power_cap"]
+    assert bench.ClockSampler(0).summary()["reasons"] == ["unsampled"]
