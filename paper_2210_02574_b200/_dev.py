@@ -111,3 +111,60 @@ def ext_primes(level, n_chain, n_special):
         ("ext", level, n_chain, n_special),
         list(range(level + 1)) + [n_chain + i for i in range(n_special)],
     )
+
+
+class PtCache:
+    """Bounded LRU cache of device plaintexts (encoded masks and constants).
+
+    Keys may carry per-input values (a bootstrap's scale correction), so an
+    unbounded dict grows with every distinct input scale.  Entries read while
+    a CUDA graph is captured must outlive the graph: captured objects keep
+    the list `pin_cached()` returns (every live entry at capture time)."""
+
+    _ALL = []
+
+    def __init__(self, maxsize=64):
+        from collections import OrderedDict
+
+        self.maxsize = maxsize
+        self._d = OrderedDict()
+        PtCache._ALL.append(self)
+
+    def get(self, key):
+        v = self._d.get(key)
+        if v is not None:
+            self._d.move_to_end(key)
+            _note_capture(v)
+        return v
+
+    def __setitem__(self, key, value):
+        self._d[key] = value
+        self._d.move_to_end(key)
+        _note_capture(value)
+        while len(self._d) > self.maxsize:
+            self._d.popitem(last=False)
+
+    def __getitem__(self, key):
+        return self._d[key]
+
+    def __len__(self):
+        return len(self._d)
+
+    def clear(self):
+        self._d.clear()
+
+
+_CAPTURE_REFS = []
+
+
+def _note_capture(v):
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+        _CAPTURE_REFS.append(v)
+
+
+def pin_cached():
+    """Strong references to every cached plaintext plus every one read during
+    the capture that just ended (held by captured graphs)."""
+    refs = [v for c in PtCache._ALL for v in c._d.values()] + _CAPTURE_REFS
+    _CAPTURE_REFS.clear()
+    return refs

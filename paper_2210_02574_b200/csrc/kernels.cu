@@ -17,6 +17,7 @@ struct EwParams {
   int64_t as, bs, os;
   int k;
   int log_n;
+  int rows;  // n_polys * k: the last grid.z slice may overhang
   const PrimeConst* pc;
   uint8_t sel[kMaxPrimes];
   uint64_t c[kMaxPrimes];
@@ -28,6 +29,7 @@ template <int OP>
 __global__ void __launch_bounds__(kEwThreads) k_elementwise(const __grid_constant__ EwParams P) {
   const int N = 1 << P.log_n;
   const int row = blockIdx.y + blockIdx.z * 65535;
+  if (row >= P.rows) return;
   const int poly = row / P.k, limb = row - poly * P.k;
   const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
   if (x >= N) return;
@@ -103,6 +105,7 @@ void launch_elementwise(const PrimeConst* dpc, const std::vector<uint64_t>& hq, 
   P.os = A.os;
   P.k = A.k;
   P.log_n = log_n;
+  P.rows = rows;
   P.pc = dpc;
   for (int l = 0; l < A.k; ++l) {
     const int p = A.primes[l];
@@ -195,6 +198,7 @@ void launch_lift_signed(const PrimeConst* dpc, int log_n, const int64_t* src, in
                         uint64_t* out, int64_t os, int n_polys, int k, const int32_t* primes,
                         cudaStream_t st) {
   if (n_polys == 0 || k == 0) return;
+  if (n_polys > 65535) throw HegpuError{HEGPU_E_ARG, "lift batch exceeds 65535 polys"};
   LiftParams P;
   P.src = src;
   P.ss = ss;
@@ -216,6 +220,7 @@ void launch_lift_centered(const PrimeConst* dpc, int log_n, const uint64_t* src,
                           uint64_t src_q, uint64_t* out, int64_t os, int n_polys, int k,
                           const int32_t* primes, cudaStream_t st) {
   if (n_polys == 0 || k == 0) return;
+  if (n_polys > 65535) throw HegpuError{HEGPU_E_ARG, "lift batch exceeds 65535 polys"};
   LiftParams P;
   P.src = src;
   P.ss = ss;
@@ -243,6 +248,7 @@ struct AutoParams {
   int64_t is, os;
   int k;
   int log_n;
+  int rows;  // n_polys * k: the last grid.z slice may overhang
   uint64_t g;  // odd, reduced mod 2N
   const PrimeConst* pc;
   uint8_t sel[kMaxPrimes];
@@ -255,6 +261,7 @@ struct AutoParams {
 __global__ void __launch_bounds__(kEwThreads) k_auto_eval(const __grid_constant__ AutoParams P) {
   const int log_n = P.log_n, N = 1 << log_n;
   const int row = blockIdx.y + blockIdx.z * 65535;
+  if (row >= P.rows) return;
   const int i = blockIdx.x * kEwThreads + threadIdx.x;
   if (i >= N) return;
   const uint32_t mask2n = (2u << log_n) - 1u;
@@ -270,6 +277,7 @@ __global__ void __launch_bounds__(kEwThreads) k_auto_eval(const __grid_constant_
 __global__ void __launch_bounds__(kEwThreads) k_auto_coeff(const __grid_constant__ AutoParams P) {
   const int log_n = P.log_n, N = 1 << log_n;
   const int row = blockIdx.y + blockIdx.z * 65535;
+  if (row >= P.rows) return;
   const int j = blockIdx.x * kEwThreads + threadIdx.x;
   if (j >= N) return;
   const int poly = row / P.k, limb = row - poly * P.k;
@@ -293,6 +301,7 @@ void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint6
   P.os = os;
   P.k = k;
   P.log_n = log_n;
+  P.rows = rows;
   P.g = g & ((2ull << log_n) - 1ull);
   if ((P.g & 1ull) == 0) throw HegpuError{HEGPU_E_ARG, "automorphism exponent must be odd"};
   P.pc = dpc;
@@ -316,6 +325,7 @@ void launch_automorphism(const PrimeConst* dpc, int log_n, bool eval_form, uint6
 __global__ void __launch_bounds__(kEwThreads) k_tensor(const __grid_constant__ TensorParams P) {
   const int N = 1 << P.log_n;
   const int row = blockIdx.y + blockIdx.z * 65535;
+  if (row >= P.rows) return;
   const int poly = row / P.k, limb = row - poly * P.k;
   const int x = blockIdx.x * kEwThreads + threadIdx.x;
   if (x >= N) return;
@@ -338,6 +348,7 @@ void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int
   const int rows = n_polys * T0.k;
   if (rows == 0) return;
   TensorParams T = T0;
+  T.rows = rows;
   T.pc = dpc;
   T.log_n = log_n;
   const dim3 grid = rows_grid(1 << log_n, rows, 1);
@@ -818,6 +829,7 @@ void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
                ipn * 8.0 * P.n_rot * (2.0 * P.beta + P.n_batch * P.beta) +
                    ipn * 8.0 * 2.0 * P.n_batch * (P.sum_mode ? 1 : P.n_rot),
                ipn * P.n_batch * P.n_rot * 2.0 * P.beta);
+  if (launch_ks_ip_rot_tma(P, st)) return;
   if (bg == 4)
     launch_ip_rot_bg<4>(P, grid, st);
   else if (bg == 2)
@@ -837,12 +849,14 @@ struct AutoSumParams {
   int64_t os;
   uint32_t gal[kMaxRot];
   int n_rot, k, log_n;
+  int rows;  // n_polys * k: the last grid.z slice may overhang
   const PrimeConst* pc;
 };
 
 __global__ void __launch_bounds__(kEwThreads) k_auto_sum(const __grid_constant__ AutoSumParams P) {
   const int N = 1 << P.log_n;
   const int row = blockIdx.y + blockIdx.z * 65535;
+  if (row >= P.rows) return;
   const int x = blockIdx.x * kEwThreads + threadIdx.x;
   if (x >= N) return;
   const int poly = row / P.k, limb = row - poly * P.k;
@@ -875,6 +889,8 @@ void launch_auto_sum(const PrimeConst* dpc, int log_n, const uint32_t* gal, int 
   P.log_n = log_n;
   P.pc = dpc;
   const int rows = n_polys * k;
+  if (rows == 0) return;
+  P.rows = rows;
   const dim3 grid = rows_grid(1 << log_n, rows, 1);
   ProfScope ps(PROF_AUTOMORPHISM, st, (double)rows * (1 << log_n) * 8.0 * (n_rot + 2), 0.0);
   k_auto_sum<<<grid, kEwThreads, 0, st>>>(P);
@@ -887,6 +903,33 @@ void launch_ks_ip(IpParams& P, cudaStream_t st) {
   const double ipn = (double)(1 << P.log_n) * P.n_ext;
   ProfScope ps(PROF_KS_IP, st, ipn * 8.0 * (2.0 * P.beta + P.n_batch * (P.beta + 2.0)),
                ipn * P.n_batch * (2.0 * P.beta + 4));
+  {  // TMA-staged key streaming: the same inner product as one "rotation" by g = 1
+    IpRotParams R{};
+    R.d = P.d;
+    R.ds = P.ds;
+    R.ext = P.ext;
+    R.ext_sb = P.ext_sb;
+    R.ext_sj = P.ext_sj;
+    for (int j = 0; j < P.beta && j < kMaxRotDigits; ++j) {
+      R.kb[0][j] = P.kb[j];
+      R.ka[0][j] = P.ka[j];
+    }
+    R.gal[0] = 1;
+    R.n_rot = 1;
+    R.accumulate = P.accumulate;
+    R.acc = P.acc;
+    R.acc_sb = P.acc_sb;
+    R.level = P.level;
+    R.alpha = P.alpha;
+    R.beta = P.beta;
+    R.n_ext = P.n_ext;
+    R.n_chain = P.n_chain;
+    R.key_sp_row0 = P.key_sp_row0;
+    R.n_batch = P.n_batch;
+    R.log_n = P.log_n;
+    R.pc = P.pc;
+    if (P.beta <= kMaxRotDigits && launch_ks_ip_rot_tma(R, st)) return;
+  }
   if (P.beta <= 2) k_ks_ip<2><<<grid, kEwThreads, 0, st>>>(P);
   else if (P.beta <= 4) k_ks_ip<4><<<grid, kEwThreads, 0, st>>>(P);
   else if (P.beta <= 8) k_ks_ip<8><<<grid, kEwThreads, 0, st>>>(P);

@@ -216,6 +216,7 @@ struct TensorParams {
   int64_t as, bs, ds;
   int amod;  // operand a of poly p is a[(p % amod) * as] (periodic broadcast)
   int k, log_n;
+  int rows;  // n_polys * k (set by launch_tensor): the last grid.z slice may overhang
   const PrimeConst* pc;
 };
 
@@ -270,6 +271,8 @@ struct IpRotParams {
   uint64_t pm[kMaxPrimes], pm_sh[kMaxPrimes];  // P mod q_r, Shoup
 };
 void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st);
+// TMA-staged variant (ks_tma.cu); false when it does not apply
+bool launch_ks_ip_rot_tma(const IpRotParams& P, cudaStream_t st);
 // out[b] = base[b] + sum_r sigma_r(in[b] + r*in_sr) (eval form, k limbs;
 // base = the unpermuted in when null).  Limbs >= kq are special primes
 // n_chain + (limb - kq) (extended-basis operands); kq < 0: all chain.

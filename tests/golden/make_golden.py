@@ -275,6 +275,98 @@ def ovr_fixture():
     return {"train_seconds": tt}
 
 
+def boot_p16_sparse_fixture():
+    """P16 (N=2^16) sparse-1024 periodic bootstrap of one seeded ciphertext: the
+    reference's own decrypted output and error (SURVEY.md 8(d) cfg3;
+    bootstrap.py:278-349).  The GPU test bootstraps the same (bit-exact)
+    ciphertext and must be within 1e-3 and no worse than 2x this error."""
+    params = load_preset("p16")
+    ctx = bs.build_context(params, n_slots=1024, input_periodic=True)
+    steps = sorted(set(ctx.required_rotation_steps()))
+    t0 = time.time()
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
+    tk = time.time() - t0
+    v = np.tile(np.random.default_rng(1002).uniform(-1, 1, 1024), params.slot_count // 1024)
+    ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=21)
+    t0 = time.time()
+    out = bs.bootstrap(ct, ctx, keys)
+    tb = time.time() - t0
+    dec = ckks.decrypt_vector(out, keys)
+    np.savez_compressed(os.path.join(HERE, "boot_p16_sparse.npz"), v=v[:1024], dec=dec[:1024])
+    return {"steps": steps, "keygen_seconds": tk, "bootstrap_seconds": tb, "enc": ct_digest(ct),
+            "out_level": out.level, "out_scale": float(out.scale).hex(),
+            "err": float(np.max(np.abs(dec - v)))}
+
+
+def logreg_p16_fixture():
+    """cfg4 shape at P16 (768-d rows, 32 rows per ciphertext): 8 minibatches of
+    64 rows trained by the reference with its debug refresher, plus the shadow
+    trainer's weights and held-out accuracies (logreg.py:290-417;
+    test_acceptance.py:98-131 pattern)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "ref_conftest", "/root/reference/pkg/tests/conftest.py")
+    rc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rc)
+    params = load_preset("p16")
+    X, y = rc.make_separable(np.random.default_rng(100), 1024, dim=768, margin=0.5)
+    Xtr, ytr, Xte, yte = X[:512], y[:512], X[512:], y[512:]
+    layout = logreg.make_layout(params, 768)
+    keys = ckks.keygen(params, rotation_steps=sorted(set(ckks.default_rotation_steps(params))),
+                       rng_seed=7)
+    pairs = logreg.pack_batch(Xtr, ytr, layout, params, keys)
+    cfg = logreg.TrainConfig(1.0, 0.9, 64, 1)
+    sig = _sigmoid15()
+
+    class LevelDebugRefresher:
+        """bootstrap.debug_refresh (bootstrap.py:352-369) re-encrypting at the
+        sparse bootstrap's output level L-10 instead of the top: at P16 the
+        top prime is 60 bits and the reference's own level alignment of
+        top-level ciphertexts overflows encode_const (ops.py:55-61)."""
+
+        insecure = True
+        output_level = params.max_level - 10
+
+        def refresh(self, ct):
+            from hebert.ckks.encoding import decode_real, encode
+
+            vals = decode_real(ops.decrypt(ct, keys))
+            out = ops.encrypt(encode(params, vals, self.output_level, params.default_scale), keys)
+            out.insecure_provenance = True
+            return out
+
+    t0 = time.time()
+    model, timing = logreg.train(pairs, len(ytr), cfg, params, keys, sig, LevelDebugRefresher(),
+                                 layout=layout)
+    tt = time.time() - t0
+    got = logreg.decrypted_weights(model, keys)
+    shadow = logreg.shadow_train(Xtr, ytr, cfg, sig, layout=layout)
+
+    def acc(w):
+        s = logreg.shadow_scores(Xte, w, sig, layout)
+        return float(np.mean((np.asarray(s) > 0.5).astype(int).ravel() == yte))
+
+    np.savez_compressed(os.path.join(HERE, "logreg_p16.npz"), X=X, y=y,
+                        ref_weights=got, shadow_weights=np.asarray(shadow.weights))
+    return {"train_seconds": tt, "epoch_seconds": timing[0]["seconds"],
+            "ref_acc": acc(got), "shadow_acc": acc(shadow.weights),
+            "w_gap": float(np.max(np.abs(got - shadow.weights))),
+            "domain_breaches": int(shadow.domain_breaches)}
+
+
+def sine_artifact():
+    """The EvalMod sine the reference fits at runtime for h = 64 (K = 14,
+    bootstrap.py:98-107), shipped as paper_2210_02574_b200/approximants/
+    sine2pi_k14_deg119.txt so the engine evaluates the reference's exact
+    polynomial."""
+    poly = minimax.remez_fit("sine2pi", (-14.5, 14.5), 119)
+    path = os.path.join(REPO, "paper_2210_02574_b200", "approximants", "sine2pi_k14_deg119.txt")
+    with open(path, "w") as fh:
+        fh.write(minimax.export_text(poly))
+    return [float(c).hex() for c in poly.cheb_coeffs]
+
+
 def logreg_fixture():
     params = ckks.get_preset("desk")
     keys = ckks.keygen(params, rng_seed=7)
@@ -299,7 +391,10 @@ def main():
     t0 = time.time()
     only = {"boot_full": ("boot_desk_full", boot_full_fixture),
             "predict_p14": ("predict_p14", predict_p14_fixture),
-            "ovr": ("ovr_desk", ovr_fixture)}
+            "ovr": ("ovr_desk", ovr_fixture),
+            "boot_p16_sparse": ("boot_p16_sparse", boot_p16_sparse_fixture),
+            "logreg_p16": ("logreg_p16", logreg_p16_fixture),
+            "sine_artifact": ("sine_artifact", sine_artifact)}
     if sys.argv[1:] and sys.argv[1] in only:  # add / refresh only these entries
         path = os.path.join(HERE, "digests.json")
         digests = json.load(open(path))

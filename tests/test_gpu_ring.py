@@ -207,3 +207,32 @@ def test_pcg64_uniform_device_matches_numpy():
         assert dev_rng.bit_generator.state == host_rng.bit_generator.state
         assert np.array_equal(dev_rng.normal(size=5), host_rng.normal(size=5))
         assert np.array_equal(dev_rng.integers(-1, 2, size=9), host_rng.integers(-1, 2, size=9))
+
+
+def test_row_grid_overhang_guard():
+    """n_polys * k just above 65535 rows (grid.z = 2 with a partial last slice):
+    every row is computed and nothing past the output is written."""
+    import torch
+
+    g = golden_npz("ring_n64.npz")
+    primes = tuple(int(x) for x in g["primes"])
+    p = ring.RingParams("r64", 64, primes)
+    k, n = 3, 64
+    cnt = 65535 // k + 2  # 21847 polys -> 65541 rows
+    rng = np.random.default_rng(9)
+    q = np.array(primes, dtype=np.uint64)[None, :, None]
+    a_h = (rng.integers(0, 1 << 62, (cnt, k, n), dtype=np.uint64) % q)
+    b_h = (rng.integers(0, 1 << 62, (cnt, k, n), dtype=np.uint64) % q)
+    a = ring.RnsPoly(p, a_h, ring.EVAL, 2)
+    b = ring.RnsPoly(p, b_h, ring.EVAL, 2)
+    # output with a sentinel tail: the guard must keep the overhanging slice out
+    big = torch.full((cnt + 1, k, n), -1, dtype=torch.int64, device=a.data.device)
+    out = big[:cnt]
+    ring._binary(ring._lib.OP_ADD, a, b, out=out)
+    got = out.cpu().numpy().view(np.uint64)
+    want = (a_h + b_h) % q
+    assert np.array_equal(got, want)
+    assert bool((big[cnt] == -1).all())
+    s = ring.poly_automorphism_eval(a, 5)
+    assert np.array_equal(s.limbs[-1], ring.poly_automorphism_eval(
+        ring.RnsPoly(p, a_h[-1], ring.EVAL, 2), 5).limbs)

@@ -72,6 +72,39 @@ def bench_bsgs(params):
             del pts
 
 
+def bench_ip(params):
+    """Key-switch inner products (ks_ip class) of a relinearising mult and a
+    15-rotation hoisted rotate-and-sum, batched, at two levels."""
+    from paper_2210_02574_b200.ckks import ops
+
+    steps = list(range(1, 16))
+    keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
+    rng = np.random.default_rng(3)
+    only = os.environ.get("IP_ONLY")  # e.g. "rotsum15:21:16"
+    for lvl in (21, 11):
+        for B in (1, 4, 16):
+            if only and not any(o.endswith(f":{lvl}:{B}") for o in only.split(",")):
+                continue
+            cts = [ckks.encrypt_vector(params, rng.uniform(-1, 1, params.slot_count), keys,
+                                       level=lvl, rng_seed=i) for i in range(B)]
+            ct = cts[0] if B == 1 else ops.stack(cts)
+            for name, fn in (("mult", lambda: ops.mult(ct, ct, keys, rescale_after=False)),
+                             ("rotsum15", lambda: ops.rotate_sum(ct, steps, keys))):
+                if only and f"{name}:{lvl}:{B}" not in only.split(","):
+                    continue
+                fn()
+                torch.cuda.synchronize()
+                _lib.profile_enable(True)
+                for _ in range(5):
+                    fn()
+                prof = _lib.profile_read()
+                _lib.profile_enable(False)
+                p = prof["ks_ip"]
+                print(f"ip {name:8s} level {lvl:2d} B={B:2d}: ks_ip {p['ms'] / 5 * 1e3:8.1f} us/op "
+                      f"{p['bytes'] / p['ms'] / 1e6:7.1f} GB/s alg  launches {p['launches'] // 5}",
+                      flush=True)
+
+
 def main():
     params = ckks.get_preset("p16")
     which = sys.argv[1:] or ["ntt", "bsgs"]
@@ -79,6 +112,8 @@ def main():
         bench_ntt(params)
     if "bsgs" in which:
         bench_bsgs(params)
+    if "ip" in which:
+        bench_ip(params)
 
 
 if __name__ == "__main__":
