@@ -178,6 +178,12 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 
 
+# EvalMod of the sparse (weight-refresh) bootstraps: "double_angle" (degree-31
+# cos + 3 squarings, ~22 key switches, one more level, max error 5.7e-4 at
+# P16) or the reference's "sine" (degree 119, ~69 key switches, 3.1e-4)
+SPARSE_EVALMOD = os.environ.get("SPARSE_EVALMOD", "double_angle")
+
+
 def p16():
     from paper_2210_02574_b200 import ckks
 
@@ -275,12 +281,52 @@ def cost_model_sample(params, histogram, units, unit_kind):
     sec = model.seconds(histogram)
     n_ks = sum(v for k, v in histogram.items() if k.startswith("ks@"))
     n_enc = sum(v for k, v in histogram.items() if k.startswith("encode@"))
+    cal = reference_calibration(unit_kind, units)
     sample = (f"oracle (C/OpenMP, all host cores) timed KS at levels {ks_levels} and "
               f"encode/rescale/pt-mult at levels {other} ({time.perf_counter() - t0:.1f}s of "
               f"CPU sampling), weighted by the step's reference op histogram ({n_ks} KS, "
               f"{n_enc} encodes): modelled {sec:.1f} s per step")
+    if cal is not None:
+        sec *= cal["measured_over_model"]
+        sample += (f"; x {cal['measured_over_model']:.3f} = the measured/modelled ratio of one "
+                   f"full reference minibatch timed end to end ({cal['source']}): "
+                   f"{sec:.1f} s per step")
     value = units / sec if unit_kind == "rate" else sec * 1e3
     return value, sample
+
+
+_CONFIG = ["train"]  # the workload this process runs (set by main)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def reference_calibration(unit_kind, units):
+    """Measured/modelled ratio of the reference CPU path: one whole cfg4
+    minibatch of the reference itself (numba, all cores) timed end to end
+    next to this cost model on the same machine (tools/ref_minibatch_time.py,
+    profiles/r02_ref_minibatch_time.log).  Applied to the train workload
+    only, the one it was measured on."""
+    if _CONFIG[0] != "train":
+        return None
+    path = os.path.join(REPO, "profiles", "r02_ref_minibatch_time.log")
+    try:
+        recs = [json.loads(ln) for ln in open(path) if ln.strip().startswith("{")]
+        ref = next(r for r in recs if "minibatch_seconds" in r)
+        mod = next(r for r in recs if "measured_over_model" in r)
+    except (OSError, StopIteration, ValueError):
+        return None
+    return {"measured_over_model": float(mod["measured_over_model"]),
+            "source": f"reference {ref['minibatch_seconds']:.0f} s vs model "
+                      f"{mod['model_minibatch_seconds']:.0f} s on {ref['cores']} cores, "
+                      "profiles/r02_ref_minibatch_time.log"}
 
 
 def diag_gib(ctx):
@@ -312,7 +358,8 @@ class BootstrapWorkload:
         from paper_2210_02574_b200 import bootstrap as bs, ckks
 
         self.params = p16()
-        self.ctx = bs.build_context(self.params, n_slots=1024, input_periodic=True)
+        self.ctx = bs.build_context(self.params, n_slots=1024, input_periodic=True,
+                                    evalmod=SPARSE_EVALMOD)
         steps = self.ctx.required_rotation_steps()
         t0 = time.time()
         self.keys = ckks.keygen(self.params, rotation_steps=steps, rng_seed=7)
@@ -541,7 +588,8 @@ class TrainWorkload:
         self.params = params = p16()
         self.sig = minimax.load_approximant("sigmoid_deg15")
         self.layout = logreg.make_layout(params, 768)
-        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True)
+        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True,
+                                    evalmod=SPARSE_EVALMOD)
         steps = sorted(set(bs.refresh_rotation_steps(self.ctx)) | logreg_rotation_steps(self.layout))
         t0 = time.time()
         self.keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
@@ -604,6 +652,7 @@ class TrainWorkload:
             "preset": "p16", "N": 65536, "batch_rows": cls.batch_rows,
             "ciphertexts_per_minibatch": cls.batch_rows // 32, "rows_per_ct": 32,
             "refresh": "w and u refreshed together: one packed sparse bootstrap of period 2048 (two of period 1024 in the reference)",
+            "evalmod": SPARSE_EVALMOD,
             "parallelism": f"minibatch sharded over {world} GPU(s)",
             "l2": "keys (>14 GiB) and diagonals (36 GiB) exceed L2"}
 
@@ -749,7 +798,8 @@ class OvrWorkload(TrainWorkload):
         self.params = params = p16()
         self.sig = minimax.load_approximant("sigmoid_deg15")
         self.layout = logreg.make_layout(params, self.dim)
-        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True)
+        self.ctx = bs.build_context(params, n_slots=self.layout.padded_dim, input_periodic=True,
+                                    evalmod=SPARSE_EVALMOD)
         steps = sorted(set(bs.refresh_rotation_steps(self.ctx)) | logreg_rotation_steps(self.layout))
         t0 = time.time()
         self.keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
@@ -1031,6 +1081,10 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     line.update(extra)
+    if hasattr(wl, "static_config"):  # the reference arm prints exactly this config
+        static = wl.static_config(world)
+        line["run_info"] = {k: v for k, v in wl.config.items() if k not in static}
+        line["config"] = static
     line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line), flush=True)
 
@@ -1095,7 +1149,8 @@ def cpu_baseline(wl):
             OK._clib = None
         value, sample = wl.oracle_sample()
         return {"value": round(value, 6), "unit": wl.unit, "cores": os.cpu_count(),
-                "kind": "port", "sample": sample}
+                "kind": "port", "method": "oracle cost model (bounded sample)",
+                "cpu": cpu_model(), "sample": sample}
     except Exception as exc:  # the baseline must never break the GPU line
         return {"value": None, "unit": wl.unit, "cores": os.cpu_count(), "kind": "port",
                 "sample": f"unavailable: {exc}"}
@@ -1134,7 +1189,9 @@ def run_reference(args):
             "config": (wl.static_config(args.gpus) if hasattr(wl, "static_config")
                        else {"workload": args.config, "preset": preset}),
             "cpu_baseline": {"value": round(value, 6), "unit": wl.unit,
-                             "cores": os.cpu_count(), "kind": "port", "sample": sample},
+                             "cores": os.cpu_count(), "kind": "port",
+                             "method": "oracle cost model (bounded sample)", "cpu": cpu_model(),
+                             "sample": sample},
             "e2e": {"value": round(value, 6), "unit": wl.unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -1142,6 +1199,7 @@ def run_reference(args):
 
 def main():
     args = parse()
+    _CONFIG[0] = args.config
     if args.impl == "reference":
         run_reference(args)
     else:

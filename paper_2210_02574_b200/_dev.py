@@ -168,3 +168,12 @@ def pin_cached():
     refs = [v for c in PtCache._ALL for v in c._d.values()] + _CAPTURE_REFS
     _CAPTURE_REFS.clear()
     return refs
+
+
+def release_cached():
+    """Return torch's cached free blocks to the driver (not while a graph is
+    captured): libhegpu's scratch comes from the stream-ordered pool
+    (cudaMallocAsync), which cannot reuse memory torch's allocator caches."""
+    if torch is not None and torch.cuda.is_available() and \
+            not torch.cuda.is_current_stream_capturing():
+        torch.cuda.empty_cache()

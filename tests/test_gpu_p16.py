@@ -91,7 +91,7 @@ def trained(p16, sigmoid15):
                    | set(ctx_full.required_rotation_steps()))
     keys = ckks.keygen(p16, rotation_steps=steps, rng_seed=7)
     pairs = logreg.pack_batch(Xtr, ytr, layout, p16, keys)
-    cfg = logreg.TrainConfig(1.0, 0.9, 64, 1)
+    cfg = logreg.TrainConfig(0.25, 0.9, 64, 1)
     model, timing = logreg.train(pairs, 512, cfg, p16, keys, sigmoid15,
                                  bs.BootstrapRefresher(ctx, keys), layout=layout,
                                  data_refresher=bs.BootstrapRefresher(ctx_full, keys))

@@ -13,86 +13,55 @@ from paper_2210_02574_b200 import bootstrap as bs, ckks, minimax  # noqa: E402
 from paper_2210_02574_b200.ckks import ops  # noqa: E402
 
 MODE = sys.argv[1] if len(sys.argv) > 1 else "full"
-DEGS = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["119", "127"])]
+SPECS = sys.argv[2].split(",") if len(sys.argv) > 2 else ["119", "da"]
+import torch  # noqa: E402
 
-params = ckks.get_preset("p16")
+params = ckks.get_preset(os.environ.get("PROBE_PRESET", "p16"))
 slots = params.slot_count
 n = slots if MODE == "full" else 1024
-ctxs = {d: bs.build_context(params, n_slots=n, evalmod_degree=d, input_periodic=(MODE != "full"))
-        for d in DEGS}
-ctx0 = ctxs[DEGS[0]]
-steps = sorted(set(ctx0.required_rotation_steps()) | set(bs.refresh_rotation_steps(ctx0)))
+
+
+def make_ctx(spec):
+    kw = dict(n_slots=n, input_periodic=(MODE != "full"))
+    if spec.startswith("da"):
+        r = int(spec[2:] or 3)
+        return bs.build_context(params, evalmod="double_angle", double_angle=r, **kw)
+    return bs.build_context(params, evalmod="sine", evalmod_degree=int(spec), **kw)
+
+
+ctxs = {sp: make_ctx(sp) for sp in SPECS}
+steps = set()
+for c in ctxs.values():
+    steps |= set(c.required_rotation_steps()) | set(bs.refresh_rotation_steps(c))
+steps = sorted(steps)
 t0 = time.time()
 keys = ckks.keygen(params, rotation_steps=steps, rng_seed=7)
 print(f"keygen {len(steps)} steps {time.time() - t0:.1f}s", flush=True)
-
 rng = np.random.default_rng(1002)
-if MODE == "full":
-    v = rng.uniform(-1, 1, slots)
-else:
-    v = np.tile(rng.uniform(-1, 1, n), slots // n)
-ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=5)
-
-
-def err(out):
-    return float(np.max(np.abs(ckks.decrypt_vector(out, keys) - v)))
-
-
-real_eval = ops.eval_poly_bsgs
-
-
-def exact_eval(ct_in, poly, keyset, input_prescaled=False):
-    out = real_eval(ct_in, poly, keyset, input_prescaled=input_prescaled)
-    D = poly.domain[1]
-    parts_in = ops.unstack(ct_in) if ct_in.batch is not None else [ct_in]
-    parts_out = ops.unstack(out) if out.batch is not None else [out]
-    res = []
-    for a, o in zip(parts_in, parts_out):
-        y = ckks.decrypt_vector(a, keys)
-        f = np.sin(2 * np.pi * D * y) / (2 * np.pi)
-        res.append(ckks.encrypt_vector(params, f, keys, level=o.level, scale=o.scale, rng_seed=9))
-    return ops.stack(res) if out.batch is not None else res[0]
-
-
-for d in DEGS:
-    ctx = ctxs[d]
+vs = []
+for i in range(2):
+    vs.append(rng.uniform(-1, 1, slots) if MODE == "full" else np.tile(rng.uniform(-1, 1, n), slots // n))
+cts = [ckks.encrypt_vector(params, v, keys, level=0, rng_seed=5 + i) for i, v in enumerate(vs)]
+for sp, ctx in ctxs.items():
     for rep in range(2):
-        out = bs.bootstrap(ct, ctx, keys)
-        print(f"deg {d} rep {rep}: err {err(out):.3e} level {out.level}", flush=True)
-    ops.eval_poly_bsgs = exact_eval
-    bs.ops.eval_poly_bsgs = exact_eval
-    try:
-        out = bs.bootstrap(ct, ctx, keys)
-        print(f"deg {d} EXACT EvalMod: err {err(out):.3e}", flush=True)
-    finally:
-        ops.eval_poly_bsgs = real_eval
-        bs.ops.eval_poly_bsgs = real_eval
-    # EvalMod-only error: decrypt in / out of the real EvalMod
-    cap = {}
-
-    def cap_eval(ct_in, poly, keyset, input_prescaled=False):
-        out = real_eval(ct_in, poly, keyset, input_prescaled=input_prescaled)
-        cap["in"], cap["out"], cap["D"] = ct_in, out, poly.domain[1]
-        return out
-
-    ops.eval_poly_bsgs = cap_eval
-    bs.ops.eval_poly_bsgs = cap_eval
-    try:
-        bs.bootstrap(ct, ctx, keys)
-    finally:
-        ops.eval_poly_bsgs = real_eval
-        bs.ops.eval_poly_bsgs = real_eval
-    ins = ops.unstack(cap["in"]) if cap["in"].batch is not None else [cap["in"]]
-    outs = ops.unstack(cap["out"]) if cap["out"].batch is not None else [cap["out"]]
-    D = cap["D"]
-    q0 = params.ring.moduli_chain[0]
-    for a, o in zip(ins, outs):
-        y = ckks.decrypt_vector(a, keys)
-        z = ckks.decrypt_vector(o, keys)
-        f = np.sin(2 * np.pi * D * y) / (2 * np.pi)
-        frac = D * y - np.round(D * y)
-        print(f"   evalmod in: |y|max {np.max(np.abs(y)):.4f} |I|max {np.max(np.abs(np.round(D*y))):.0f}"
-              f" frac rms {np.sqrt(np.mean(frac**2)):.3e} max {np.max(np.abs(frac)):.3e};"
-              f" out-f max {np.max(np.abs(z - f)):.3e} rms {np.sqrt(np.mean((z - f)**2)):.3e}"
-              f" (x q0/scale = msg units {np.max(np.abs(z - f)) * q0 / params.default_scale:.3e})",
-              flush=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        outs = bs.bootstrap_many(cts, ctx, keys) if MODE != "full" else [bs.bootstrap(cts[0], ctx, keys)]
+        e1.record()
+        torch.cuda.synchronize()
+        errs = [float(np.max(np.abs(ckks.decrypt_vector(o, keys) - v))) for o, v in zip(outs, vs)]
+        print(f"{MODE} {sp}: err {max(errs):.3e} level {outs[0].level} time {e0.elapsed_time(e1):.1f} ms"
+              f" (B={len(outs)})", flush=True)
+    if MODE != "full":
+        refr = bs.BootstrapRefresher(ctx, keys)
+        for rep in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            outs = refr.refresh_many(cts)
+            e1.record()
+            torch.cuda.synchronize()
+            errs = [float(np.max(np.abs(ckks.decrypt_vector(o, keys) - v))) for o, v in zip(outs, vs)]
+            print(f"{MODE} {sp} packed pair: err {max(errs):.3e} time {e0.elapsed_time(e1):.1f} ms",
+                  flush=True)

@@ -32,7 +32,8 @@ def main():
     params = ckks.get_preset("p16")
     sig = minimax.load_approximant("sigmoid_deg15")
     layout = logreg.make_layout(params, 768)
-    ctx = bs.build_context(params, n_slots=layout.padded_dim, input_periodic=True)
+    ctx = bs.build_context(params, n_slots=layout.padded_dim, input_periodic=True,
+                           evalmod=os.environ.get("SPARSE_EVALMOD", "double_angle"))
     ctx_full = bs.build_context(params, n_slots=params.slot_count)
     steps = sorted(set(bs.refresh_rotation_steps(ctx)) | set(logreg.rotation_steps(layout))
                    | set(ctx_full.required_rotation_steps()))
