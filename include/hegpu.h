@@ -263,11 +263,21 @@ int hegpu_ks_rotsum(hegpu_ring_t ring, int level, int alpha, const uint64_t* c, 
  * partials are P-scaled extended-basis ciphertexts (n_batch, 2, level+1+K, N)
  * from double-hoisted babies; only each giant's c1 is brought down for its
  * key switch, one final ModDown by q_level * P remains; partials are
- * clobbered.  N >= 2^12. */
+ * clobbered.  N >= 2^12.  pq_in = 2: as 1, but out receives the
+ * extended-basis sum (n_batch, 2, level+1+K, N) BEFORE the final ModDown
+ * (a transform split across ranks modular-all-reduces these first, then
+ * calls hegpu_moddown_rescale_ext). */
 int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* partials,
                       int64_t gstride, int n_batch, int n_giants, const uint64_t* galois,
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
                       uint64_t* out, int rescale, int pq_in, void* stream);
+
+/* ModDown of P-scaled extended-basis ciphertexts by q_level * P (the final
+ * step of a double-hoisted transform, bootstrap.py:243-247 + keys.py:330-338):
+ * in (n_batch, 2, level+1+K, N) eval form (clobbered) -> out (n_batch, 2,
+ * level, N) at level - 1.  N >= 2^12. */
+int hegpu_moddown_rescale_ext(hegpu_ring_t ring, int level, int alpha, uint64_t* in,
+                              int n_batch, uint64_t* out, void* stream);
 
 /* Rescale by q_level (_poly_rescale, ops.py:164-189): in has level+1 chain
  * limbs (eval form), out gets `level` limbs.  in may equal out. */

@@ -1101,7 +1101,8 @@ static void ks_rotsum_impl(Ring& R, int level, int alpha, const uint64_t* c, int
 static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials,
                                int64_t gstride, int B, int n_giants, const uint64_t* galois,
                                const uint64_t* const* key_b, const uint64_t* const* key_a,
-                               int n_digits, uint64_t* down, cudaStream_t st);
+                               int n_digits, uint64_t* down, cudaStream_t st,
+                               bool ext_out = false);
 
 static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* partials,
                             int64_t gstride, int B, int n_giants, const uint64_t* galois,
@@ -1197,7 +1198,7 @@ static void bsgs_giants_sum(Ring& R, int level, int alpha, const uint64_t* parti
 static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials,
                                int64_t gstride, int B, int n_giants, const uint64_t* galois,
                                const uint64_t* const* key_b, const uint64_t* const* key_a,
-                               int n_digits, uint64_t* down, cudaStream_t st) {
+                               int n_digits, uint64_t* down, cudaStream_t st, bool ext_out) {
   const KsLevel& L = R.ks_level(level, alpha);
   const int k = level + 1, n_ext = L.n_ext, beta = L.beta;
   const size_t N = R.n;
@@ -1217,8 +1218,11 @@ static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials
   const size_t sz_pq = (size_t)B * cs, sz_q = (size_t)CH * B * k * N;
   const size_t sz_ext = (size_t)CH * B * beta * n_ext * N;
   Scratch ws((sz_pq + 2 * sz_q + sz_ext + sz_pq + sz_q) * 8, st);
-  uint64_t* sum = ws.u64();     // (B, 2, n_ext, N)
-  uint64_t* c1q = sum + sz_pq;  // (CH*B, k, N)
+  // (B, 2, n_ext, N); ext_out: the caller's buffer receives the extended-basis
+  // sum and the final ModDown is left to it (a distributed transform reduces
+  // the per-rank sums first)
+  uint64_t* sum = ext_out ? down : ws.u64();
+  uint64_t* c1q = ws.u64() + sz_pq;  // (CH*B, k, N)
   uint64_t* dcoeff = c1q + sz_q;
   uint64_t* ext = dcoeff + sz_q;
   uint64_t* acc = ext + sz_ext;  // (B, 2, n_ext, N)
@@ -1277,6 +1281,7 @@ static void bsgs_giants_sum_pq(Ring& R, int level, int alpha, uint64_t* partials
              (int64_t)n_ext * (int64_t)N, 2 * B, n_ext, ext_rows.data(), nullptr};
     launch_elementwise(R.dpc, R.primes, R.log_n, A, st);
   }
+  if (ext_out) return;
   ks_moddown_rescale(R, L, sum, corr, B, nullptr, 0, 0, down, (int64_t)2 * level * N,
                      (int64_t)level * N, st);
 }
@@ -1787,11 +1792,23 @@ int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* p
     if (pq_in) {
       if (!rescale) throw HegpuError{HEGPU_E_ARG, "extended-basis giants need rescale = 1"};
       bsgs_giants_sum_pq(R, level, alpha, const_cast<uint64_t*>(partials), gstride, n_batch,
-                         n_giants, galois, key_b, key_a, n_digits, out, S_(stream));
+                         n_giants, galois, key_b, key_a, n_digits, out, S_(stream), pq_in == 2);
       return HEGPU_OK;
     }
     bsgs_giants_impl(R, level, alpha, partials, gstride, n_batch, n_giants, galois, key_b, key_a,
                      n_digits, out, S_(stream), rescale != 0);
+  })
+}
+
+int hegpu_moddown_rescale_ext(hegpu_ring_t ring, int level, int alpha, uint64_t* in,
+                              int n_batch, uint64_t* out, void* stream) {
+  HEGPU_TRY({
+    Ring& R = RR(ring);
+    if (n_batch <= 0) return HEGPU_OK;
+    const KsLevel& L = R.ks_level(level, alpha);
+    Scratch corr((size_t)n_batch * 2 * level * R.n * 8, S_(stream));
+    ks_moddown_rescale(R, L, in, corr.u64(), n_batch, nullptr, 0, 0, out,
+                       (int64_t)2 * level * R.n, (int64_t)level * R.n, S_(stream));
   })
 }
 

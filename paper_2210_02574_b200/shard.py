@@ -18,15 +18,40 @@ from . import _dev
 from . import _lib
 
 
-def world():
-    """(rank, world_size) of the default process group, (0, 1) if none."""
+def world(group=None):
+    """(rank, size) in `group` (default: the world), (0, 1) without a process group."""
     try:
         import torch.distributed as dist
     except Exception:
         return 0, 1
     if dist.is_available() and dist.is_initialized():
-        return dist.get_rank(), dist.get_world_size()
+        return dist.get_rank(group), dist.get_world_size(group)
     return 0, 1
+
+
+def global_rank(group, rank):
+    """Global rank of group-local `rank` (collectives take global source ranks)."""
+    if group is None:
+        return rank
+    import torch.distributed as dist
+
+    return dist.get_global_rank(group, rank)
+
+
+def class_groups(n_models, world_size):
+    """2-D (class x minibatch) layout of One-vs-Rest training over ranks
+    (logreg.py:393-398: classes are independent): returns, per class, the
+    ranks that train it.  world <= classes: classes dealt round-robin, one
+    rank each; world a multiple of classes: world/classes ranks per class,
+    sharding that class's minibatches; otherwise every rank trains every
+    class (1-D minibatch sharding)."""
+    if world_size <= 1:
+        return [[0] for _ in range(n_models)]
+    if world_size <= n_models:
+        return [[c % world_size] for c in range(n_models)]
+    if world_size % n_models == 0:
+        return [[r for r in range(world_size) if r % n_models == c] for c in range(n_models)]
+    return [list(range(world_size)) for _ in range(n_models)]
 
 
 def shard_range(n_items, rank, world_size):
@@ -57,11 +82,11 @@ def modular_sum_host(residue_arrays, primes):
     return acc % q
 
 
-def allreduce_ciphertext(ct):
-    """In-place modular all-reduce of an (unbatched) ciphertext over all ranks."""
+def allreduce_ciphertext(ct, group=None):
+    """In-place modular all-reduce of an (unbatched) ciphertext over `group`."""
     import torch.distributed as dist
 
-    rank, ws = world()
+    rank, ws = world(group)
     if ws == 1:
         return ct
     params = ct.params
@@ -77,7 +102,7 @@ def allreduce_ciphertext(ct):
     base = ct.c0.data
     n = params.ring_degree
     flat = base.as_strided((2, k, n), (k * n, n, 1))
-    dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
     p, cnt, s = grp
     _lib.call(
         "hegpu_elementwise", params.ring.device(), _lib.OP_REDUCE, p, s, None, 0, p, s, cnt, k,
@@ -86,11 +111,12 @@ def allreduce_ciphertext(ct):
     return ct
 
 
-def broadcast_ciphertext(ct, src, template):
-    """Broadcast a ciphertext from rank `src`; other ranks pass a same-shaped template."""
+def broadcast_ciphertext(ct, src, template, group=None):
+    """Broadcast a ciphertext from (group-local) rank `src`; other ranks pass a
+    same-shaped template."""
     import torch.distributed as dist
 
-    rank, ws = world()
+    rank, ws = world(group)
     if ws == 1:
         return ct
     from .ckks import ops
@@ -102,10 +128,34 @@ def broadcast_ciphertext(ct, src, template):
     k = holder.level + 1
     n = holder.params.ring_degree
     flat = holder.c0.data.as_strided((2, k, n), (k * n, n, 1))
-    dist.broadcast(flat, src=src)
+    gsrc = global_rank(group, src)
+    dist.broadcast(flat, src=gsrc, group=group)
     meta = [holder.scale, int(holder.insecure_provenance)]
     obj = [meta]
-    dist.broadcast_object_list(obj, src=src)
+    dist.broadcast_object_list(obj, src=gsrc, group=group)
     holder.scale = float(obj[0][0])
     holder.insecure_provenance = bool(obj[0][1])
     return holder
+
+
+def allreduce_residues(t, primes_idx, params, group=None):
+    """In-place modular all-reduce of a residue tensor (..., k, N) whose row i
+    lives modulo prime index primes_idx[i] (chain and special rows mixed):
+    wrapping int64 SUM, then one mod-q pass.  Exact for world*(q-1) < 2^64."""
+    import torch.distributed as dist
+
+    ws = dist.get_world_size(group) if group is not None else world()[1]
+    if ws == 1:
+        return t
+    primes_idx = np.ascontiguousarray(primes_idx, dtype=np.int32)
+    all_primes = list(params.ring.moduli_chain) + list(params.ring.special_moduli)
+    if not check_allreduce_exact([all_primes[i] for i in primes_idx], ws):
+        raise ValueError("world size too large for an exact wrapping all-reduce")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    k, n = int(t.shape[-2]), int(t.shape[-1])
+    p, cnt, s = _dev.group(t, k, n)
+    _lib.call(
+        "hegpu_elementwise", params.ring.device(), _lib.OP_REDUCE, p, s, None, 0, p, s, cnt, k,
+        primes_idx.ctypes.data, None, _dev.stream(),
+    )
+    return t

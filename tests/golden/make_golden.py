@@ -347,7 +347,10 @@ def logreg_p16_fixture():
         s = logreg.shadow_scores(Xte, w, sig, layout)
         return float(np.mean((np.asarray(s) > 0.5).astype(int).ravel() == yte))
 
-    np.savez_compressed(os.path.join(HERE, "logreg_p16.npz"), X=X, y=y,
+    # X is regenerated by the tests from its seed (synth.make_separable mirrors
+    # T/conftest.py:68-82); its digest pins it
+    np.savez_compressed(os.path.join(HERE, "logreg_p16.npz"), y=y,
+                        X_sha256=hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest(),
                         ref_weights=got, shadow_weights=np.asarray(shadow.weights))
     return {"train_seconds": tt, "epoch_seconds": timing[0]["seconds"],
             "ref_acc": acc(got), "shadow_acc": acc(shadow.weights),

@@ -67,3 +67,17 @@ def test_two_rank_gradient_allreduce():
     assert out[0][1] == (0, 8) and out[1][1] == (8, 16)
     assert out[0][2] == out[1][2] == 7 and out[0][3] == out[1][3] == 9
     assert out[0][4]  # w and u refresh on different ranks
+
+
+def test_class_groups_layout():
+    """2-D (class x minibatch) layout of One-vs-Rest training over ranks."""
+    from paper_2210_02574_b200 import shard
+
+    assert shard.class_groups(4, 1) == [[0]] * 4
+    assert shard.class_groups(4, 2) == [[0], [1], [0], [1]]
+    assert shard.class_groups(4, 4) == [[0], [1], [2], [3]]
+    assert shard.class_groups(4, 8) == [[0, 4], [1, 5], [2, 6], [3, 7]]
+    assert shard.class_groups(3, 5) == [list(range(5))] * 3  # 1-D fallback
+    for world in (1, 2, 4, 8):  # every rank trains something, every class has ranks
+        g = shard.class_groups(4, world)
+        assert sorted({r for m in g for r in m}) == list(range(world))

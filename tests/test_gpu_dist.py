@@ -153,3 +153,145 @@ def test_two_rank_captured_sharded_minibatch():
     for r in range(2):
         assert np.max(np.abs(np.array(out[r][1]) - want_w)) < 5e-3
         assert np.max(np.abs(np.array(out[r][2]) - want_u)) < 5e-3
+
+
+def _split_boot_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_02574_b200 import bootstrap as bs, ckks
+
+        params = ckks.get_preset("desk-boot")
+        ctx = bs.build_context(params, n_slots=256, input_periodic=True)
+        keys = ckks.keygen(params, rotation_steps=ctx.required_rotation_steps(), rng_seed=7)
+        rng = np.random.default_rng(77)
+        vs = [np.tile(rng.uniform(-1, 1, 256), params.slot_count // 256) for _ in range(2)]
+        cts = [ckks.encrypt_vector(params, v, keys, level=0, rng_seed=300 + i)
+               for i, v in enumerate(vs)]
+        single = bs.bootstrap_many(cts, ctx, keys)  # this rank alone
+        with bs.distributed():
+            split = bs.bootstrap_many(cts, ctx, keys)
+        same = all(np.array_equal(a.c0.limbs, b.c0.limbs) and np.array_equal(a.c1.limbs, b.c1.limbs)
+                   for a, b in zip(single, split))
+        err = max(float(np.max(np.abs(ckks.decrypt_vector(o, keys) - v))) for o, v in zip(split, vs))
+        out[rank] = (same, err, split[0].c0.limbs.tobytes()[:4096])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_split_transform_bootstrap_bit_exact(world):
+    """The bootstrap with CoeffToSlot / SlotToCoeff giant steps split across
+    `world` gloo ranks (bootstrap.distributed: each rank its giants' diagonal
+    products and key switches, one modular all-reduce of the extended-basis
+    sums per transform) gives limbs identical to the single-process bootstrap
+    on every rank."""
+    ctx_mp = mp.get_context("spawn")
+    out = ctx_mp.Manager().dict()
+    mp.start_processes(_split_boot_worker, args=(world, _free_port(), out), nprocs=world,
+                       join=True, start_method="spawn")
+    for r in range(world):
+        same, err, head = out[r]
+        assert same, f"rank {r}: split bootstrap limbs differ from the single-process ones"
+        assert err < 1e-2
+        assert head == out[0][2]
+
+
+def _eager_split_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg
+
+        params, keys, sig, layout, ctx, cfg, xs, ys, w0, u0, ops = _boot_setup()
+        w, u = logreg.train_minibatch(w0, u0, xs, ys, cfg.batch_size, cfg, keys, sig, layout,
+                                      bs.BootstrapRefresher(ctx, keys))
+        out[rank] = (w.c0.limbs.tobytes(), u.c1.limbs.tobytes(),
+                     ckks.decrypt_vector(w, keys).tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_eager_minibatch_split_refresh():
+    """train_minibatch over two gloo ranks with a bootstrap refresher: sharded
+    gradients, modular all-reduce, then the packed (w, u) refresh run by both
+    ranks with the transforms' giants split (no broadcast): identical limbs on
+    both ranks, decrypting like the single-process update."""
+    from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg
+
+    params, keys, sig, layout, ctx, cfg, xs, ys, w0, u0, ops = _boot_setup()
+    w, _ = logreg.train_minibatch(w0, u0, ops.stack(xs), ops.stack(ys), cfg.batch_size, cfg,
+                                  keys, sig, layout, bs.BootstrapRefresher(ctx, keys))
+    want_w = ckks.decrypt_vector(w, keys)
+    ctx_mp = mp.get_context("spawn")
+    out = ctx_mp.Manager().dict()
+    mp.start_processes(_eager_split_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    assert np.max(np.abs(np.array(out[0][2]) - want_w)) < 5e-3
+
+
+def _ovr_setup():
+    from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg, minimax
+    from paper_2210_02574_b200.synth import make_blob_embeddings
+
+    params = ckks.get_preset("desk")
+    keys = ckks.keygen(params, rng_seed=7)
+    sig = minimax.load_approximant("sigmoid_deg15")
+    layout = logreg.make_layout(params, 16)
+    X, y = make_blob_embeddings(np.random.default_rng(5), 64, 4, dim=16)
+    X = X * 0.25
+    pairs = logreg.pack_batch(X, y.astype(np.float64), layout, params, keys,
+                              target_level=params.max_level, rng_seed=500)
+    ovr = logreg.pack_labels_ovr(y, 4, layout, params, keys)
+    cfg = logreg.TrainConfig(0.5, 0.9, 2 * layout.rows_per_ct, 1)
+    return params, keys, sig, layout, X, y, pairs, ovr, cfg, bs.DebugRefresher(keys, enabled=True)
+
+
+def _ovr_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_02574_b200 import logreg
+
+        params, keys, sig, layout, X, y, pairs, ovr, cfg, ref = _ovr_setup()
+        model, _ = logreg.train(pairs, len(y), cfg, params, keys, sig, ref, class_count=4,
+                                ovr_labels=ovr, layout=layout, refreshed_data=[d for d, _ in pairs])
+        out[rank] = logreg.decrypted_weights(model, keys).tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_ovr_class_by_minibatch_sharding(world):
+    """One-vs-Rest over `world` gloo ranks on one GPU: 4 ranks = one class per
+    rank; 8 ranks = the 2-D layout, each class's minibatches sharded over a
+    2-rank subgroup (shard.class_groups).  Every rank returns the whole
+    model, decrypting like the single-process training."""
+    from paper_2210_02574_b200 import logreg
+
+    params, keys, sig, layout, X, y, pairs, ovr, cfg, ref = _ovr_setup()
+    model, _ = logreg.train(pairs, len(y), cfg, params, keys, sig, ref, class_count=4,
+                            ovr_labels=ovr, layout=layout, refreshed_data=[d for d, _ in pairs])
+    want = logreg.decrypted_weights(model, keys)
+    ctx_mp = mp.get_context("spawn")
+    out = ctx_mp.Manager().dict()
+    mp.start_processes(_ovr_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        assert np.max(np.abs(np.array(out[r]) - want)) < 1e-4

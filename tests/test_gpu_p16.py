@@ -55,6 +55,23 @@ def test_p16_sparse_bootstrap_vs_reference(p16, sparse):
     assert np.max(np.abs(dec[:1024] - g["dec"])) <= 2e-3
 
 
+def test_p16_sparse_bootstrap_double_angle(p16, sparse):
+    """The double-angle EvalMod (degree-31 cos + 3 squarings, the trainer's
+    refresh in bench.py) on the reference's ciphertext: within 1e-3."""
+    _, keys, d = sparse
+    ctx = bs.build_context(p16, n_slots=1024, input_periodic=True, evalmod="double_angle")
+    missing = set(ctx.required_rotation_steps()) - set(keys.rotation_keys)
+    assert not missing
+    g = golden_npz("boot_p16_sparse.npz")
+    v = np.tile(g["v"], p16.slot_count // 1024)
+    ct = ckks.encrypt_vector(p16, v, keys, level=0, rng_seed=21)
+    out = bs.bootstrap(ct, ctx, keys)
+    assert out.level == ctx.output_level == p16.max_level - 11
+    err = float(np.max(np.abs(ckks.decrypt_vector(out, keys) - v)))
+    print(f"P16 sparse-1024 double-angle bootstrap: err {err:.3e}")
+    assert err <= 1e-3
+
+
 def test_p16_full_slot_bootstrap(p16):
     """Full-slot (32,768 slots) ingest bootstrap at P16.  The P16 preset keeps
     the reference's parameters (q0/scale = 32, EvalMod at scale 2^40), whose
@@ -81,11 +98,19 @@ def trained(p16, sigmoid15):
     """8 minibatches (64 rows = 2 ciphertexts each) through the public
     logreg.train(): batched full-slot ingest of the level-3 transport
     ciphertexts, sparse-1024 bootstrap refresh of w and u."""
+    import hashlib
+
+    from paper_2210_02574_b200.synth import make_separable
+
     g = golden_npz("logreg_p16.npz")
-    X, y = g["X"], g["y"]
+    X, y = make_separable(np.random.default_rng(100), 1024, dim=768, margin=0.5)
+    assert hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest() == str(g["X_sha256"])
+    assert np.array_equal(y, g["y"])
     Xtr, ytr = X[:512], y[:512]
     layout = logreg.make_layout(p16, 768)
-    ctx = bs.build_context(p16, n_slots=layout.padded_dim, input_periodic=True)
+    # the bench's configuration: double-angle EvalMod for the weight refresh
+    ctx = bs.build_context(p16, n_slots=layout.padded_dim, input_periodic=True,
+                           evalmod="double_angle")
     ctx_full = bs.build_context(p16, n_slots=p16.slot_count)
     steps = sorted(set(bs.refresh_rotation_steps(ctx)) | set(logreg.rotation_steps(layout))
                    | set(ctx_full.required_rotation_steps()))
@@ -96,11 +121,11 @@ def trained(p16, sigmoid15):
                                  bs.BootstrapRefresher(ctx, keys), layout=layout,
                                  data_refresher=bs.BootstrapRefresher(ctx_full, keys))
     got = logreg.decrypted_weights(model, keys)
-    return g, layout, got, timing
+    return g, X, y, layout, got, timing
 
 
 def test_p16_training_vs_reference_and_shadow(trained, sigmoid15):
-    g, layout, got, timing = trained
+    g, X, y, layout, got, timing = trained
     ref, shadow = g["ref_weights"], g["shadow_weights"]
     gap_ref = float(np.max(np.abs(got - ref)))
     gap_shadow = float(np.max(np.abs(got - shadow)))
@@ -112,8 +137,7 @@ def test_p16_training_vs_reference_and_shadow(trained, sigmoid15):
 
 
 def test_p16_training_test_accuracy(trained, sigmoid15):
-    g, layout, got, _ = trained
-    X, y = g["X"], g["y"]
+    g, X, y, layout, got, _ = trained
     Xte, yte = X[512:], y[512:]
 
     def acc(w):
