@@ -397,7 +397,9 @@ def main():
             "ovr": ("ovr_desk", ovr_fixture),
             "boot_p16_sparse": ("boot_p16_sparse", boot_p16_sparse_fixture),
             "logreg_p16": ("logreg_p16", logreg_p16_fixture),
-            "sine_artifact": ("sine_artifact", sine_artifact)}
+            "sine_artifact": ("sine_artifact", sine_artifact),
+            "p16s": ("p16s", lambda: scheme_digests(load_preset("p16s"), "p16s", [1], conj=False,
+                                                    full=False)[0])}
     if sys.argv[1:] and sys.argv[1] in only:  # add / refresh only these entries
         path = os.path.join(HERE, "digests.json")
         digests = json.load(open(path))

@@ -43,7 +43,7 @@ def keyset(name, d):
     return _KEYS[name]
 
 
-@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+@pytest.mark.parametrize("name", ["desk", "p14", "p16", "p16s"])
 def test_keygen_bit_exact(name, digests):
     d = digests[name]
     params, keys = keyset(name, d)
@@ -60,7 +60,7 @@ def test_keygen_bit_exact(name, digests):
         assert [sha(x) for x in c.digits_b] + [sha(x) for x in c.digits_a] == d["conj"]
 
 
-@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+@pytest.mark.parametrize("name", ["desk", "p14", "p16", "p16s"])
 def test_key_switch_bit_exact(name, digests):
     d = digests[name]
     params, keys = keyset(name, d)
@@ -72,7 +72,7 @@ def test_key_switch_bit_exact(name, digests):
         assert [sha(kb.limbs), sha(ka.limbs)] == want, f"level {lvl}"
 
 
-@pytest.mark.parametrize("name", ["desk", "p14", "p16"])
+@pytest.mark.parametrize("name", ["desk", "p14", "p16", "p16s"])
 def test_ciphertext_ops_bit_exact(name, digests):
     d = digests[name]
     params, keys = keyset(name, d)

@@ -213,7 +213,13 @@ def _eager_split_worker(rank, world, port, out):
     try:
         from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg
 
+        from paper_2210_02574_b200 import shard
+
         params, keys, sig, layout, ctx, cfg, xs, ys, w0, u0, ops = _boot_setup()
+        # the split refresh needs identical (w, u) limbs on every rank (train()
+        # broadcasts its initial state the same way); zeros are encrypted unseeded
+        w0 = shard.broadcast_ciphertext(w0, 0, w0)
+        u0 = shard.broadcast_ciphertext(u0, 0, u0)
         w, u = logreg.train_minibatch(w0, u0, xs, ys, cfg.batch_size, cfg, keys, sig, layout,
                                       bs.BootstrapRefresher(ctx, keys))
         out[rank] = (w.c0.limbs.tobytes(), u.c1.limbs.tobytes(),

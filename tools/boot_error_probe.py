@@ -42,6 +42,28 @@ vs = []
 for i in range(2):
     vs.append(rng.uniform(-1, 1, slots) if MODE == "full" else np.tile(rng.uniform(-1, 1, n), slots // n))
 cts = [ckks.encrypt_vector(params, v, keys, level=0, rng_seed=5 + i) for i, v in enumerate(vs)]
+_real_evalmod = bs._evalmod
+
+
+def _spy_evalmod(w, ctx, keyset):
+    out = _real_evalmod(w, ctx, keyset)
+    parts_in = ops.unstack(w) if w.batch is not None else [w]
+    parts_out = ops.unstack(out) if out.batch is not None else [out]
+    D = ctx.range_k + 0.5
+    q0 = params.ring.moduli_chain[0]
+    for a, o in zip(parts_in[:1], parts_out[:1]):
+        y = ckks.decrypt_vector(a, keys)
+        z = ckks.decrypt_vector(o, keys)
+        f = np.sin(2 * np.pi * D * y) / (2 * np.pi)
+        frac = D * y - np.round(D * y)
+        print(f"   evalmod in: level {a.level} scale {a.scale:.4g} |y|max {np.max(np.abs(y)):.4f} "
+              f"|I|max {np.max(np.abs(np.round(D * y))):.0f} frac max {np.max(np.abs(frac)):.3e}; "
+              f"out level {o.level} scale {o.scale:.4g} |out - f| max {np.max(np.abs(z - f)):.3e}"
+              f" (x q0/scale {np.max(np.abs(z - f)) * q0 / params.default_scale:.3e})", flush=True)
+    return out
+
+
+bs._evalmod = _spy_evalmod
 for sp, ctx in ctxs.items():
     for rep in range(2):
         torch.cuda.synchronize()

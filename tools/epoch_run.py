@@ -11,7 +11,11 @@ Reports epoch samples/s (reference semantics: ingest excluded,
 logreg.py:337-339), ingest ciphertexts/s, the weight gap to the shadow and
 the held-out accuracies.  Usage (GPU box):
 
-    python tools/epoch_run.py [n_rows] [n_test]     # default 67349 2000
+    PYTORCH_CUDA_ALLOC_CONF=backend:cudaMallocAsync python tools/epoch_run.py [n_rows] [n_test]
+
+(default 67349 2000; the cudaMallocAsync backend puts torch's tensors in the
+same stream-ordered pool as libhegpu's scratch, so neither allocator strands
+memory the other needs)
 """
 import json
 import os
@@ -59,6 +63,10 @@ def main():
             torch.cuda.synchronize()
             TimedRefresher.seconds += time.time() - t
             TimedRefresher.count += len(cts)
+            if TimedRefresher.count % 200 < len(cts):
+                free, total = torch.cuda.mem_get_info()
+                print(f"ingest {TimedRefresher.count} cts {TimedRefresher.seconds:.0f}s "
+                      f"free {free / 2**30:.1f}/{total / 2**30:.0f} GiB", flush=True)
             return out
 
     t0 = time.time()
