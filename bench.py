@@ -184,6 +184,16 @@ def measured_peaks():
 SPARSE_EVALMOD = os.environ.get("SPARSE_EVALMOD", "double_angle")
 
 
+def zeros_ct(params, keys, level, seed=4242):
+    """Encryption of zeros with a fixed seed: every rank starts from the same
+    limbs (the split refresh needs identical (w, u) on all ranks; train()
+    broadcasts instead)."""
+    from paper_2210_02574_b200 import ckks
+
+    return ckks.encrypt(ckks.encode(params, np.zeros(params.slot_count), level), keys,
+                        rng_seed=seed)
+
+
 def p16():
     from paper_2210_02574_b200 import ckks
 
@@ -621,8 +631,8 @@ class TrainWorkload:
                        for xb, _ in self.pool_dev]
         self.host_y = [torch.stack([yb.c0.data, yb.c1.data], dim=1).cpu().pin_memory()
                        for _, yb in self.pool_dev]
-        self.w = logreg._zeros_ct(params, self.keys, top)
-        self.u = logreg._zeros_ct(params, self.keys, top)
+        self.w = zeros_ct(params, self.keys, top)
+        self.u = zeros_ct(params, self.keys, top)
         self.it = 0
         self.graph = self.sgraph = None
         if os.environ.get("BENCH_GRAPH", "1") == "1":
@@ -747,8 +757,8 @@ class TrainWorkload:
         from paper_2210_02574_b200 import ckks, logreg
 
         top = self.ctx.output_level
-        zero_w = logreg._zeros_ct(self.params, self.keys, top)
-        zero_u = logreg._zeros_ct(self.params, self.keys, top)
+        zero_w = zeros_ct(self.params, self.keys, top)
+        zero_u = zeros_ct(self.params, self.keys, top)
         g = self.graph if self.graph is not None else self.sgraph
         if g is not None:
             for dst, src in ((g.w, zero_w), (g.u, zero_u)):
@@ -793,8 +803,22 @@ class OvrWorkload(TrainWorkload):
         from paper_2210_02574_b200.ckks import ops
         from paper_2210_02574_b200.synth import make_blob_embeddings
 
-        if world > self.n_classes:
-            raise SystemExit(f"ovr: classes are the sharded axis, at most {self.n_classes} ranks")
+        from paper_2210_02574_b200 import shard
+
+        # 2-D layout (shard.class_groups): world <= 4 deals the classes to
+        # ranks; world = 4k gives each class k ranks sharding its minibatch
+        members = shard.class_groups(self.n_classes, world)
+        self.cgroup = {}
+        if world > 1:
+            import torch.distributed as dist
+
+            made = {}
+            for c, m in enumerate(members):
+                key = tuple(m)
+                if key not in made:
+                    made[key] = None if len(m) == world else dist.new_group(list(m))
+                self.cgroup[c] = made[key]
+        self.members = members
         self.params = params = p16()
         self.sig = minimax.load_approximant("sigmoid_deg15")
         self.layout = logreg.make_layout(params, self.dim)
@@ -806,8 +830,11 @@ class OvrWorkload(TrainWorkload):
         self.keygen_s = time.time() - t0
         self.refresher = bs.BootstrapRefresher(self.ctx, self.keys)
         self.cfg = logreg.TrainConfig(0.5, 0.9, self.batch_rows, 1)  # T/test_acceptance.py:151-154
-        self.mine = [c for c in range(self.n_classes) if c % world == rank]
+        self.mine = [c for c in range(self.n_classes) if rank in members[c]]
         rpc = self.layout.rows_per_ct
+        n_cts = self.batch_rows // rpc
+        m0 = members[self.mine[0]]
+        ct_lo, ct_hi = shard.shard_range(n_cts, m0.index(rank), len(m0))  # this rank's cts
         n_per_class = self.batch_rows * self.n_pool // self.n_classes
         X, y = make_blob_embeddings(np.random.default_rng(200), n_per_class, self.n_classes,
                                     dim=self.dim)
@@ -816,7 +843,7 @@ class OvrWorkload(TrainWorkload):
         self.pool_dev = []
         for b in range(self.n_pool):
             xs, ys = [], {c: [] for c in self.mine}
-            for i in range(self.batch_rows // rpc):
+            for i in range(ct_lo, ct_hi):
                 r0 = b * self.batch_rows + i * rpc
                 xs.append(ckks.encrypt(
                     ckks.encode(params, logreg._pack_slots(X[r0 : r0 + rpc], self.layout), top),
@@ -831,14 +858,21 @@ class OvrWorkload(TrainWorkload):
                        for xb, _ in self.pool_dev]
         self.host_y = [{c: torch.stack([yb[c].c0.data, yb[c].c1.data], dim=1).cpu().pin_memory()
                         for c in self.mine} for _, yb in self.pool_dev]
-        self.w = {c: logreg._zeros_ct(params, self.keys, top) for c in self.mine}
-        self.u = {c: logreg._zeros_ct(params, self.keys, top) for c in self.mine}
+        self.w = {c: zeros_ct(params, self.keys, top) for c in self.mine}
+        self.u = {c: zeros_ct(params, self.keys, top) for c in self.mine}
         self.it = 0
         xb, yb = self.pool_dev[0]
         # one captured minibatch per class (independent state, same data shape)
         # (replayed in capture order every step, so they share one graph pool)
         self.graphs, pool = {}, None
         for c in self.mine:
+            if len(members[c]) > 1:  # this class's minibatch sharded over its group
+                self.w[c] = shard.broadcast_ciphertext(self.w[c], 0, self.w[c], self.cgroup[c])
+                self.u[c] = shard.broadcast_ciphertext(self.u[c], 0, self.u[c], self.cgroup[c])
+                self.graphs[c] = logreg.CapturedShardedMinibatch(
+                    self.w[c], self.u[c], xb, yb[c], self.batch_rows, self.cfg, self.keys,
+                    self.sig, self.layout, self.refresher, group=self.cgroup[c])
+                continue
             g = logreg.CapturedMinibatch(self.w[c], self.u[c], xb, yb[c], self.batch_rows,
                                          self.cfg, self.keys, self.sig, self.layout,
                                          self.refresher, pool=pool)
@@ -865,7 +899,10 @@ class OvrWorkload(TrainWorkload):
             "rows_per_ct": 16,
             "refresh": "per class: w and u refreshed as one batch of two sparse-2048 "
                        "bootstraps (pair packing stops at period 1024: bootstrap.PACKED_PAIR_MAX_SLOTS)",
-            "parallelism": f"classes dealt round-robin over {world} GPU(s), no exchange",
+            "parallelism": (f"classes dealt round-robin over {world} GPU(s), no exchange"
+                            if world <= cls.n_classes else
+                            f"2-D: {cls.n_classes} class groups x {world // cls.n_classes} ranks "
+                            "sharding each class's minibatch (split refresh)"),
             "l2": "keys and diagonals exceed L2"}
 
     def profile_step(self):
@@ -877,9 +914,10 @@ class OvrWorkload(TrainWorkload):
         xb, yb = self.pool_dev[self.it % self.n_pool]
         self.it += 1
         for c, g in self.graphs.items():
+            grp = self.cgroup.get(c) if len(self.members[c]) > 1 else logreg._SOLO
             w, u = logreg.train_minibatch(g.w, g.u, xb, yb[c], self.batch_rows, self.cfg,
                                           self.keys, self.sig, self.layout, self.refresher,
-                                          local_shard=True)
+                                          local_shard=True, group=grp)
             for dst, src in ((g.w, w), (g.u, u)):
                 dst.c0.data.copy_(src.c0.data)
                 dst.c1.data.copy_(src.c1.data)
@@ -929,7 +967,7 @@ class OvrWorkload(TrainWorkload):
         top = self.ctx.output_level
         for g in self.graphs.values():
             for dst in (g.w, g.u):
-                z = logreg._zeros_ct(self.params, self.keys, top)
+                z = zeros_ct(self.params, self.keys, top)
                 dst.c0.data.copy_(z.c0.data)
                 dst.c1.data.copy_(z.c1.data)
         self.it = 0

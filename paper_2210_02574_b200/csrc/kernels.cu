@@ -1043,7 +1043,7 @@ namespace hegpu {
 // diagonal, every baby and every output is touched exactly once (the per-giant
 // formulation re-reads all babies once per giant).
 // ---------------------------------------------------------------------------
-constexpr int kBsgsMaxTerms = 128;
+constexpr int kBsgsMaxTerms = 256;
 
 struct BsgsParams {
   const uint64_t* baby[kBsgsMaxTerms];
@@ -1341,7 +1341,7 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
                  int64_t pt_stride, int pt_log_run, const int32_t* pt_idx, int n_giants,
                  uint64_t* out, int64_t out_gstride, int k, cudaStream_t st, int kq,
                  int n_chain) {
-  if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..128 terms"};
+  if (n_terms < 1 || n_terms > kBsgsMaxTerms) throw HegpuError{HEGPU_E_ARG, "bsgs: 1..256 terms"};
   if (pt_log_run < 0 || pt_log_run > 5 || pt_log_run >= log_n)
     throw HegpuError{HEGPU_E_ARG, "bsgs: pt_log_run must be in [0, 5]"};
   if ((1 << log_n) % kBsgsTile) throw HegpuError{HEGPU_E_ARG, "bsgs: N too small"};

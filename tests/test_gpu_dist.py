@@ -120,6 +120,8 @@ def _captured_worker(rank, world, port, out):
         from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg, shard
 
         params, keys, sig, layout, ctx, cfg, xs, ys, w0, u0, ops = _boot_setup()
+        w0 = shard.broadcast_ciphertext(w0, 0, w0)  # identical state on every rank
+        u0 = shard.broadcast_ciphertext(u0, 0, u0)
         lo, hi = shard.shard_range(len(xs), rank, world)
         xb, yb = ops.stack(xs[lo:hi]), ops.stack(ys[lo:hi])
         ref = bs.BootstrapRefresher(ctx, keys)
@@ -135,8 +137,9 @@ def _captured_worker(rank, world, port, out):
 
 def test_two_rank_captured_sharded_minibatch():
     """CapturedShardedMinibatch over two (gloo) ranks: each rank's gradient
-    graph, the eager modular all-reduce, w refreshed by rank 0's and u by rank
-    1's captured bootstrap, broadcast: both ranks end with the same limbs,
+    graph, the eager modular all-reduce, then the segment-captured packed
+    refresh with the transforms' giants split across the ranks (eager modular
+    all-reduces between the segments): both ranks end with the same limbs,
     decrypting like the single-process eager update (up to bootstrap error)."""
     from paper_2210_02574_b200 import bootstrap as bs, ckks, logreg
 
