@@ -272,6 +272,15 @@ int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* p
                       const uint64_t* const* key_b, const uint64_t* const* key_a, int n_digits,
                       uint64_t* out, int rescale, int pq_in, void* stream);
 
+/* Scratch allocator hook.  The library's temporary device buffers
+ * (stream-ordered, freed before the call returns in stream order) come from
+ * alloc/free when set -- e.g. a framework's caching allocator, so one pool
+ * serves both -- and from cudaMallocAsync/cudaFreeAsync when both are NULL.
+ * alloc(bytes, stream) returns NULL on failure (-> HEGPU_E_NOMEM). */
+typedef void* (*hegpu_alloc_fn)(size_t bytes, void* stream);
+typedef void (*hegpu_free_fn)(void* ptr, size_t bytes, void* stream);
+int hegpu_set_allocator(hegpu_alloc_fn alloc, hegpu_free_fn free_fn);
+
 /* ModDown of P-scaled extended-basis ciphertexts by q_level * P (the final
  * step of a double-hoisted transform, bootstrap.py:243-247 + keys.py:330-338):
  * in (n_batch, 2, level+1+K, N) eval form (clobbered) -> out (n_batch, 2,

@@ -29,6 +29,42 @@ def require():
     _lib.require_gpu()
     if not torch.cuda.is_available():
         raise DeviceError("torch sees no CUDA device")
+    if not _ALLOCATOR:
+        _install_allocator()
+
+
+_ALLOCATOR = []  # keeps the ctypes callbacks alive
+
+
+def _install_allocator():
+    """Route libhegpu's scratch buffers through torch's caching allocator
+    (hegpu_set_allocator): one pool for tensors and scratch, so a large
+    workload (e.g. the full-slot ingest next to ~100 GB of keys and data)
+    does not strand memory in one allocator that the other needs.
+    HEGPU_DRIVER_SCRATCH=1 keeps the driver's stream-ordered pool."""
+    import ctypes
+    import os
+
+    if os.environ.get("HEGPU_DRIVER_SCRATCH") == "1":
+        _ALLOCATOR.append(None)
+        return
+    alloc_t = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+    free_t = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+    def _alloc(nbytes, stream):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(),
+                                                      int(stream or 0))
+        except Exception:  # noqa: BLE001 -- OOM becomes HEGPU_E_NOMEM in the library
+            return None
+
+    def _free(ptr, nbytes, stream):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    fa, ff = alloc_t(_alloc), free_t(_free)
+    _lib.call("hegpu_set_allocator", ctypes.cast(fa, ctypes.c_void_p),
+              ctypes.cast(ff, ctypes.c_void_p))
+    _ALLOCATOR.extend([fa, ff])
 
 
 def device():
@@ -170,10 +206,19 @@ def pin_cached():
     return refs
 
 
-def release_cached():
-    """Return torch's cached free blocks to the driver (not while a graph is
+def driver_scratch():
+    """True when libhegpu's scratch uses the driver pool, not torch's allocator."""
+    return bool(_ALLOCATOR) and _ALLOCATOR[0] is None
+
+
+def release_cached(min_free_bytes=48 << 30):
+    """Return torch's cached free blocks to the driver when less than
+    `min_free_bytes` of device memory is free (not while a graph is
     captured): libhegpu's scratch comes from the stream-ordered pool
-    (cudaMallocAsync), which cannot reuse memory torch's allocator caches."""
-    if torch is not None and torch.cuda.is_available() and \
-            not torch.cuda.is_current_stream_capturing():
+    (cudaMallocAsync), which cannot reuse memory torch's allocator caches.
+    Releasing unconditionally costs the next call its re-allocations."""
+    if torch is None or not torch.cuda.is_available() or \
+            torch.cuda.is_current_stream_capturing():
+        return
+    if torch.cuda.mem_get_info()[0] < min_free_bytes:
         torch.cuda.empty_cache()

@@ -55,6 +55,7 @@ SIGNATURES = {
     "hegpu_ks_hoisted": [_P, _I, _I, _P, _I64, _I64, _I, _I, _P, _P, _P, _I, _P, _I, _P],
     "hegpu_bsgs_giants": [_P, _I, _I, _P, _I64, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P],
     "hegpu_moddown_rescale_ext": [_P, _I, _I, _P, _I, _P, _P],
+    "hegpu_set_allocator": [_P, _P],
     "hegpu_rescale": [_P, _I, _P, _I64, _P, _I64, _I, _P],
     "hegpu_mod_raise": [_P, _P, _I64, _P, _I64, _I, _I, _P],
     "hegpu_encrypt_combine": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],

@@ -262,8 +262,12 @@ constexpr int kNttPolysPerCta = HEGPU_NTT_PPB;
 // conversion prologue: up to this many source limbs take the unrolled path
 // (all source words of a coefficient in flight at once)
 constexpr int kConvMaxSrc = 8;
+#ifndef HEGPU_NTT_BULK
+#define HEGPU_NTT_BULK 0  // measured: 76.5 ms per train step with it, 75.1 without (3 vs 4 CTAs/SM)
+#endif
 #ifndef HEGPU_BLOCKS_MINB
-#define HEGPU_BLOCKS_MINB 4
+// 3 with the bulk-prefetch buffers (their shared memory fits 3 CTAs per SM)
+#define HEGPU_BLOCKS_MINB (HEGPU_NTT_BULK ? 3 : 4)
 #endif
 #ifndef HEGPU_CONV_HYBRID
 #define HEGPU_CONV_HYBRID 0
@@ -316,10 +320,13 @@ constexpr size_t cols_r_smem() {
   return ((size_t)(1 << LOGS) * (kRegWarps + 1) + kRegWarps * RegShape<LOGS>::PAD_S) * 8 +
          (size_t)(1 << LOGS) * 16 + kConvMaxSrc * 3 * 8 + kConvMaxSrc * 16;
 }
+// blocks pass: each warp's next-poly block is prefetched into shared memory
+// by a bulk copy (TMA engine) while the current one is transformed
 template <int LOGS>
 constexpr size_t blocks_r_smem() {
   return (size_t)kRegWarps * RegShape<LOGS>::PAD_S * 8 +
-         (size_t)kRegWarps * (1 << LOGS) * 16;
+         (size_t)kRegWarps * (1 << LOGS) * 16 +
+         (HEGPU_NTT_BULK ? (size_t)kRegWarps * ((1 << LOGS) * 8 + 16) : 0);
 }
 
 // CM: first-pass input -- 0 plain load, 1 centered lift of one limb
@@ -571,12 +578,28 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_BLOCKS_
     }
   }
   const uint64_t cc = P.epi ? P.c[limb] : 0, ccsh = P.epi ? P.csh[limb] : 0;
+  auto src_of = [&](int poly) {
+    return INV ? (sg.in + poly * sg.in_stride + off) : (sg.out + poly * sg.out_stride + off);
+  };
   auto load = [&](uint64_t (&x)[E], int poly) {
-    const uint64_t* src = INV ? (sg.in + poly * sg.in_stride + off)
-                              : (sg.out + poly * sg.out_stride + off);
+    const uint64_t* src = src_of(poly);
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = src[lane + 32 * e];
   };
+  // bulk prefetch: this warp's S-word block of the next poly lands in pbuf
+  // (mbarrier bar) while the current poly is transformed in registers
+  uint64_t* pbuf = reinterpret_cast<uint64_t*>(stw + kRegWarps * (S - 1)) + (size_t)warp * S;
+  uint64_t* pbar =
+      reinterpret_cast<uint64_t*>(stw + kRegWarps * (S - 1)) + (size_t)kRegWarps * S + warp * 2;
+  if (HEGPU_NTT_BULK) {
+    if (lane == 0) {
+      mbar_init(pbar, 1);
+      mbar_init_fence();
+      mbar_expect_tx(pbar, S * 8);
+      bulk_g2s(pbuf, src_of(U.p0), S * 8, pbar);
+    }
+    __syncwarp();
+  }
   auto finish = [&](uint64_t (&x)[E], int poly) {
     uint64_t* dst = sg.out + poly * sg.out_stride + off;
     if (!INV) {
@@ -617,7 +640,19 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_BLOCKS_
   uint64_t x[E];
 #pragma unroll 1
   for (int pi = 0; pi < U.np; ++pi) {
-    load(x, U.p0 + pi);
+    if (HEGPU_NTT_BULK) {
+      mbar_wait(pbar, pi & 1);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = pbuf[lane + 32 * e];
+      __syncwarp();
+      if (lane == 0 && pi + 1 < U.np) {  // refill the buffer with the next poly's block
+        fence_proxy_async_smem();
+        mbar_expect_tx(pbar, S * 8);
+        bulk_g2s(pbuf, src_of(U.p0 + pi + 1), S * 8, pbar);
+      }
+    } else {
+      load(x, U.p0 + pi);
+    }
     if (pi == 0) {
       cp_async_wait_all();
       __syncthreads();

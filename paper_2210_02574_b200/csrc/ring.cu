@@ -60,15 +60,35 @@ ProfScope::~ProfScope() {
 
 // Stream-ordered scratch from the device's default memory pool (cached: the
 // pool's release threshold is raised at ring creation).
+// Scratch memory: stream-ordered, from the host's allocator when one is
+// registered (hegpu_set_allocator: the Python layer registers torch's caching
+// allocator, so tensors and scratch share ONE pool and neither strands memory
+// the other needs), else the driver's stream-ordered pool (cudaMallocAsync).
+static hegpu_alloc_fn g_alloc = nullptr;
+static hegpu_free_fn g_free = nullptr;
+
 struct Scratch {
   void* p = nullptr;
+  size_t n = 0;
   cudaStream_t st;
-  Scratch(size_t bytes, cudaStream_t s) : st(s) {
-    if (bytes) check_cuda(cudaMallocAsync(&p, bytes, s), "scratch alloc");
+  Scratch(size_t bytes, cudaStream_t s) : n(bytes), st(s) {
+    if (!bytes) return;
+    if (g_alloc) {
+      p = g_alloc(bytes, static_cast<void*>(s));
+      if (!p) throw HegpuError{HEGPU_E_NOMEM, "scratch alloc: out of memory (host allocator)"};
+    } else {
+      check_cuda(cudaMallocAsync(&p, bytes, s), "scratch alloc");
+    }
   }
   ~Scratch() {
-    if (p) cudaFreeAsync(p, st);
+    if (!p) return;
+    if (g_alloc && g_free)
+      g_free(p, n, static_cast<void*>(st));
+    else if (!g_alloc)
+      cudaFreeAsync(p, st);
   }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
   uint64_t* u64() const { return static_cast<uint64_t*>(p); }
 };
 
@@ -1797,6 +1817,15 @@ int hegpu_bsgs_giants(hegpu_ring_t ring, int level, int alpha, const uint64_t* p
     }
     bsgs_giants_impl(R, level, alpha, partials, gstride, n_batch, n_giants, galois, key_b, key_a,
                      n_digits, out, S_(stream), rescale != 0);
+  })
+}
+
+int hegpu_set_allocator(hegpu_alloc_fn alloc, hegpu_free_fn free_fn) {
+  HEGPU_TRY({
+    if ((alloc == nullptr) != (free_fn == nullptr))
+      throw HegpuError{HEGPU_E_ARG, "allocator needs both alloc and free (or neither)"};
+    g_alloc = alloc;
+    g_free = free_fn;
   })
 }
 

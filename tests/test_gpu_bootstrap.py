@@ -259,3 +259,24 @@ def test_full_slot_bootstrap_batched(boot_full):
     outs = bs.bootstrap_many(cts, ctx, keys)
     for o, v in zip(outs, vs):
         assert np.max(np.abs(ckks.decrypt_vector(o, keys) - v)) < 1e-2
+
+
+def test_segmented_capture_replays_bootstrap(boot):
+    """bootstrap.SegmentedCapture (the capture the sharded trainer uses around
+    its split refresh) replays a bootstrap with the eager result's limbs."""
+    import torch
+
+    params, ctx, keys, _ = boot
+    v = np.random.default_rng(41).uniform(-1, 1, 64)
+    ct = ckks.encrypt_vector(params, v, keys, level=0, rng_seed=42)
+    want = bs.bootstrap(ct, ctx, keys)
+    inp = ct.copy()
+    seg = bs.SegmentedCapture()
+    out = seg.capture(lambda: bs.bootstrap(inp, ctx, keys))
+    assert len(seg.graphs) == 1 and not seg.points  # one process: no collective cut
+    inp.c0.data.copy_(ct.c0.data)
+    inp.c1.data.copy_(ct.c1.data)
+    seg.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.c0.limbs, want.c0.limbs)
+    assert np.array_equal(out.c1.limbs, want.c1.limbs)

@@ -51,3 +51,52 @@ for name, fn in (("gradient", lambda: logreg._batched_gradient(xb, yb, wl.w, lay
     _lib.profile_enable(False)
     print(name, {c: round(p["ms"], 1) for c, p in prof.items() if p["launches"]},
           {c: p["launches"] for c, p in prof.items() if p["launches"]})
+
+# captured (graph-replayed) device time of the two phases, as in the bench
+from paper_2210_02574_b200 import bootstrap as bs  # noqa: E402
+
+
+def captured_ms(fn, reps=5):
+    seg = bs.SegmentedCapture()
+    fn()  # warm caches
+    seg.capture(fn)
+    seg.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        seg.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+grad_ms = captured_ms(lambda: logreg._gradient_phase(wl.w, wl.u, xb, yb, wl.batch_rows, cfg, keys,
+                                                     sig, layout))
+ref_ms = captured_ms(lambda: wl.refresher.refresh_many([w2, u2]))
+print(f"captured: gradient phase (lookahead + 16 gradients + sum) {grad_ms:.2f} ms, "
+      f"packed refresh {ref_ms:.2f} ms")
+
+# per-rank device time at G ranks, simulated on this GPU: the rank's shard of
+# the gradient (16/G ciphertexts) and the split refresh with rank 0's share of
+# the giant steps (the modular all-reduces are skipped: the numbers are
+# garbage, the timing is the rank's compute).  Collective cost is added in
+# DESIGN.md from the message sizes.
+from paper_2210_02574_b200 import shard  # noqa: E402
+
+_real_ar = shard.allreduce_residues
+for G in (2, 4, 8):
+    shard.allreduce_residues = lambda *a, **k: None
+    xs, ys = ops.unstack(xb), ops.unstack(yb)
+    lo, hi = shard.shard_range(len(xs), 0, G)
+    xg, yg = ops.stack(xs[lo:hi]), ops.stack(ys[lo:hi])
+    g_ms = captured_ms(lambda: logreg._gradient_phase(wl.w, wl.u, xg, yg, wl.batch_rows, cfg,
+                                                      keys, sig, layout))
+    bs._DIST = (0, G, None)
+    try:
+        r_ms = captured_ms(lambda: wl.refresher.refresh_many([w2, u2]))
+    finally:
+        bs._DIST = None
+        shard.allreduce_residues = _real_ar
+    print(f"G={G}: rank-0 gradient shard ({hi - lo} cts) {g_ms:.2f} ms, split refresh share "
+          f"{r_ms:.2f} ms", flush=True)
