@@ -159,3 +159,34 @@ def allreduce_residues(t, primes_idx, params, group=None):
         primes_idx.ctypes.data, None, _dev.stream(),
     )
     return t
+
+
+def reduce_scatter_residues(t, out, primes_idx, params, group=None):
+    """Modular reduce-scatter along dim 0: `out` (t.shape[0] // world rows of
+    t's layout) receives this rank's contiguous block of the sum over ranks,
+    reduced mod q.  NCCL reduce_scatter_tensor when available (half the
+    traffic of an all-reduce), else an all-reduce and a copy of the block."""
+    import torch.distributed as dist
+
+    rank, ws = world(group)
+    if ws == 1:
+        out.copy_(t)
+        return out
+    n = int(t.shape[0])
+    if dist.get_backend(group) == "nccl" and n % ws == 0:
+        primes_idx = np.ascontiguousarray(primes_idx, dtype=np.int32)
+        all_primes = list(params.ring.moduli_chain) + list(params.ring.special_moduli)
+        if not check_allreduce_exact([all_primes[i] for i in primes_idx], ws):
+            raise ValueError("world size too large for an exact wrapping reduction")
+        dist.reduce_scatter_tensor(out, t, op=dist.ReduceOp.SUM, group=group)
+        k, nn = int(out.shape[-2]), int(out.shape[-1])
+        p, cnt, s = _dev.group(out, k, nn)
+        _lib.call(
+            "hegpu_elementwise", params.ring.device(), _lib.OP_REDUCE, p, s, None, 0, p, s, cnt,
+            k, primes_idx.ctypes.data, None, _dev.stream(),
+        )
+        return out
+    allreduce_residues(t, primes_idx, params, group)
+    lo, hi = shard_range(n, rank, ws)
+    out.copy_(t[lo:hi])
+    return out

@@ -92,11 +92,15 @@ for G in (2, 4, 8):
     xg, yg = ops.stack(xs[lo:hi]), ops.stack(ys[lo:hi])
     g_ms = captured_ms(lambda: logreg._gradient_phase(wl.w, wl.u, xg, yg, wl.batch_rows, cfg,
                                                       keys, sig, layout))
-    bs._DIST = (0, G, None)
-    try:
-        r_ms = captured_ms(lambda: wl.refresher.refresh_many([w2, u2]))
-    finally:
-        bs._DIST = None
-        shard.allreduce_residues = _real_ar
-    print(f"G={G}: rank-0 gradient shard ({hi - lo} cts) {g_ms:.2f} ms, split refresh share "
-          f"{r_ms:.2f} ms", flush=True)
+    shares = {}
+    for babies in (False, True):
+        bs._DIST = (0, G, None)
+        bs.SPLIT_BABIES = babies
+        try:
+            shares[babies] = captured_ms(lambda: wl.refresher.refresh_many([w2, u2]))
+        finally:
+            bs._DIST = None
+    shard.allreduce_residues = _real_ar
+    print(f"G={G}: rank-0 gradient shard ({hi - lo} cts) {g_ms:.2f} ms, split refresh share: "
+          f"giants only {shares[False]:.2f} ms, giants + babies {shares[True]:.2f} ms",
+          flush=True)
