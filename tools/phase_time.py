@@ -85,8 +85,10 @@ print(f"captured: gradient phase (lookahead + 16 gradients + sum) {grad_ms:.2f} 
 from paper_2210_02574_b200 import shard  # noqa: E402
 
 _real_ar = shard.allreduce_residues
+_real_rs = shard.reduce_scatter_residues
 for G in (2, 4, 8):
     shard.allreduce_residues = lambda *a, **k: None
+    shard.reduce_scatter_residues = lambda t, out, *a, **k: out.copy_(t[: out.shape[0]])
     xs, ys = ops.unstack(xb), ops.unstack(yb)
     lo, hi = shard.shard_range(len(xs), 0, G)
     xg, yg = ops.stack(xs[lo:hi]), ops.stack(ys[lo:hi])
@@ -101,6 +103,7 @@ for G in (2, 4, 8):
         finally:
             bs._DIST = None
     shard.allreduce_residues = _real_ar
+    shard.reduce_scatter_residues = _real_rs
     print(f"G={G}: rank-0 gradient shard ({hi - lo} cts) {g_ms:.2f} ms, split refresh share: "
           f"giants only {shares[False]:.2f} ms, giants + babies {shares[True]:.2f} ms",
           flush=True)
