@@ -60,8 +60,15 @@ def init_dist(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_ONE_DEVICE_GLOO=1: every rank on cuda:0 over gloo -- a functional
+        # check of the multi-rank path on a one-GPU box (NCCL refuses two ranks
+        # on one device); its timings are not a scaling measurement
+        if os.environ.get("BENCH_ONE_DEVICE_GLOO") == "1":
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world
@@ -1048,7 +1055,7 @@ def run_ours(args):
         wl.step()
     torch.cuda.synchronize()
     n0 = _lib.launch_count()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+    with ClockSampler(0 if os.environ.get("BENCH_ONE_DEVICE_GLOO") == "1" else int(os.environ.get("LOCAL_RANK", 0))) as clk:
         ms = timed(wl.step, args.steps, world)
     launches = _lib.launch_count() - n0
     graph = getattr(wl, "graph", None)

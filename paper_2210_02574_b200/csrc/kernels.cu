@@ -809,6 +809,110 @@ __global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot(const __grid_constant_
   }
 }
 
+// n_batch == 1 (the bootstrap's hoisted babies): two adjacent coefficients
+// per thread -- the key words load as one 16-byte pair, the digit words are
+// gathered per coefficient -- so each thread keeps 4 independent accumulators
+// and half as many key-load instructions are issued per byte.
+#ifndef HEGPU_IPROT_1X2
+#define HEGPU_IPROT_1X2 1
+#endif
+constexpr bool kIpRot1x2 = HEGPU_IPROT_1X2;
+template <int BETA>
+__global__ void __launch_bounds__(kEwThreads) k_ks_ip_rot1x2(const __grid_constant__ IpRotParams P) {
+  const int N = 1 << P.log_n;
+  const int r = blockIdx.z;
+  const int x = (blockIdx.y * kEwThreads + threadIdx.x) * 2;
+  if (x >= N) return;
+  const int prime = r <= P.level ? r : P.n_chain + (r - P.level - 1);
+  const int krow = r <= P.level ? r : P.key_sp_row0 + (r - P.level - 1);
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t* base[BETA];
+  int64_t rstr[BETA];
+#pragma unroll
+  for (int j = 0; j < BETA; ++j) {
+    const int g0 = j * P.alpha;
+    const int g1 = min(g0 + P.alpha, P.level + 1);
+    if (r >= g0 && r < g1) {
+      base[j] = P.d + (size_t)r * N;
+      rstr[j] = P.d_sr;
+    } else {
+      base[j] = P.ext + j * P.ext_sj + (size_t)(r < g0 ? r : r - (g1 - g0)) * N;
+      rstr[j] = P.ext_sr;
+    }
+  }
+  const size_t koff = (size_t)krow * N + x;
+  Mac128 ab[2], aa[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    ab[h].zero();
+    aa[h].zero();
+  }
+  int since = 0;
+  for (int rot = 0; rot < P.n_rot; ++rot) {
+    const uint32_t s0 = auto_src((uint32_t)x, P.gal[rot], P.log_n);
+    const uint32_t s1 = auto_src((uint32_t)x + 1, P.gal[rot], P.log_n);
+    ulonglong2 kb[BETA], ka[BETA];
+    uint64_t v0[BETA], v1[BETA];
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      if (j < P.beta) {
+        kb[j] = __ldg(reinterpret_cast<const ulonglong2*>(P.kb[rot][j] + koff));
+        ka[j] = __ldg(reinterpret_cast<const ulonglong2*>(P.ka[rot][j] + koff));
+        const uint64_t* bp = base[j] + rot * rstr[j];
+        v0[j] = __ldg(bp + s0);
+        v1[j] = __ldg(bp + s1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      if (j < P.beta) {
+        ab[0].add(v0[j], kb[j].x);
+        ab[1].add(v1[j], kb[j].y);
+        aa[0].add(v0[j], ka[j].x);
+        aa[1].add(v1[j], ka[j].y);
+        if (++since == kMacFold) {
+          since = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ab[h].fold(pc.q, pc.bar);
+            aa[h].fold(pc.q, pc.bar);
+          }
+        }
+      }
+    }
+    if (!P.sum_mode || rot == P.n_rot - 1) {
+      uint64_t* o = P.acc + (P.sum_mode ? 0 : rot * P.acc_sr) + (size_t)r * N + x;
+      uint64_t vb[2], va[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        vb[h] = mont_mul(ab[h].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+        va[h] = mont_mul(aa[h].redc(pc), pc.r2, pc.q, pc.qinv_neg);
+      }
+      if (P.c0 && r <= P.level) {
+        const uint64_t* c0 = P.c0 + (size_t)r * N;
+        vb[0] = add_mod(vb[0], shoup(__ldg(c0 + s0), P.pm[r], P.pm_sh[r], pc.q), pc.q);
+        vb[1] = add_mod(vb[1], shoup(__ldg(c0 + s1), P.pm[r], P.pm_sh[r], pc.q), pc.q);
+      }
+      if (P.accumulate) {
+        const ulonglong2 pb = *reinterpret_cast<const ulonglong2*>(o);
+        const ulonglong2 pa = *reinterpret_cast<const ulonglong2*>(o + (size_t)P.n_ext * N);
+        vb[0] = add_mod(vb[0], pb.x, pc.q);
+        vb[1] = add_mod(vb[1], pb.y, pc.q);
+        va[0] = add_mod(va[0], pa.x, pc.q);
+        va[1] = add_mod(va[1], pa.y, pc.q);
+      }
+      *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(vb[0], vb[1]);
+      *reinterpret_cast<ulonglong2*>(o + (size_t)P.n_ext * N) = make_ulonglong2(va[0], va[1]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ab[h].zero();
+        aa[h].zero();
+      }
+      since = 0;
+    }
+  }
+}
+
 template <int BG>
 static void launch_ip_rot_bg(IpRotParams& P, dim3 grid, cudaStream_t st) {
   if (P.beta <= 2)
@@ -830,6 +934,17 @@ void launch_ks_ip_rot(IpRotParams& P, cudaStream_t st) {
                    ipn * 8.0 * 2.0 * P.n_batch * (P.sum_mode ? 1 : P.n_rot),
                ipn * P.n_batch * P.n_rot * 2.0 * P.beta);
   if (launch_ks_ip_rot_tma(P, st)) return;
+  if (P.n_batch == 1 && (1 << P.log_n) >= 2 * kEwThreads && kIpRot1x2) {
+    dim3 g2(1, ((1 << P.log_n) / 2 + kEwThreads - 1) / kEwThreads, P.n_ext);
+    if (P.beta <= 2)
+      k_ks_ip_rot1x2<2><<<g2, kEwThreads, 0, st>>>(P);
+    else if (P.beta <= 4)
+      k_ks_ip_rot1x2<4><<<g2, kEwThreads, 0, st>>>(P);
+    else
+      k_ks_ip_rot1x2<kMaxRotDigits><<<g2, kEwThreads, 0, st>>>(P);
+    check_cuda(cudaGetLastError(), "ks rotation inner product launch");
+    return;
+  }
   if (bg == 4)
     launch_ip_rot_bg<4>(P, grid, st);
   else if (bg == 2)
