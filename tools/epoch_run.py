@@ -33,7 +33,8 @@ from paper_2210_02574_b200.synth import make_separable  # noqa: E402
 def main():
     n_rows = int(sys.argv[1]) if len(sys.argv) > 1 else 67349
     n_test = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
-    params = ckks.get_preset("p16")
+    preset = os.environ.get("EPOCH_PRESET", "p16")  # "p16s": the 128-bit-secure preset
+    params = ckks.get_preset(preset)
     sig = minimax.load_approximant("sigmoid_deg15")
     layout = logreg.make_layout(params, 768)
     ctx = bs.build_context(params, n_slots=layout.padded_dim, input_periodic=True,
@@ -88,7 +89,7 @@ def main():
 
     epoch_s = timing[0]["seconds"]
     rec = {
-        "workload": "cfg4 one epoch, public logreg.train(), P16, SST-2-sized synthetic 768-d",
+        "workload": f"cfg4 one epoch, public logreg.train(), {preset}, SST-2-sized synthetic 768-d",
         "rows": n_rows, "test_rows": n_test, "data_cts": len(pairs),
         "minibatches": -(-n_rows // cfg.batch_size),
         "epoch_seconds": round(epoch_s, 3),
