@@ -205,8 +205,12 @@ def zeros_ct(params, keys, level, seed=4242):
                         rng_seed=seed)
 
 
-# BENCH_BOOT_PRESET=p16s: cfg3 on the 128-bit-secure preset (h = 192)
-BOOT_PRESET = os.environ.get("BENCH_BOOT_PRESET", "p16")
+# The N = 2^16 preset of every workload but cfg1: "p16s", the 128-bit-secure
+# bootstrappable preset the north star names (h = 192), or "p16",
+# the reference-parity preset (h = 64, insecure-test-only).  BENCH_PRESET
+# selects it; BENCH_BOOT_PRESET overrides it for cfg3.
+PRESET = os.environ.get("BENCH_PRESET", "p16s")
+BOOT_PRESET = os.environ.get("BENCH_BOOT_PRESET", PRESET)
 
 
 def boot_preset():
@@ -218,7 +222,7 @@ def boot_preset():
 def p16():
     from paper_2210_02574_b200 import ckks
 
-    return ckks.get_preset("p16")
+    return ckks.get_preset(PRESET)
 
 
 class KsWorkload:
@@ -252,7 +256,7 @@ class KsWorkload:
         self.h2d = self.host.numel() * 8
         self.d2h = self.out_host.numel() * 8
         self.units = self.batch * world
-        self.config = {"workload": "cfg2 NTT/iNTT + key-switch microbench", "preset": "p16",
+        self.config = {"workload": "cfg2 NTT/iNTT + key-switch microbench", "preset": PRESET,
                        "N": n, "level": L, "ciphertexts_per_gpu": self.batch,
                        "l2": "inputs (1.4 GiB) exceed L2"}
 
@@ -689,7 +693,7 @@ class TrainWorkload:
     def static_config(cls, world):
         return {
             "workload": "cfg4 encrypted-LR training minibatch (SST-2-shaped synthetic 768-d)",
-            "preset": "p16", "N": 65536,
+            "preset": PRESET, "N": 65536,
             "batch_rows": cls.batch_rows * (world if WEAK else 1),
             "ciphertexts_per_minibatch": cls.batch_rows * (world if WEAK else 1) // 32,
             "rows_per_ct": 32,
@@ -926,7 +930,7 @@ class OvrWorkload(TrainWorkload):
         return {
             "workload": "cfg5 encrypted One-vs-Rest training minibatch (AG-News-shaped "
                         "synthetic 1024-d, 4 classes)",
-            "preset": "p16", "N": 65536, "batch_rows": cls.batch_rows,
+            "preset": PRESET, "N": 65536, "batch_rows": cls.batch_rows,
             "classes": cls.n_classes, "ciphertexts_per_minibatch": cls.batch_rows // 16,
             "rows_per_ct": 16,
             "refresh": "per class: w and u refreshed as one batch of two sparse-2048 "
@@ -1243,10 +1247,14 @@ def run_reference(args):
         def to_config_text(self):
             return self.text
 
-    preset = "p14" if args.config == "predict" else "p16"
+    preset = "p14" if args.config == "predict" else (
+        BOOT_PRESET if args.config.startswith("bootstrap") else PRESET)
     wl.params = _Preset(os.path.join(REPO, "paper_2210_02574_b200", "presets", f"{preset}.preset"))
     if args.config in ("train", "bootstrap", "bootstrap_full", "predict", "ovr"):
-        wl.histogram = load_histogram(args.config)
+        try:  # the histogram recorded on this preset, else the P16 one
+            wl.histogram = load_histogram(f"{args.config}_{preset}")
+        except OSError:
+            wl.histogram = load_histogram(args.config)
         # the modelled minibatch is the reference's 512 rows (samples/s does not
         # depend on how many minibatches a step holds)
         wl.units = TrainWorkload.batch_rows if args.config in ("train", "ovr") else 1

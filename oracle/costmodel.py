@@ -49,6 +49,9 @@ class OracleCostModel:
 
     def sample(self, ks_levels, other_levels):
         p = self.p
+        top = len(p.chain) - 1  # a histogram recorded on a deeper chain: clamp its levels
+        ks_levels = [min(int(lvl), top) for lvl in ks_levels]
+        other_levels = [min(int(lvl), top) for lvl in other_levels]
         for lvl in sorted(set(ks_levels)):
             d = self._rand(lvl, 100 + lvl)
             self.t[("ks", lvl)] = self._time(lambda: S.ks_apply(p, self.keys.relin, d, lvl))
@@ -79,9 +82,10 @@ class OracleCostModel:
     def seconds(self, histogram):
         """Modelled reference seconds for an op histogram {"op@level": count}."""
         total = 0.0
+        top = len(self.p.chain) - 1
         for key, count in histogram.items():
             op, lvl = key.split("@")
-            total += count * self._interp(op, int(lvl))
+            total += count * self._interp(op, min(int(lvl), top))
         return total
 
 
