@@ -1,6 +1,6 @@
 """The 128-bit-secure N = 2^16 bootstrappable preset (p16s: sparse secret
 h = 192, scale 2^45, 45-bit rescale primes, 50-bit q0, 60-bit CoeffToSlot
-and special primes, logQP = 1325).  Its scheme ops are pinned
+and special primes, logQP = 1430).  Its scheme ops are pinned
 bit-exact to the reference in test_gpu_ckks.py; here: full-slot and sparse
 bootstrapping within the north-star 1e-3, with the double-angle EvalMod that
 the wider h = 192 range (K = 25) needs."""
@@ -27,7 +27,7 @@ def test_p16s_context(secure):
     params, full, sparse, keys = secure
     assert params.secret_hamming_weight == 192 and params.default_scale == 2.0 ** 45
     assert full.range_k == 25 and full.double_angle == 4 and full.evalmod_poly.degree == 31
-    assert full.output_level == sparse.output_level == params.max_level - 12 == 8
+    assert full.output_level == sparse.output_level == params.max_level - 12 == 9
 
 
 def test_p16s_full_slot_bootstrap_within_1e3(secure):
