@@ -700,7 +700,7 @@ class TrainWorkload:
             "refresh": "w and u refreshed together: one packed sparse bootstrap of period 2048 (two of period 1024 in the reference)",
             "evalmod": SPARSE_EVALMOD,
             "parallelism": f"minibatch sharded over {world} GPU(s)",
-            "l2": "keys (>14 GiB) and diagonals (36 GiB) exceed L2"}
+            "l2": "inputs exceed L2 (126 MB): keys ~30 GiB, run-compressed diagonals ~10 GiB, minibatch 0.3 GiB"}
 
     def profile_step(self):
         """Eager (un-captured) step: per-launch profile and op histogram."""
