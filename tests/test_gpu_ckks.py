@@ -318,3 +318,40 @@ def test_batched_ciphertext_ingest(desk_keys):
         ckks.deserialize_ciphertexts(blobs + [other], params)
     with pytest.raises(SerializationError):
         ckks.deserialize_ciphertexts([blobs[0][:-8]], params)
+
+
+def test_tma_and_register_inner_products_agree(digests):
+    """The TMA-staged key-switch inner product (default) and the
+    register-staged one (HEGPU_NO_TMA=1, a separate process: the switch is read
+    once) give the same limbs -- both equal the reference's digests."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, numpy as np\n"
+        "from oracle.scheme import sha\n"
+        "from paper_2210_02574_b200 import ckks, ring\n"
+        "from paper_2210_02574_b200.ckks import keys as K\n"
+        "from conftest import preset_text\n"
+        "p = ckks.CkksParams.from_config_text(preset_text('p16'))\n"
+        "keys = ckks.keygen(p, rotation_steps=[1], rng_seed=7, include_conjugation=False)\n"
+        "out = {}\n"
+        "for lvl in (21, 10):\n"
+        "    dp = ring.sample_poly(p.ring, 'uniform', lvl, np.random.default_rng(2000 + lvl))\n"
+        "    dp = ring.RnsPoly(p.ring, dp.limbs, ring.EVAL, lvl)\n"
+        "    kb, ka = K.ks_apply(keys, keys.relin_key, dp)\n"
+        "    out[str(lvl)] = [sha(kb.limbs), sha(ka.limbs)]\n"
+        "print(json.dumps(out))\n"
+    )
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, HEGPU_NO_TMA="1",
+               PYTHONPATH=os.pathsep.join([os.path.dirname(here), here]))
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=os.path.dirname(here))
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    for lvl in ("21", "10"):
+        if lvl in digests["p16"]["ks"]:
+            assert got[lvl] == digests["p16"]["ks"][lvl]
