@@ -219,3 +219,36 @@ def test_pair_packing_stops_at_period_1024():
     assert bs._pair_packable_ctx(ctx(64)) and bs._pair_packable_ctx(ctx(1024))
     assert not bs._pair_packable_ctx(ctx(2048))
     assert not bs._pair_packable_ctx(ctx(1024, periodic=False))
+
+
+def test_double_angle_evalmod_fit():
+    """The double-angle EvalMod base (bootstrap._cos_quarter_target): a
+    degree-31 minimax fit of cos(2 pi (x - 1/4) / 2^r) on +-(K + 1/2), whose r
+    doublings reproduce sin(2 pi x) -- the function the reference's degree-119
+    sine approximates -- to better than its fit."""
+    from paper_2210_02574_b200 import bootstrap as bs
+
+    for K, r in ((14, 3), (25, 4)):
+        D = K + 0.5
+        poly = minimax.remez_fit(bs._cos_quarter_target(D, r), (-D, D), 31)
+        x = np.linspace(-D, D, 20001)
+        c = minimax.eval_cheb(poly, x)
+        for _ in range(r):
+            c = 2 * c * c - 1
+        err = np.max(np.abs(c / (2 * np.pi) - np.sin(2 * np.pi * x) / (2 * np.pi)))
+        assert poly.certified_max_error < 1e-10
+        assert err < 1e-9
+
+
+def test_evalmod_context_levels():
+    """Level budgets: the reference sine (K = 14) costs 10 levels, the double
+    angle 11 (P16); p16s (h = 192 -> K = 25) picks the double angle with r = 4
+    and keeps output level 9 (the trainer's 8 + the packed refresh's mask)."""
+    from paper_2210_02574_b200 import bootstrap as bs
+
+    p16 = P.get_preset("p16")
+    assert bs.build_context(p16, 1024, input_periodic=True).output_level == 11
+    da = bs.build_context(p16, 1024, input_periodic=True, evalmod="double_angle")
+    assert (da.double_angle, da.output_level) == (3, 10)
+    secure = bs.build_context(P.get_preset("p16s"), 1024, input_periodic=True)
+    assert (secure.range_k, secure.double_angle, secure.output_level) == (25, 4, 9)
