@@ -19,6 +19,8 @@
 // N = 2^16 is 16 tiles, so every launch has (16 x limbs x polys) CTAs.
 // Intermediate values stay in Harvey lazy ranges ([0,4q) forward, [0,2q)
 // inverse); outputs are fully reduced.
+#include <cooperative_groups.h>
+
 #include <mutex>
 #include <vector>
 
@@ -685,6 +687,189 @@ __global__ void __launch_bounds__(32 * kRegWarps, (LOGS >= 9 ? 2 : HEGPU_BLOCKS_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused inverse NTT for N = S^2 (2^16): one thread-block CLUSTER of
+// kFuseCluster CTAs owns one (poly, limb).  Pass B (row blocks: the GS stages
+// with span < S) leaves the intermediate in the cluster's distributed shared
+// memory -- CTA c holds rows [c*ROWS, (c+1)*ROWS) -- and after one cluster
+// barrier pass A (columns: the last stages, N^-1 / post-scale) fills its
+// 8-column tiles over DSMEM.  The intermediate never reaches HBM (one read and
+// one write per coefficient instead of two of each).  Same butterflies and
+// twiddles as k_ntt_blocks_r / k_ntt_cols_r, so the limbs are identical.
+// ---------------------------------------------------------------------------
+#ifndef HEGPU_INTT_FUSED
+#define HEGPU_INTT_FUSED 0
+#endif
+#ifndef HEGPU_INTT_CLUSTER
+#define HEGPU_INTT_CLUSTER 16  // 16 (non-portable): 86 KiB smem, 2 CTAs per SM
+#endif
+constexpr int kFuseCluster = HEGPU_INTT_CLUSTER;
+constexpr int kFuseTwBufs = kFuseCluster >= 16 ? 1 : 2;  // per-warp twiddle runs in pass B
+
+template <int LOGS>
+struct FusedLayout {
+  static constexpr int S = 1 << LOGS;
+  static constexpr int ROWS = S / kFuseCluster;          // rows (and columns) per CTA
+  static constexpr int RPW = ROWS / kRegWarps;           // rows per warp in pass B
+  static constexpr int TILES = ROWS / kRegWarps;         // 8-column tiles in pass A
+  static constexpr size_t t_words = (size_t)ROWS * S;    // this CTA's rows (DSMEM-shared)
+  static constexpr size_t wb_words = (size_t)kRegWarps * RegShape<LOGS>::PAD_S;
+  static constexpr size_t stw_words = (size_t)(S - 1) * 2;           // pass-A twiddles
+  static constexpr size_t twb_words = (size_t)kRegWarps * kFuseTwBufs * (S - 1) * 2;  // pass B
+  static constexpr size_t tile_words = (size_t)S * kRegWarps * TILES;
+  static constexpr size_t region_words = twb_words > tile_words ? twb_words : tile_words;
+  static constexpr size_t bar_words = kRegWarps;
+  static constexpr size_t bytes =
+      (t_words + wb_words + stw_words + region_words + bar_words) * 8;
+};
+
+template <int LOGS>
+__global__ void __cluster_dims__(kFuseCluster, 1, 1) __launch_bounds__(32 * kRegWarps, kFuseCluster >= 16 ? 2 : 1)
+    k_intt_fused(const __grid_constant__ NttParams P) {
+  namespace cg = cooperative_groups;
+  using Sh = RegShape<LOGS>;
+  using L = FusedLayout<LOGS>;
+  constexpr int S = Sh::S, E = Sh::E, EB = Sh::EB;
+  constexpr int LO_S = LOGS - EB;
+  constexpr int ROWS = L::ROWS, RPW = L::RPW;
+  extern __shared__ __align__(128) uint64_t sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int log_n = P.log_n, N = 1 << log_n, a = log_n - LOGS;  // N == S * S
+  const UnitPos U = unit_pos(P, blockIdx.y + P.unit0);           // ppb == 1: one poly
+  const Seg& sg = P.S.seg[U.s];
+  const int limb = U.limb, poly = U.p0;
+  const int prime = P.S.sel[U.s][limb];
+  const PrimeConst pc = P.pc[prime];
+  const uint64_t q = pc.q;
+  const ulonglong2* tw =
+      reinterpret_cast<const ulonglong2*>(P.tw + (size_t)prime * 4 * N + 2 * (size_t)N);
+  const bool fpp = pc.twf != nullptr;
+  const ulonglong2* tws = fpp ? reinterpret_cast<const ulonglong2*>(pc.twf + N) : tw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* T = sm;
+  uint64_t* wbuf = T + L::t_words + warp * Sh::PAD_S;
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(T + L::t_words + L::wb_words);
+  uint64_t* region = T + L::t_words + L::wb_words + L::stw_words;
+  uint64_t* bars = region + L::region_words;
+  const uint64_t* src = sg.in + poly * sg.in_stride + (size_t)limb * N;
+  uint64_t* dst = sg.out + poly * sg.out_stride + (size_t)limb * N;
+  const double qd = (double)q, qinv = 1.0 / qd;
+  uint64_t x[E];
+
+  // ---- pass B: warp w transforms rows crank*ROWS + w*RPW + [0, RPW) in T ----
+  // the warp's RPW contiguous rows arrive by one bulk copy; per-row twiddle
+  // runs are double-buffered with cp.async, so only __syncwarp is needed
+  const int row0 = crank * ROWS + warp * RPW;
+  uint64_t* trows = T + (size_t)warp * RPW * S;
+  uint64_t* bar = bars + warp;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init_fence();
+    mbar_expect_tx(bar, RPW * S * 8);
+    bulk_g2s(trows, src + (size_t)row0 * S, RPW * S * 8, bar);
+  }
+  // pass-A twiddles: every column transform uses [1, S) of the table
+  for (int i = threadIdx.x; i < S - 1; i += blockDim.x)
+    cp_async16(stw + i, tws + tw_slot_index<LOGS, true>(i, 0));
+  ulonglong2* twb = reinterpret_cast<ulonglong2*>(region) + (size_t)warp * kFuseTwBufs * (S - 1);
+  auto stage = [&](int i) {
+    ulonglong2* d = twb + (i % kFuseTwBufs) * (S - 1);
+    const int blk = row0 + i;
+    for (int v = lane; v < S - 1; v += 32) {
+      const int code = g_tw_slot[1][LOGS - 6][v];
+      const int st = code >> 16, local = code & 0xffff;
+      cp_async16(d + v, tws + (1 << (a + st)) + (blk << st) + local);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  if (kFuseTwBufs > 1 && RPW > 1) stage(1);
+  __syncwarp();
+  mbar_wait(bar, 0);
+#pragma unroll 1
+  for (int i = 0; i < RPW; ++i) {
+    if (kFuseTwBufs > 1 && i + 1 < RPW) cp_async_wait_group<1>(); else cp_async_wait_group<0>();
+    __syncwarp();
+    const ulonglong2* tab = twb + (i % kFuseTwBufs) * (S - 1);
+    uint64_t* trow = trows + (size_t)i * S;
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = trow[lane + 32 * e];
+    if (fpp) {
+      double xf[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) xf[e] = fp_from_s64(x[e]);
+      const double2 one = make_double2(1.0, 1.0 / qd);  // no final stage in this pass
+      inv_sub_fp<LOGS>(xf, reinterpret_cast<double*>(wbuf), lane, LO_S, LO_S, -1,
+                       reinterpret_cast<const double2*>(tab), qd, qinv, one, one);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = __double_as_longlong(xf[e]);
+    } else {
+      const ulonglong2 fs = make_ulonglong2(pc.ninv, pc.ninv_sh);
+      const ulonglong2 fd = make_ulonglong2(pc.ilast, pc.ilast_sh);
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, -1, tab, pc, fs, fd);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) trow[lane + 32 * e] = x[e];
+    __syncwarp();  // this row's twiddle buffer is consumed
+    if (i + kFuseTwBufs < RPW) stage(i + kFuseTwBufs);
+  }
+  cp_async_wait_all();
+  cluster.sync();  // every CTA's rows are in place (and visible cluster-wide)
+
+  // ---- pass A: this CTA's ROWS columns as TILES tiles of 8 -----------------
+  // gather the whole 256 x ROWS block over DSMEM (16-byte loads), then each
+  // warp runs one column transform per tile
+  auto tix = [](int t, int r, int c) {
+    return (size_t)t * S * 8 + r * 8 + (c ^ ((r >> 1) & 7));
+  };
+  uint64_t* tile = region;
+  const int cbase = crank * ROWS;
+  constexpr int PAIRS = S * ROWS / 2;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < PAIRS; e += blockDim.x) {
+    const int r = e / (ROWS / 2), cp = (e % (ROWS / 2)) * 2;
+    const uint64_t* rs = cluster.map_shared_rank(T, r / ROWS);
+    const ulonglong2 v =
+        *reinterpret_cast<const ulonglong2*>(rs + (size_t)(r % ROWS) * S + cbase + cp);
+    const int t = cp >> 3, c = cp & 7;
+    tile[tix(t, r, c)] = v.x;
+    tile[tix(t, r, c + 1)] = v.y;
+  }
+  __syncthreads();
+  const ulonglong2 fs = P.post ? P.fin_s[limb] : make_ulonglong2(pc.ninv, pc.ninv_sh);
+  const ulonglong2 fd = P.post ? P.fin_d[limb] : make_ulonglong2(pc.ilast, pc.ilast_sh);
+#pragma unroll 1
+  for (int t = 0; t < L::TILES; ++t) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = tile[tix(t, reg_j(lane, e, LO_S, EB), warp)];
+    if (fpp) {
+      double xf[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) xf[e] = __longlong_as_double(x[e]);
+      const double2 fsf = make_double2((double)fs.x, (double)fs.x / qd);
+      const double2 fdf = make_double2((double)fd.x, (double)fd.x / qd);
+      inv_sub_fp<LOGS>(xf, reinterpret_cast<double*>(wbuf), lane, LO_S, LO_S, LOGS - 1,
+                       reinterpret_cast<const double2*>(stw), qd, qinv, fsf, fdf);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = fp_to_residue_small(xf[e], qd);
+    } else {
+      inv_sub<LOGS>(x, wbuf, lane, LO_S, LO_S, LOGS - 1, stw, pc, fs, fd);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) tile[tix(t, reg_j(lane, e, LO_S, EB), warp)] = x[e];
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int e = threadIdx.x; e < PAIRS; e += blockDim.x) {
+    const int r = e / (ROWS / 2), cp = (e % (ROWS / 2)) * 2;
+    const int t = cp >> 3, c = cp & 7;
+    *reinterpret_cast<ulonglong2*>(dst + (size_t)S * r + cbase + cp) =
+        make_ulonglong2(tile[tix(t, r, c)], tile[tix(t, r, c + 1)]);
+  }
+  cluster.sync();  // no CTA leaves while others still read its rows
+}
+
 template <int LOGS, bool INV, int CM>
 static void launch_cols_r_cm(const NttParams& P, dim3 grid, cudaStream_t st) {
   const size_t smem = cols_r_smem<LOGS>();
@@ -784,6 +969,31 @@ static inline int ilog2(int x) {
   return r;
 }
 
+static bool intt_fused_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HEGPU_INTT_FUSED");
+    return e ? e[0] == '1' : (HEGPU_INTT_FUSED != 0);
+  }();
+  return on;
+}
+
+template <int LOGS>
+static void launch_intt_fused(const NttParams& P, int n_units, cudaStream_t st) {
+  const size_t smem = FusedLayout<LOGS>::bytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (kFuseCluster > 8)
+      check_cuda(cudaFuncSetAttribute(k_intt_fused<LOGS>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "cluster attr");
+    check_cuda(cudaFuncSetAttribute(k_intt_fused<LOGS>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    attr_set = true;
+  }
+  k_intt_fused<LOGS><<<dim3(kFuseCluster, n_units), 32 * kRegWarps, smem, st>>>(P);
+}
+
 void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inverse,
                 SegSet& S, const NttEpilogue* epi, cudaStream_t st, const uint64_t* fp_mask) {
   // one kernel per pass serves both arithmetic classes (a per-CTA uniform
@@ -842,6 +1052,22 @@ void launch_ntt(const PrimeConst* dpc, const uint64_t* dtw, int log_n, bool inve
   const double mm_b = rows * nn / 2 * (log_n - a) + ((P_epi_guard(epi)) ? rows * nn : 0.0);
   pa.tile_log = ilog2(cpb);
   pb.tile_log = ilog2(bpc);
+  if (inverse && log_n == 16 && intt_fused_enabled()) {
+    // one cluster per (poly, limb): units with one poly each
+    int n_units = 0;
+    for (int g = 0; g < S.n_seg; ++g) {
+      pa.unit_start[g] = n_units;
+      n_units += S.seg[g].k * S.seg[g].n_polys;
+    }
+    pa.unit_start[S.n_seg] = n_units;
+    pa.ppb = 1;
+    pa.unit0 = 0;
+    if (n_units > 65535) throw HegpuError{1, "NTT batch exceeds 65535 units"};
+    ProfScope ps(PROF_NTT, st, bytes_pass, rows * nn / 2 * log_n + rows * nn);
+    launch_intt_fused<8>(pa, n_units, st);
+    check_cuda(cudaGetLastError(), "fused intt launch");
+    return;
+  }
   if (log_n >= 12) {
     const int logs_b = log_n - a;
     // units: (segment, limb, chunk of ppb polys); a unit's polys share the

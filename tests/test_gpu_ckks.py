@@ -355,3 +355,23 @@ def test_tma_and_register_inner_products_agree(digests):
     for lvl in ("21", "10"):
         if lvl in digests["p16"]["ks"]:
             assert got[lvl] == digests["p16"]["ks"][lvl]
+
+
+@pytest.mark.gpu
+def test_fused_inverse_ntt_bit_identical():
+    """The cluster/DSMEM fused inverse NTT (HEGPU_INTT_FUSED=1, read once per
+    process) gives the same limbs as the default two-kernel inverse."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, HEGPU_INTT_FUSED=flag, PROBE_POLYS="3", PROBE_LIMBS="22")
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "intt_fused_probe.py")],
+                             env=env, capture_output=True, text=True, timeout=600, cwd=root)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[flag] = json.loads(res.stdout.strip().splitlines()[-1])["digest"]
+    assert out["0"] == out["1"]
