@@ -1301,8 +1301,11 @@ constexpr int kRunGiants = 32; // giants per CTA (grid.z covers more)
 #endif
 constexpr int kRunChunk = HEGPU_RUN_CHUNK;  // terms per shared-memory stage (double-buffered)
 
+// a run's row of giants is padded by one 16-byte slot so the (up to 4) runs a
+// warp reads in one step sit in different banks
+constexpr int run_row(int ng) { return ng + 2; }
 constexpr size_t bsgs_run_smem(int ng, int rt) {
-  return (size_t)2 * kRunChunk * (2 * kRunTile + ng * rt) * 8;  // two stage buffers
+  return (size_t)2 * kRunChunk * (2 * kRunTile + run_row(ng) * rt) * 8;  // two stage buffers
 }
 
 // RT = runs per tile (2 for pt_log_run 4, 1 for 5); one batch element per CTA.
@@ -1314,7 +1317,8 @@ __global__ void __launch_bounds__(32 * (NG / GPT), GPT == 8 ? 3 : 2)
   extern __shared__ __align__(16) uint64_t sm[];
   constexpr int COLS = 2 * kRunTile;  // (c0, c1) x 32 coefficients
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
-  constexpr int BUF = kRunChunk * (COLS + NG * RT);  // words per stage buffer
+  constexpr int RROW = run_row(NG);
+  constexpr int BUF = kRunChunk * (COLS + RROW * RT);  // words per stage buffer
   const int N = 1 << P.log_n;
   // grid (giant groups, tiles, limbs): the groups staging the same baby tile
   // run back to back, so all but the first read it from L2
@@ -1351,18 +1355,20 @@ __global__ void __launch_bounds__(32 * (NG / GPT), GPT == 8 ? 3 : 2)
       cp_async16(bab + (size_t)t * COLS + cc * kRunTile + xx,
                  P.baby[tc + t] + cc * P.c1_off + (size_t)limb * N + x0 + xx);
     }
+    // giant-major within a term: consecutive threads fill consecutive words
+    // of the [t][run][giant] layout (conflict-free shared-memory writes)
     for (int e = threadIdx.x; e < kRunGiants * nt; e += blockDim.x) {
-      const int g = e / nt, t = e - g * nt;
+      const int t = e / kRunGiants, g = e - t * kRunGiants;
       const int idx =
           g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + tc + t) : -1;
-      uint64_t* d = pts + (size_t)t * RT * kRunGiants + g;
+      uint64_t* d = pts + (size_t)t * RT * RROW + g;
       const uint64_t* srcp = P.pt_base + (size_t)(idx < 0 ? 0 : idx) * P.pt_stride + pcol;
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
         if (idx < 0)
-          d[r * kRunGiants] = 0;
+          d[r * RROW] = 0;
         else
-          cp_async8(d + r * kRunGiants, srcp + r);
+          cp_async8(d + r * RROW, srcp + r);
       }
     }
     cp_async_commit();
@@ -1380,14 +1386,14 @@ __global__ void __launch_bounds__(32 * (NG / GPT), GPT == 8 ? 3 : 2)
     __syncthreads();
     const uint64_t* bab = sm + (size_t)(ch & 1) * BUF;
     const uint64_t* pts = bab + (size_t)kRunChunk * COLS;
-    const uint64_t* pt_g = pts + run * kRunGiants + gg * kRunGpt;
+    const uint64_t* pt_g = pts + run * RROW + gg * kRunGpt;
     const uint64_t* bab_c = bab + c * kRunTile + xl;
     const int nt = T - ch * kRunChunk < kRunChunk ? T - ch * kRunChunk : kRunChunk;
 #pragma unroll 2
     for (int t = 0; t < nt; ++t) {
       const ulonglong2 bv = *reinterpret_cast<const ulonglong2*>(bab_c + (size_t)t * COLS);
       const ulonglong2* pp =
-          reinterpret_cast<const ulonglong2*>(pt_g + (size_t)t * RT * kRunGiants);
+          reinterpret_cast<const ulonglong2*>(pt_g + (size_t)t * RT * RROW);
 #pragma unroll
       for (int h = 0; h < kRunGpt / 2; ++h) {
         const ulonglong2 pv = pp[h];
@@ -1444,6 +1450,250 @@ static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
     launch_bsgs_run_g<RT, HEGPU_RUN_GPT, kRunGiants>(P, k, st);
 }
 
+// ---------------------------------------------------------------------------
+// Run-compressed BSGS MAC on the tensor cores (pt_log_run >= 3).  Within one
+// run of 2^LR coefficients the product is a small exact GEMM,
+//   out[g][col] = sum_t P[g][t] * B[t][col]   (mod q),
+// with 16 giants x 8 columns x 32 terms per IMMA m16n8k32 tile.  Both operands
+// (< 2^64) are split into byte planes a = sum_i a_i 2^(8i); the u8 x u8 -> s32
+// products of plane pair (i, j) accumulate into sum_{i+j=s} of shift s (at most
+// 8 pairs x 255^2 x 256 terms < 2^31), and the epilogue recombines the
+// 15 shifts into the exact 128-bit sum (< 256 q^2 < 2^128) before one Barrett /
+// Montgomery reduction: the limbs are identical to k_bsgs_run's.
+// CTA = 8 warps over 32 coefficients x 16 giants of one limb; warp w owns the
+// 8-column tile w (component w / 4, coefficients 8 (w % 4) ..); the byte
+// planes of a 32-term chunk are staged in shared memory (PRMT transposes).
+// ---------------------------------------------------------------------------
+#ifndef HEGPU_BSGS_MMA
+#define HEGPU_BSGS_MMA 1
+#endif
+constexpr int kMmaGiants = 16;
+constexpr int kMmaTile = 32;  // coefficients per CTA
+
+// 4 x u64 -> 8 byte planes: plane p = bytes p of (v0, v1, v2, v3), v0 lowest
+__device__ __forceinline__ void byte_planes4(const uint64_t (&v)[4], uint32_t (&pl)[8]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t w0 = static_cast<uint32_t>(v[0] >> (32 * h));
+    const uint32_t w1 = static_cast<uint32_t>(v[1] >> (32 * h));
+    const uint32_t w2 = static_cast<uint32_t>(v[2] >> (32 * h));
+    const uint32_t w3 = static_cast<uint32_t>(v[3] >> (32 * h));
+    const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+    const uint32_t u0 = __byte_perm(w2, w3, 0x5140), u1 = __byte_perm(w2, w3, 0x7362);
+    pl[4 * h + 0] = __byte_perm(t0, u0, 0x5410);
+    pl[4 * h + 1] = __byte_perm(t0, u0, 0x7632);
+    pl[4 * h + 2] = __byte_perm(t1, u1, 0x5410);
+    pl[4 * h + 3] = __byte_perm(t1, u1, 0x7632);
+  }
+}
+
+// word swizzle of an 8-word (32-term) row: conflict-free fragment loads
+// (8 consecutive rows x 4 words) and staging stores (32 consecutive rows)
+__device__ __forceinline__ int mma_sw(int row) {
+  return (((row >> 2) & 1) << 2) | ((row >> 3) & 3);
+}
+
+__device__ __forceinline__ void imma_u8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// shared-memory plan of k_bsgs_mma: raw u64 chunks (double-buffered, cp.async),
+// byte planes of the current chunk, and the CTA's diagonal-index table
+template <int RT>
+struct MmaSmem {
+  static constexpr int COLS = 2 * kMmaTile;
+  static constexpr int RAW_B = 32 * COLS;                 // u64 words [t][col]
+  static constexpr int RAW_A = 32 * kMmaGiants * RT;      // u64 words [t][giant][run]
+  static constexpr int PL_B = 8 * COLS * 8;               // u32 words [plane][col][8]
+  static constexpr int PL_A = 8 * RT * kMmaGiants * 8;    // u32 words [plane][run][giant][8]
+  static size_t bytes(int T) {
+    return (size_t)2 * (RAW_B + RAW_A) * 8 + (size_t)(PL_B + PL_A) * 4 +
+           (size_t)kMmaGiants * T * 4;
+  }
+};
+
+template <int RT>
+__global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ BsgsParams P) {
+  using L = MmaSmem<RT>;
+  constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
+  constexpr int COLS = L::COLS;
+  extern __shared__ __align__(16) uint64_t smem_mma[];
+  uint64_t* raw_b = smem_mma;                       // 2 buffers
+  uint64_t* raw_a = raw_b + 2 * L::RAW_B;           // 2 buffers
+  uint32_t* Bs = reinterpret_cast<uint32_t*>(raw_a + 2 * L::RAW_A);
+  uint32_t* As = Bs + L::PL_B;
+  int* s_idx = reinterpret_cast<int*>(As + L::PL_A);
+  const int N = 1 << P.log_n;
+  const int limb = blockIdx.z;
+  const int x0 = blockIdx.y * kMmaTile;
+  const int g0 = blockIdx.x * kMmaGiants;
+  const int T = P.n_terms;
+  const int nch = (T + 31) >> 5;
+  const PrimeConst pc = P.pc[limb < P.kq ? limb : P.n_chain + (limb - P.kq)];
+  const int nby = (64 - __clzll(pc.q) + 7) >> 3;  // byte planes in use
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int comp = warp >> 2, xo = (warp & 3) * 8;  // this warp's column tile
+  const int run = xo >> LR;
+  const size_t pcol = ((size_t)limb * N + x0) >> LR;
+  for (int e = threadIdx.x; e < kMmaGiants * T; e += 256) {
+    const int g = e / T, t = e - g * T;
+    s_idx[e] = g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + t) : -1;
+  }
+  __syncthreads();
+  // raw chunk ch -> buffer ch & 1 (terms past T and absent diagonals are
+  // zero-filled by plain stores)
+  auto stage = [&](int ch) {
+    uint64_t* rb = raw_b + (ch & 1) * L::RAW_B;
+    uint64_t* ra = raw_a + (ch & 1) * L::RAW_A;
+    const int tc = ch * 32;
+    for (int e = threadIdx.x; e < 32 * COLS / 2; e += 256) {
+      const int t = e / (COLS / 2), j = (e % (COLS / 2)) * 2;
+      const int c = j / kMmaTile, xl = j % kMmaTile;
+      uint64_t* d = rb + t * COLS + j;
+      if (tc + t < T)
+        cp_async16(d, P.baby[tc + t] + c * P.c1_off + (size_t)limb * N + x0 + xl);
+      else
+        *reinterpret_cast<ulonglong2*>(d) = make_ulonglong2(0, 0);
+    }
+    for (int e = threadIdx.x; e < 32 * kMmaGiants; e += 256) {
+      const int t = e / kMmaGiants, g = e % kMmaGiants;
+      const int idx = tc + t < T ? s_idx[g * T + tc + t] : -1;
+      uint64_t* d = ra + (t * kMmaGiants + g) * RT;
+      const uint64_t* src = P.pt_base + (size_t)(idx < 0 ? 0 : idx) * P.pt_stride + pcol;
+#pragma unroll
+      for (int r = 0; r < RT; r += (RT >= 2 ? 2 : 1)) {
+        if (RT >= 2) {
+          if (idx < 0)
+            *reinterpret_cast<ulonglong2*>(d + r) = make_ulonglong2(0, 0);
+          else
+            cp_async16(d + r, src + r);
+        } else {
+          if (idx < 0)
+            d[r] = 0;
+          else
+            cp_async8(d + r, src + r);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  int acc[15][4];
+#pragma unroll
+  for (int s = 0; s < 15; ++s)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[s][i] = 0;
+  const int fr = lane >> 2, fq = lane & 3;  // fragment row / word
+  stage(0);
+#pragma unroll 1
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait_group<0>();
+    __syncthreads();  // raw chunk ch landed; planes of ch - 1 consumed
+    if (ch + 1 < nch) stage(ch + 1);
+    const uint64_t* rb = raw_b + (ch & 1) * L::RAW_B;
+    const uint64_t* ra = raw_a + (ch & 1) * L::RAW_A;
+    // ---- byte planes: babies (64 cols x 8 term quads) ------------------------
+    for (int e = threadIdx.x; e < COLS * 8; e += 256) {
+      const int j = e % COLS, q = e / COLS;
+      uint64_t v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = rb[(4 * q + i) * COLS + j];
+      uint32_t pl[8];
+      byte_planes4(v, pl);
+      const int w = j * 8 + (q ^ mma_sw(j));
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < nby) Bs[p * COLS * 8 + w] = pl[p];
+    }
+    // ---- diagonals: 16 giants x 8 quads x RT runs -----------------------------
+    for (int e = threadIdx.x; e < kMmaGiants * 8 * RT; e += 256) {
+      const int g = e % kMmaGiants, q = (e / kMmaGiants) % 8, r = e / (kMmaGiants * 8);
+      uint64_t v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = ra[((4 * q + i) * kMmaGiants + g) * RT + r];
+      uint32_t pl[8];
+      byte_planes4(v, pl);
+      const int w = (r * kMmaGiants + g) * 8 + (q ^ mma_sw(g));
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < nby) As[p * RT * kMmaGiants * 8 + w] = pl[p];
+    }
+    __syncthreads();
+    // ---- MMAs: plane pairs (i, j) into shift i + j ----------------------------
+    const int jb = comp * kMmaTile + xo + fr;  // this lane's B column
+    uint32_t bf[8][2];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const uint32_t* bp = Bs + p * COLS * 8 + jb * 8;
+      bf[p][0] = bp[fq ^ mma_sw(jb)];
+      bf[p][1] = bp[(fq + 4) ^ mma_sw(jb)];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i >= nby) break;
+      const uint32_t* ap = As + i * RT * kMmaGiants * 8 + run * kMmaGiants * 8;
+      uint32_t af[4];
+      af[0] = ap[fr * 8 + (fq ^ mma_sw(fr))];
+      af[1] = ap[(fr + 8) * 8 + (fq ^ mma_sw(fr + 8))];
+      af[2] = ap[fr * 8 + ((fq + 4) ^ mma_sw(fr))];
+      af[3] = ap[(fr + 8) * 8 + ((fq + 4) ^ mma_sw(fr + 8))];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < nby) imma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
+      }
+    }
+  }
+  // ---- epilogue: C rows fr / fr + 8 (giants), columns 2 fq, 2 fq + 1 ----------
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int gi = g0 + fr + 8 * h;
+    if (gi >= P.n_giants) continue;
+    uint64_t r[2];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      unsigned __int128 v = 0;
+#pragma unroll
+      for (int s = 0; s < 15; ++s)
+        v += static_cast<unsigned __int128>(static_cast<uint32_t>(acc[s][2 * h + cc])) << (8 * s);
+      Mac128 m;
+      m.L = static_cast<uint64_t>(v);
+      m.H = static_cast<uint64_t>(v >> 64);
+      m.M = 0;
+      m.c = 0;
+      r[cc] = mont_mul(m.redc(pc), pc.r2, pc.q, pc.qinv_neg);
+    }
+    *reinterpret_cast<ulonglong2*>(P.out + (size_t)gi * P.out_gstride + comp * P.c1_off +
+                                   (size_t)limb * N + x0 + xo + 2 * fq) =
+        make_ulonglong2(r[0], r[1]);
+  }
+}
+
+static bool bsgs_mma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HEGPU_BSGS_MMA");
+    return e ? e[0] == '1' : (HEGPU_BSGS_MMA != 0);
+  }();
+  return on;
+}
+
+template <int RT>
+static void launch_bsgs_mma(const BsgsParams& P, int k, cudaStream_t st) {
+  const size_t smem = MmaSmem<RT>::bytes(P.n_terms);
+  static bool attr_set = false;
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(k_bsgs_mma<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)MmaSmem<RT>::bytes(kBsgsMaxTerms)),
+               "bsgs mma smem attr");
+    attr_set = true;
+  }
+  dim3 grid((P.n_giants + kMmaGiants - 1) / kMmaGiants, (1 << P.log_n) / kMmaTile, k);
+  k_bsgs_mma<RT><<<grid, 256, smem, st>>>(P);
+}
+
 template <int NB>
 static void launch_bsgs_nb(const BsgsParams& P, int k, cudaStream_t st) {
   constexpr int W = 16;  // <= 128 registers per thread (7-word accumulators)
@@ -1494,7 +1744,14 @@ void launch_bsgs(const PrimeConst* dpc, int log_n, const uint64_t* const* babies
           for (int t = 0; t < n_terms; ++t) Q.baby[t] = P.baby[t] + bi * bstride;
           Q.out = P.out + bi * bstride;
           Q.n_batch = 1;
-          if (pt_log_run == 3)
+          if (bsgs_mma_enabled()) {
+            if (pt_log_run == 3)
+              launch_bsgs_mma<4>(Q, k, st);
+            else if (pt_log_run == 4)
+              launch_bsgs_mma<2>(Q, k, st);
+            else
+              launch_bsgs_mma<1>(Q, k, st);
+          } else if (pt_log_run == 3)
             launch_bsgs_run<4>(Q, k, st);
           else if (pt_log_run == 4)
             launch_bsgs_run<2>(Q, k, st);

@@ -143,11 +143,14 @@ def test_batched_ops_equal_single():
         assert np.array_equal(coeff.limbs[i], ring.to_coeff(x).limbs)
 
 
-@pytest.mark.parametrize("lr,ns,T", [(2, 0, 21), (3, 0, 100), (4, 0, 21), (5, 0, 21), (4, 2, 21)])
-def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T):
+@pytest.mark.parametrize("lr,ns,T,G", [(2, 0, 21, 5), (3, 0, 100, 5), (4, 0, 21, 5), (5, 0, 21, 5),
+                                        (4, 2, 21, 5), (3, 2, 256, 37), (5, 1, 33, 17)])
+def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T, G):
     """hegpu_bsgs on run-compressed diagonals (pt_log_run, the sparse-bootstrap
-    cache layout; lr >= 4 takes the shared-memory GEMM kernel) equals the dense
-    kernel on the expanded diagonals and the exact sum mod q."""
+    cache layout; lr >= 3 takes the tensor-core byte-plane GEMM) equals the dense
+    kernel on the expanded diagonals and the exact sum mod q -- including 256
+    terms on 60-bit special primes (the largest exact sum, < 2^128) and giant
+    counts that are not multiples of the 16-giant tile."""
     import ctypes
 
     import torch
@@ -155,7 +158,7 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T):
     from paper_2210_02574_b200 import _dev, _lib, ckks
 
     params = ckks.get_preset("desk")
-    n, k, G, nb = params.ring_degree, 3 + ns, 5, 2
+    n, k, nb = params.ring_degree, 3 + ns, 2
     # ns > 0: the last ns limbs are special primes (extended-basis babies)
     qs = ([int(q) for q in params.ring.moduli_chain[:k - ns]]
           + [int(q) for q in params.ring.special_moduli[:ns]])
@@ -180,7 +183,8 @@ def test_bsgs_run_compressed_matches_dense_and_exact(lr, ns, T):
         outs.append(out.cpu().numpy().view(np.uint64))
     assert np.array_equal(outs[0], outs[1])
     bab = babies.cpu().numpy().view(np.uint64)
-    for (g, b, c, l, x) in [(0, 0, 0, 0, 0), (4, 1, 1, 2, n - 1), (2, 1, 0, 1, 37)]:
+    for (g, b, c, l, x) in [(0, 0, 0, 0, 0), (4, 1, 1, 2, n - 1), (2, 1, 0, 1, 37),
+                            (G - 1, 1, 1, k - 1, n - 2)]:
         want = sum(int(pts_c[idx[g, t], l, x >> lr]) * int(bab[t, b, c, l, x])
                    for t in range(T) if idx[g, t] >= 0) % qs[l]
         assert int(outs[0][g, b, c, l, x]) == want
