@@ -1655,13 +1655,22 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
     uint64_t r[2];
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
-      unsigned __int128 v = 0;
+      // four 32-bit-aligned groups of 4 shifts, each < 2^52, then one 128-bit sum
+      uint64_t S[4];
 #pragma unroll
-      for (int s = 0; s < 15; ++s)
-        v += static_cast<unsigned __int128>(static_cast<uint32_t>(acc[s][2 * h + cc])) << (8 * s);
+      for (int grp = 0; grp < 4; ++grp) {
+        uint64_t x = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * grp + u < 15)
+            x += static_cast<uint64_t>(static_cast<uint32_t>(acc[4 * grp + u][2 * h + cc])) << (8 * u);
+        S[grp] = x;
+      }
+      const uint64_t lo = S[0] + (S[1] << 32);
+      const uint64_t hi = (S[1] >> 32) + S[2] + (S[3] << 32) + (lo < S[0]);
       Mac128 m;
-      m.L = static_cast<uint64_t>(v);
-      m.H = static_cast<uint64_t>(v >> 64);
+      m.L = lo;
+      m.H = hi;
       m.M = 0;
       m.c = 0;
       r[cc] = mont_mul(m.redc(pc), pc.r2, pc.q, pc.qinv_neg);
