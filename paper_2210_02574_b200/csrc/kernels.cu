@@ -1467,6 +1467,10 @@ static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
 #ifndef HEGPU_BSGS_MMA
 #define HEGPU_BSGS_MMA 1
 #endif
+#ifndef HEGPU_MMA_1BUF
+#define HEGPU_MMA_1BUF 0  // 1: single raw buffer, 3 CTAs/SM: measured 17% slower (spills)
+#endif
+constexpr int kMmaNbuf = HEGPU_MMA_1BUF ? 1 : 2;
 constexpr int kMmaGiants = 16;
 constexpr int kMmaTile = 32;  // coefficients per CTA
 
@@ -1512,20 +1516,20 @@ struct MmaSmem {
   static constexpr int PL_B = 8 * COLS * 8;               // u32 words [plane][col][8]
   static constexpr int PL_A = 8 * RT * kMmaGiants * 8;    // u32 words [plane][run][giant][8]
   static size_t bytes(int T) {
-    return (size_t)2 * (RAW_B + RAW_A) * 8 + (size_t)(PL_B + PL_A) * 4 +
+    return (size_t)kMmaNbuf * (RAW_B + RAW_A) * 8 + (size_t)(PL_B + PL_A) * 4 +
            (size_t)kMmaGiants * T * 4;
   }
 };
 
 template <int RT>
-__global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ BsgsParams P) {
+__global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const __grid_constant__ BsgsParams P) {
   using L = MmaSmem<RT>;
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
   constexpr int COLS = L::COLS;
   extern __shared__ __align__(16) uint64_t smem_mma[];
   uint64_t* raw_b = smem_mma;                       // 2 buffers
-  uint64_t* raw_a = raw_b + 2 * L::RAW_B;           // 2 buffers
-  uint32_t* Bs = reinterpret_cast<uint32_t*>(raw_a + 2 * L::RAW_A);
+  uint64_t* raw_a = raw_b + kMmaNbuf * L::RAW_B;
+  uint32_t* Bs = reinterpret_cast<uint32_t*>(raw_a + kMmaNbuf * L::RAW_A);
   uint32_t* As = Bs + L::PL_B;
   int* s_idx = reinterpret_cast<int*>(As + L::PL_A);
   const int N = 1 << P.log_n;
@@ -1548,8 +1552,8 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
   // raw chunk ch -> buffer ch & 1 (terms past T and absent diagonals are
   // zero-filled by plain stores)
   auto stage = [&](int ch) {
-    uint64_t* rb = raw_b + (ch & 1) * L::RAW_B;
-    uint64_t* ra = raw_a + (ch & 1) * L::RAW_A;
+    uint64_t* rb = raw_b + (ch % kMmaNbuf) * L::RAW_B;
+    uint64_t* ra = raw_a + (ch % kMmaNbuf) * L::RAW_A;
     const int tc = ch * 32;
     for (int e = threadIdx.x; e < 32 * COLS / 2; e += 256) {
       const int t = e / (COLS / 2), j = (e % (COLS / 2)) * 2;
@@ -1593,9 +1597,9 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
   for (int ch = 0; ch < nch; ++ch) {
     cp_async_wait_group<0>();
     __syncthreads();  // raw chunk ch landed; planes of ch - 1 consumed
-    if (ch + 1 < nch) stage(ch + 1);
-    const uint64_t* rb = raw_b + (ch & 1) * L::RAW_B;
-    const uint64_t* ra = raw_a + (ch & 1) * L::RAW_A;
+    if (kMmaNbuf == 2 && ch + 1 < nch) stage(ch + 1);
+    const uint64_t* rb = raw_b + (ch % kMmaNbuf) * L::RAW_B;
+    const uint64_t* ra = raw_a + (ch % kMmaNbuf) * L::RAW_A;
     // ---- byte planes: babies (64 cols x 8 term quads) ------------------------
     for (int e = threadIdx.x; e < COLS * 8; e += 256) {
       const int j = e % COLS, q = e / COLS;
@@ -1623,14 +1627,18 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
         if (p < nby) As[p * RT * kMmaGiants * 8 + w] = pl[p];
     }
     __syncthreads();
+    if (kMmaNbuf == 1 && ch + 1 < nch) stage(ch + 1);  // the raw buffer is converted
     // ---- MMAs: plane pairs (i, j) into shift i + j ----------------------------
     const int jb = comp * kMmaTile + xo + fr;  // this lane's B column
+    const uint32_t* bcol = Bs + jb * 8;
+    const int bw0 = fq ^ mma_sw(jb), bw1 = (fq + 4) ^ mma_sw(jb);
     uint32_t bf[8][2];
+    if constexpr (kMmaNbuf == 2) {  // all B fragments in registers (3 CTAs/SM: reloaded)
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const uint32_t* bp = Bs + p * COLS * 8 + jb * 8;
-      bf[p][0] = bp[fq ^ mma_sw(jb)];
-      bf[p][1] = bp[(fq + 4) ^ mma_sw(jb)];
+      for (int p = 0; p < 8; ++p) {
+        bf[p][0] = bcol[p * COLS * 8 + bw0];
+        bf[p][1] = bcol[p * COLS * 8 + bw1];
+      }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -1643,7 +1651,12 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
       af[3] = ap[(fr + 8) * 8 + ((fq + 4) ^ mma_sw(fr + 8))];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (j < nby) imma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
+        if (j < nby) {
+          if constexpr (kMmaNbuf == 2)
+            imma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
+          else
+            imma_u8(acc[i + j], af, bcol[j * COLS * 8 + bw0], bcol[j * COLS * 8 + bw1]);
+        }
       }
     }
   }
@@ -1655,22 +1668,13 @@ __global__ void __launch_bounds__(256, 2) k_bsgs_mma(const __grid_constant__ Bsg
     uint64_t r[2];
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
-      // four 32-bit-aligned groups of 4 shifts, each < 2^52, then one 128-bit sum
-      uint64_t S[4];
+      unsigned __int128 v = 0;
 #pragma unroll
-      for (int grp = 0; grp < 4; ++grp) {
-        uint64_t x = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (4 * grp + u < 15)
-            x += static_cast<uint64_t>(static_cast<uint32_t>(acc[4 * grp + u][2 * h + cc])) << (8 * u);
-        S[grp] = x;
-      }
-      const uint64_t lo = S[0] + (S[1] << 32);
-      const uint64_t hi = (S[1] >> 32) + S[2] + (S[3] << 32) + (lo < S[0]);
+      for (int s = 0; s < 15; ++s)
+        v += static_cast<unsigned __int128>(static_cast<uint32_t>(acc[s][2 * h + cc])) << (8 * s);
       Mac128 m;
-      m.L = lo;
-      m.H = hi;
+      m.L = static_cast<uint64_t>(v);
+      m.H = static_cast<uint64_t>(v >> 64);
       m.M = 0;
       m.c = 0;
       r[cc] = mont_mul(m.redc(pc), pc.r2, pc.q, pc.qinv_neg);

@@ -13,7 +13,7 @@ BENCH_NVTX=1 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx \
     python bench.py --steps 1 --warmup 3 > gpurun_out/prof_launches.log 2>&1
 BENCH_NVTX=1 ncu --set full --clock-control none --import-source on --nvtx \
     --nvtx-include "profile_step/" --kernel-name-base demangled \
-    -k regex:"k_ntt_cols_r<\(int\)8, \(bool\)0, \(int\)2|k_ntt_blocks_r<\(int\)8, \(bool\)0|k_bsgs_run|k_ks_ip_rot<\(int\)1|k_ks_ip_rot_tma" -c 10 \
+    -k regex:"k_ntt_cols_r<\(int\)8, \(bool\)0, \(int\)2|k_ntt_blocks_r<\(int\)8, \(bool\)0|k_bsgs_mma|k_ks_ip_rot<\(int\)1|k_ks_ip_rot_tma" -c 10 \
     -o gpurun_out/prof_train python bench.py --steps 1 --warmup 3 > gpurun_out/prof_full.log 2>&1
 BENCH_NVTX=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx \
     --nvtx-include "profile_step/" --csv --log-file gpurun_out/dram_train.csv \
