@@ -1508,22 +1508,27 @@ __device__ __forceinline__ void imma_u8(int (&d)[4], const uint32_t (&a)[4], uin
 
 // shared-memory plan of k_bsgs_mma: raw u64 chunks (double-buffered, cp.async),
 // byte planes of the current chunk, and the CTA's diagonal-index table
-template <int RT>
+template <int RT, int MG>
 struct MmaSmem {
+  static constexpr int NGC = kMmaGiants * MG;             // giants per CTA
   static constexpr int COLS = 2 * kMmaTile;
   static constexpr int RAW_B = 32 * COLS;                 // u64 words [t][col]
-  static constexpr int RAW_A = 32 * kMmaGiants * RT;      // u64 words [t][giant][run]
+  static constexpr int RAW_A = 32 * NGC * RT;      // u64 words [t][giant][run]
   static constexpr int PL_B = 8 * COLS * 8;               // u32 words [plane][col][8]
-  static constexpr int PL_A = 8 * RT * kMmaGiants * 8;    // u32 words [plane][run][giant][8]
+  static constexpr int PL_A = 8 * RT * NGC * 8;    // u32 words [plane][run][giant][8]
   static size_t bytes(int T) {
     return (size_t)kMmaNbuf * (RAW_B + RAW_A) * 8 + (size_t)(PL_B + PL_A) * 4 +
-           (size_t)kMmaGiants * T * 4;
+           (size_t)NGC * T * 4;
   }
 };
 
-template <int RT>
-__global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const __grid_constant__ BsgsParams P) {
-  using L = MmaSmem<RT>;
+// MG = 16-giant m-tiles per CTA (8 warps each): MG = 2 stages and converts the
+// babies' planes once for 32 giants
+template <int RT, int MG>
+__global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 2))
+    k_bsgs_mma(const __grid_constant__ BsgsParams P) {
+  using L = MmaSmem<RT, MG>;
+  constexpr int NGC = L::NGC, NT = 256 * MG;
   constexpr int LR = RT == 4 ? 3 : RT == 2 ? 4 : 5;
   constexpr int COLS = L::COLS;
   extern __shared__ __align__(16) uint64_t smem_mma[];
@@ -1535,16 +1540,17 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
   const int N = 1 << P.log_n;
   const int limb = blockIdx.z;
   const int x0 = blockIdx.y * kMmaTile;
-  const int g0 = blockIdx.x * kMmaGiants;
+  const int g0 = blockIdx.x * NGC;
   const int T = P.n_terms;
   const int nch = (T + 31) >> 5;
   const PrimeConst pc = P.pc[limb < P.kq ? limb : P.n_chain + (limb - P.kq)];
   const int nby = (64 - __clzll(pc.q) + 7) >> 3;  // byte planes in use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int comp = warp >> 2, xo = (warp & 3) * 8;  // this warp's column tile
+  const int mt = warp >> 3;                          // this warp's 16-giant m-tile
+  const int comp = (warp & 7) >> 2, xo = (warp & 3) * 8;  // and 8-column tile
   const int run = xo >> LR;
   const size_t pcol = ((size_t)limb * N + x0) >> LR;
-  for (int e = threadIdx.x; e < kMmaGiants * T; e += 256) {
+  for (int e = threadIdx.x; e < NGC * T; e += NT) {
     const int g = e / T, t = e - g * T;
     s_idx[e] = g0 + g < P.n_giants ? __ldg(P.pt_idx + (size_t)(g0 + g) * T + t) : -1;
   }
@@ -1555,7 +1561,7 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
     uint64_t* rb = raw_b + (ch % kMmaNbuf) * L::RAW_B;
     uint64_t* ra = raw_a + (ch % kMmaNbuf) * L::RAW_A;
     const int tc = ch * 32;
-    for (int e = threadIdx.x; e < 32 * COLS / 2; e += 256) {
+    for (int e = threadIdx.x; e < 32 * COLS / 2; e += NT) {
       const int t = e / (COLS / 2), j = (e % (COLS / 2)) * 2;
       const int c = j / kMmaTile, xl = j % kMmaTile;
       uint64_t* d = rb + t * COLS + j;
@@ -1564,10 +1570,10 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
       else
         *reinterpret_cast<ulonglong2*>(d) = make_ulonglong2(0, 0);
     }
-    for (int e = threadIdx.x; e < 32 * kMmaGiants; e += 256) {
-      const int t = e / kMmaGiants, g = e % kMmaGiants;
+    for (int e = threadIdx.x; e < 32 * NGC; e += NT) {
+      const int t = e / NGC, g = e % NGC;
       const int idx = tc + t < T ? s_idx[g * T + tc + t] : -1;
-      uint64_t* d = ra + (t * kMmaGiants + g) * RT;
+      uint64_t* d = ra + (t * NGC + g) * RT;
       const uint64_t* src = P.pt_base + (size_t)(idx < 0 ? 0 : idx) * P.pt_stride + pcol;
 #pragma unroll
       for (int r = 0; r < RT; r += (RT >= 2 ? 2 : 1)) {
@@ -1601,7 +1607,7 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
     const uint64_t* rb = raw_b + (ch % kMmaNbuf) * L::RAW_B;
     const uint64_t* ra = raw_a + (ch % kMmaNbuf) * L::RAW_A;
     // ---- byte planes: babies (64 cols x 8 term quads) ------------------------
-    for (int e = threadIdx.x; e < COLS * 8; e += 256) {
+    for (int e = threadIdx.x; e < COLS * 8; e += NT) {
       const int j = e % COLS, q = e / COLS;
       uint64_t v[4];
 #pragma unroll
@@ -1614,17 +1620,17 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
         if (p < nby) Bs[p * COLS * 8 + w] = pl[p];
     }
     // ---- diagonals: 16 giants x 8 quads x RT runs -----------------------------
-    for (int e = threadIdx.x; e < kMmaGiants * 8 * RT; e += 256) {
-      const int g = e % kMmaGiants, q = (e / kMmaGiants) % 8, r = e / (kMmaGiants * 8);
+    for (int e = threadIdx.x; e < NGC * 8 * RT; e += NT) {
+      const int g = e % NGC, q = (e / NGC) % 8, r = e / (NGC * 8);
       uint64_t v[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = ra[((4 * q + i) * kMmaGiants + g) * RT + r];
+      for (int i = 0; i < 4; ++i) v[i] = ra[((4 * q + i) * NGC + g) * RT + r];
       uint32_t pl[8];
       byte_planes4(v, pl);
-      const int w = (r * kMmaGiants + g) * 8 + (q ^ mma_sw(g));
+      const int w = (r * NGC + g) * 8 + (q ^ mma_sw(g));
 #pragma unroll
       for (int p = 0; p < 8; ++p)
-        if (p < nby) As[p * RT * kMmaGiants * 8 + w] = pl[p];
+        if (p < nby) As[p * RT * NGC * 8 + w] = pl[p];
     }
     __syncthreads();
     if (kMmaNbuf == 1 && ch + 1 < nch) stage(ch + 1);  // the raw buffer is converted
@@ -1643,12 +1649,13 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i >= nby) break;
-      const uint32_t* ap = As + i * RT * kMmaGiants * 8 + run * kMmaGiants * 8;
+      const uint32_t* ap = As + i * RT * NGC * 8 + run * NGC * 8;
+      const int ga = mt * 16 + fr, gb = ga + 8;
       uint32_t af[4];
-      af[0] = ap[fr * 8 + (fq ^ mma_sw(fr))];
-      af[1] = ap[(fr + 8) * 8 + (fq ^ mma_sw(fr + 8))];
-      af[2] = ap[fr * 8 + ((fq + 4) ^ mma_sw(fr))];
-      af[3] = ap[(fr + 8) * 8 + ((fq + 4) ^ mma_sw(fr + 8))];
+      af[0] = ap[ga * 8 + (fq ^ mma_sw(ga))];
+      af[1] = ap[gb * 8 + (fq ^ mma_sw(gb))];
+      af[2] = ap[ga * 8 + ((fq + 4) ^ mma_sw(ga))];
+      af[3] = ap[gb * 8 + ((fq + 4) ^ mma_sw(gb))];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (j < nby) {
@@ -1663,7 +1670,7 @@ __global__ void __launch_bounds__(256, HEGPU_MMA_1BUF ? 3 : 2) k_bsgs_mma(const 
   // ---- epilogue: C rows fr / fr + 8 (giants), columns 2 fq, 2 fq + 1 ----------
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int gi = g0 + fr + 8 * h;
+    const int gi = g0 + mt * 16 + fr + 8 * h;
     if (gi >= P.n_giants) continue;
     uint64_t r[2];
 #pragma unroll
@@ -1693,18 +1700,29 @@ static bool bsgs_mma_enabled() {
   return on;
 }
 
-template <int RT>
-static void launch_bsgs_mma(const BsgsParams& P, int k, cudaStream_t st) {
-  const size_t smem = MmaSmem<RT>::bytes(P.n_terms);
+#ifndef HEGPU_MMA_MG2
+#define HEGPU_MMA_MG2 0  // 32-giant CTAs (512 threads, 1 CTA/SM): measured 37% slower
+#endif
+template <int RT, int MG>
+static void launch_bsgs_mma_g(const BsgsParams& P, int k, cudaStream_t st) {
+  using L = MmaSmem<RT, MG>;
+  const size_t smem = L::bytes(P.n_terms);
   static bool attr_set = false;
   if (!attr_set) {
-    check_cuda(cudaFuncSetAttribute(k_bsgs_mma<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)MmaSmem<RT>::bytes(kBsgsMaxTerms)),
+    check_cuda(cudaFuncSetAttribute(k_bsgs_mma<RT, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)L::bytes(kBsgsMaxTerms)),
                "bsgs mma smem attr");
     attr_set = true;
   }
-  dim3 grid((P.n_giants + kMmaGiants - 1) / kMmaGiants, (1 << P.log_n) / kMmaTile, k);
-  k_bsgs_mma<RT><<<grid, 256, smem, st>>>(P);
+  dim3 grid((P.n_giants + L::NGC - 1) / L::NGC, (1 << P.log_n) / kMmaTile, k);
+  k_bsgs_mma<RT, MG><<<grid, 256 * MG, smem, st>>>(P);
+}
+template <int RT>
+static void launch_bsgs_mma(const BsgsParams& P, int k, cudaStream_t st) {
+  if (HEGPU_MMA_MG2 && P.n_giants > kMmaGiants)
+    launch_bsgs_mma_g<RT, 2>(P, k, st);
+  else
+    launch_bsgs_mma_g<RT, 1>(P, k, st);
 }
 
 template <int NB>
