@@ -390,6 +390,27 @@ def logreg_fixture():
                         shadow_weights=shadow.weights)
 
 
+def wire_fixture():
+    """CKT1 / CKK1 / HLR1 bytes of the reference (serial.py:61-209, logreg.py:583-633)
+    for seeded desk material: SHA-256 of each blob and its length."""
+    import hashlib as _h
+
+    from hebert.ckks import serial as S
+
+    params = ckks.get_preset("desk")
+    keys = ckks.keygen(params, rotation_steps=[1, -1, 2, 4], rng_seed=7, include_conjugation=True)
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, params.slot_count)
+    cts = [ckks.encrypt_vector(params, u * (i + 1) / 4, keys, rng_seed=20 + i) for i in range(4)]
+    layout = logreg.make_layout(params, 100)
+    model = logreg.EncryptedModel(3, layout, cts[:3], [cts[3]] * 3, "secure")
+    blobs = {"ckt1": S.serialize_ciphertext(cts[0]),
+             "ckk1_eval": S.serialize_keyset(keys, include_secret=False),
+             "ckk1_secret": S.serialize_keyset(keys, include_secret=True),
+             "hlr1": logreg.serialize_model(model)}
+    return {k: {"sha256": _h.sha256(b).hexdigest(), "bytes": len(b)} for k, b in blobs.items()}
+
+
 def main():
     t0 = time.time()
     only = {"boot_full": ("boot_desk_full", boot_full_fixture),
@@ -398,6 +419,7 @@ def main():
             "boot_p16_sparse": ("boot_p16_sparse", boot_p16_sparse_fixture),
             "logreg_p16": ("logreg_p16", logreg_p16_fixture),
             "sine_artifact": ("sine_artifact", sine_artifact),
+            "wire": ("wire_desk", wire_fixture),
             "p16s": ("p16s", lambda: scheme_digests(load_preset("p16s"), "p16s", [1], conj=False,
                                                     full=False)[0])}
     if sys.argv[1:] and sys.argv[1] in only:  # add / refresh only these entries

@@ -375,3 +375,37 @@ def test_fused_inverse_ntt_bit_identical():
         assert res.returncode == 0, res.stderr[-2000:]
         out[flag] = json.loads(res.stdout.strip().splitlines()[-1])["digest"]
     assert out["0"] == out["1"]
+
+
+def test_wire_formats_match_reference_bytes(desk_keys, digests):
+    """CKT1, CKK1 (evaluation and secret roles) and HLR1 blobs written from
+    the device tensors are byte-identical to the reference's for the same
+    seeds (tests/golden/make_golden.py wire_fixture), and parse straight back
+    into device tensors that re-serialize to the same bytes and decrypt."""
+    import hashlib
+
+    from paper_2210_02574_b200 import logreg
+
+    params, keys = desk_keys  # keygen(desk, [1, -1, 2, 4], seed 7, conjugation)
+    want = digests["wire_desk"]
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, params.slot_count)
+    cts = [ckks.encrypt_vector(params, u * (i + 1) / 4, keys, rng_seed=20 + i) for i in range(4)]
+    layout = logreg.make_layout(params, 100)
+    model = logreg.EncryptedModel(3, layout, cts[:3], [cts[3]] * 3, "secure")
+    blobs = {"ckt1": ckks.serialize_ciphertext(cts[0]),
+             "ckk1_eval": ckks.serialize_keyset(keys, include_secret=False),
+             "ckk1_secret": ckks.serialize_keyset(keys, include_secret=True),
+             "hlr1": logreg.serialize_model(model)}
+    for name, blob in blobs.items():
+        assert len(blob) == want[name]["bytes"], name
+        assert hashlib.sha256(blob).hexdigest() == want[name]["sha256"], name
+    k2 = ckks.deserialize_keyset(blobs["ckk1_secret"], params)
+    assert k2.relin_key.b.is_cuda and k2.public_key[0].data.is_cuda
+    assert ckks.serialize_keyset(k2, include_secret=True) == blobs["ckk1_secret"]
+    assert ckks.serialize_keyset(ckks.deserialize_keyset(blobs["ckk1_eval"], params)) == \
+        blobs["ckk1_eval"]
+    m2 = logreg.deserialize_model(blobs["hlr1"], params)
+    assert logreg.serialize_model(m2) == blobs["hlr1"]
+    got = ckks.decrypt_vector(m2.weights[1], k2)[:64]
+    assert np.max(np.abs(got - u[:64] * 2 / 4)) < 1e-3
