@@ -155,6 +155,14 @@ int hegpu_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, u
                         const uint64_t* bounds, int k, int n, uint64_t* out,
                         int64_t out_stride, long long* consumed, void* stream);
 
+/* Encryption randomness of an UNSEEDED encryption (replaces the host draws of
+ * ops.py:87-100 when the reference would seed numpy from OS entropy): out
+ * rows 0, 1, 2 (each n int64) = v ternary on {-1,0,1}, e0, e1 = rint of
+ * N(0, sigma^2), expanded on the device from the 64-bit `seed` (the caller's
+ * OS entropy) by Philox4x32-10.  Seeded encryptions keep the host numpy
+ * stream for bit-exact parity. */
+int hegpu_sample_encrypt(int64_t* out, int n, uint64_t seed, double sigma, void* stream);
+
 /* Forward NTT of signed int64 coefficient rows into k eval-form limbs: the
  * lift of poly_from_signed (ring.py:381-393) fused into the NTT's first pass.
  * src poly p at src + p*src_stride, out poly p at out + p*out_stride. */

@@ -46,6 +46,7 @@ SIGNATURES = {
     "hegpu_encode_overflow": [_P, _P],
     "hegpu_ntt_from_signed": [_P, _P, _I64, _P, _I64, _I, _I, _P, _P],
     "hegpu_pcg64_uniform": [_U64, _U64, _U64, _U64, _P, _I, _I, _P, _I64, _P, _P],
+    "hegpu_sample_encrypt": [_P, _I, _U64, ctypes.c_double, _P],
     "hegpu_tensor": [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],
     "hegpu_ks_apply": [_P, _I, _I, _P, _I64, _I, _P, _P, _I, _P, _P, _I64, _I, _P],
     "hegpu_tensor_periodic": [_P, _P, _P, _I64, _I, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _P],

@@ -18,6 +18,7 @@ import threading
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from .. import _dev
 from .. import _lib
@@ -250,14 +251,37 @@ def encrypt(pt, keyset, target_level=None, rng_seed=None, min_circuit_level=None
         )
     if pt.level < level:
         raise CryptoError("plaintext level below requested ciphertext level")
+    if rng_seed is None and DEVICE_UNSEEDED_RANDOMNESS:
+        # the reference seeds numpy from OS entropy here (never reproducible):
+        # expand 64 bits of OS entropy on the device instead of drawing and
+        # uploading 3 N samples
+        return _encrypt_from_samples(pt, keyset, level, device_samples(params))
     rng = np.random.default_rng(None if rng_seed is None else np.random.PCG64(rng_seed))
     ring = params.ring
-    n = params.ring_degree
-    k = level + 1
     v = rg._sample_signed(ring, "ternary", rng)
     e0 = rg._sample_signed(ring, "discrete_gaussian", rng, sigma=params.error_sigma)
     e1 = rg._sample_signed(ring, "discrete_gaussian", rng, sigma=params.error_sigma)
     return _encrypt_from_samples(pt, keyset, level, np.stack([v, e0, e1]))
+
+
+# unseeded encryptions draw v, e0, e1 on the device (hegpu_sample_encrypt);
+# False restores the host numpy draws for them too
+DEVICE_UNSEEDED_RANDOMNESS = True
+
+
+def device_samples(params, seed=None):
+    """(3, N) int64 device tensor: ternary v and rounded-Gaussian e0, e1
+    (ring.py:499-509 distributions) expanded from a 64-bit seed (default:
+    OS entropy) by the device Philox generator."""
+    import os as _os
+
+    n = params.ring_degree
+    if seed is None:
+        seed = int.from_bytes(_os.urandom(8), "little")
+    out = _dev.empty(3, n)
+    _lib.call("hegpu_sample_encrypt", out.data_ptr(), n, int(seed) & ((1 << 64) - 1),
+              float(params.error_sigma), _dev.stream())
+    return out
 
 
 def _encrypt_from_samples(pt, keyset, level, samples):
@@ -266,7 +290,8 @@ def _encrypt_from_samples(pt, keyset, level, samples):
     n = params.ring_degree
     k = level + 1
     sel = _dev.chain_primes(k)
-    lifted = rg._lift_signed_dev(ring, _dev.to_device(samples), sel)  # (3, k, N)
+    dev_samples = samples if isinstance(samples, torch.Tensor) else _dev.to_device(samples)
+    lifted = rg._lift_signed_dev(ring, dev_samples, sel)  # (3, k, N)
     rg._ntt_dev(ring, lifted, lifted, k, sel, False)
     b_full, a_full = keyset.public_key
     out = _packed(params, (), level)

@@ -1706,6 +1706,10 @@ int hegpu_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, u
                                            out_stride, S_(stream)))
 }
 
+int hegpu_sample_encrypt(int64_t* out, int n, uint64_t seed, double sigma, void* stream) {
+  HEGPU_TRY(sample_encrypt(out, n, seed, sigma, S_(stream)))
+}
+
 int hegpu_encode_overflow(hegpu_ring_t ring, int* flag) {
   HEGPU_TRY({
     Ring& R = RR(ring);

@@ -308,6 +308,7 @@ void launch_encode_diags(Ring& R, int kind, int half, double fold, double scale,
 bool encode_overflow_check(Ring& R);
 
 // rng.cu: numpy-compatible PCG64 bounded uniform draws; returns draws consumed
+void sample_encrypt(int64_t* out, int n, uint64_t seed, double sigma, cudaStream_t st);
 long long pcg64_uniform_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                              uint64_t inc_lo, const uint64_t* bounds, int k, int n,
                              uint64_t* out, int64_t out_stride, cudaStream_t st);

@@ -144,4 +144,72 @@ long long pcg64_uniform_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
   return P.n_out + P.n_rej;
 }
 
+
+// ---------------------------------------------------------------------------
+// Encryption randomness for UNSEEDED encryptions (the reference draws v, e0,
+// e1 from numpy's Generator seeded by OS entropy there: ops.py:87-100,
+// logreg.py:151-156, bootstrap.py:367 -- never reproducible, so there is no
+// stream to match).  The host supplies 64 bits of OS entropy; the device
+// expands them with the counter-based Philox4x32-10 generator:
+//   v  = ternary, uniform on {-1, 0, 1}   (ring.py:499-501)
+//   e0, e1 = rint(N(0, sigma^2))          (ring.py:507-509), Box-Muller
+// Seeded encryptions keep numpy on the host (bit-exact with the reference).
+// ---------------------------------------------------------------------------
+struct Philox {
+  uint32_t c[4];
+};
+
+__device__ __forceinline__ Philox philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                uint32_t k0, uint32_t k1) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+    const uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+    k0 += W0;
+    k1 += W1;
+  }
+  Philox o;
+  o.c[0] = c0;
+  o.c[1] = c1;
+  o.c[2] = c2;
+  o.c[3] = c3;
+  return o;
+}
+
+__device__ __forceinline__ double u01_53(uint32_t a, uint32_t b) {  // (0, 1]
+  const uint64_t x = ((uint64_t)a << 21) ^ (uint64_t)b;  // 53 bits
+  return ((double)(x & ((1ull << 53) - 1)) + 1.0) * 0x1.0p-53;
+}
+
+__global__ void __launch_bounds__(256) k_sample_encrypt(int64_t* out, int n, uint64_t seed,
+                                                        double sigma) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  // one Philox block per (coefficient, draw): counters never repeat
+  const Philox t = philox4x32_10((uint32_t)x, 0u, 0x7e3a11u, 0u, k0, k1);
+  const Philox g = philox4x32_10((uint32_t)x, 1u, 0x7e3a11u, 0u, k0, k1);
+  // ternary: floor(3 u / 2^32) - 1 (bias 2^-32)
+  out[x] = (int64_t)((((uint64_t)t.c[0]) * 3u) >> 32) - 1;
+  // Box-Muller: two independent N(0, 1) from two 53-bit uniforms
+  const double u1 = u01_53(g.c[0], g.c[1]), u2 = u01_53(g.c[2], g.c[3]);
+  const double r = sqrt(-2.0 * log(u1)) * sigma;
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  out[n + x] = (int64_t)rint(r * cs);
+  out[2 * n + x] = (int64_t)rint(r * sn);
+}
+
+void sample_encrypt(int64_t* out, int n, uint64_t seed, double sigma, cudaStream_t st) {
+  if (n <= 0 || sigma <= 0.0) throw HegpuError{HEGPU_E_ARG, "sample_encrypt: n > 0, sigma > 0"};
+  k_sample_encrypt<<<(n + 255) / 256, 256, 0, st>>>(out, n, seed, sigma);
+  check_cuda(cudaGetLastError(), "sample_encrypt launch");
+}
+
 }  // namespace hegpu

@@ -409,3 +409,29 @@ def test_wire_formats_match_reference_bytes(desk_keys, digests):
     assert logreg.serialize_model(m2) == blobs["hlr1"]
     got = ckks.decrypt_vector(m2.weights[1], k2)[:64]
     assert np.max(np.abs(got - u[:64] * 2 / 4)) < 1e-3
+
+
+def test_unseeded_encrypt_uses_device_randomness(desk_keys):
+    """Unseeded encryptions (OS entropy in the reference, ops.py:87) expand
+    their v, e0, e1 on the device (hegpu_sample_encrypt): ternary on {-1,0,1}
+    and rint(N(0, sigma^2)) like ring.py:499-509, fresh per call, and the
+    ciphertexts decrypt; seeded encryptions keep the reference's host stream
+    (their digests are checked in test_scheme_digests)."""
+    from paper_2210_02574_b200.ckks import ops
+
+    params, keys = desk_keys
+    big = type("P", (), {"ring_degree": 1 << 20, "error_sigma": params.error_sigma})()
+    s = ops.device_samples(big, seed=12345).cpu().numpy()
+    v, e = s[0], s[1:].ravel()
+    counts = np.bincount(v + 1, minlength=3) / v.size
+    assert set(np.unique(v)) <= {-1, 0, 1} and np.all(np.abs(counts - 1 / 3) < 3e-3)
+    assert abs(e.mean()) < 0.02 and abs(e.std() - np.sqrt(params.error_sigma ** 2 + 1 / 12)) < 0.02
+    assert np.max(np.abs(e)) < 12 * params.error_sigma
+    assert np.array_equal(ops.device_samples(big, seed=12345).cpu().numpy(), s)  # counter-based
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-1, 1, params.slot_count)
+    c1 = ckks.encrypt_vector(params, u, keys)
+    c2 = ckks.encrypt_vector(params, u, keys)
+    assert not np.array_equal(c1.c1.limbs, c2.c1.limbs)
+    for c in (c1, c2):
+        assert np.max(np.abs(ckks.decrypt_vector(c, keys) - u)) < 1e-4
