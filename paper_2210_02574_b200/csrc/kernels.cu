@@ -1467,10 +1467,11 @@ static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
 #ifndef HEGPU_BSGS_MMA
 #define HEGPU_BSGS_MMA 1
 #endif
-#ifndef HEGPU_MMA_1BUF
-#define HEGPU_MMA_1BUF 0  // 1: single raw buffer, 3 CTAs/SM: measured 17% slower (spills)
+#ifndef HEGPU_MMA_BDIRECT
+#define HEGPU_MMA_BDIRECT 1  // B fragments built in registers from the raw chunk
 #endif
-constexpr int kMmaNbuf = HEGPU_MMA_1BUF ? 1 : 2;
+constexpr int kMmaNbuf = 2;  // raw chunk buffers (1 buffer at 3 CTAs/SM measured 17% slower)
+constexpr bool kMmaBDirect = HEGPU_MMA_BDIRECT != 0;
 constexpr int kMmaGiants = 16;
 constexpr int kMmaTile = 32;  // coefficients per CTA
 
@@ -1512,9 +1513,12 @@ template <int RT, int MG>
 struct MmaSmem {
   static constexpr int NGC = kMmaGiants * MG;             // giants per CTA
   static constexpr int COLS = 2 * kMmaTile;
-  static constexpr int RAW_B = 32 * COLS;                 // u64 words [t][col]
+  // raw babies [t][col], rows padded by 16 B when the B fragments are read
+  // straight from them (4 term rows of one fragment fall in 2 wavefronts)
+  static constexpr int BSTR = COLS + (kMmaBDirect ? 2 : 0);
+  static constexpr int RAW_B = 32 * BSTR;
   static constexpr int RAW_A = 32 * NGC * RT;      // u64 words [t][giant][run]
-  static constexpr int PL_B = 8 * COLS * 8;               // u32 words [plane][col][8]
+  static constexpr int PL_B = kMmaBDirect ? 0 : 8 * COLS * 8;  // u32 [plane][col][8]
   static constexpr int PL_A = 8 * RT * NGC * 8;    // u32 words [plane][run][giant][8]
   static size_t bytes(int T) {
     return (size_t)kMmaNbuf * (RAW_B + RAW_A) * 8 + (size_t)(PL_B + PL_A) * 4 +
@@ -1525,7 +1529,7 @@ struct MmaSmem {
 // MG = 16-giant m-tiles per CTA (8 warps each): MG = 2 stages and converts the
 // babies' planes once for 32 giants
 template <int RT, int MG>
-__global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 2))
+__global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : 2)
     k_bsgs_mma(const __grid_constant__ BsgsParams P) {
   using L = MmaSmem<RT, MG>;
   constexpr int NGC = L::NGC, NT = 256 * MG;
@@ -1564,7 +1568,7 @@ __global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 
     for (int e = threadIdx.x; e < 32 * COLS / 2; e += NT) {
       const int t = e / (COLS / 2), j = (e % (COLS / 2)) * 2;
       const int c = j / kMmaTile, xl = j % kMmaTile;
-      uint64_t* d = rb + t * COLS + j;
+      uint64_t* d = rb + t * L::BSTR + j;
       if (tc + t < T)
         cp_async16(d, P.baby[tc + t] + c * P.c1_off + (size_t)limb * N + x0 + xl);
       else
@@ -1603,15 +1607,15 @@ __global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 
   for (int ch = 0; ch < nch; ++ch) {
     cp_async_wait_group<0>();
     __syncthreads();  // raw chunk ch landed; planes of ch - 1 consumed
-    if (kMmaNbuf == 2 && ch + 1 < nch) stage(ch + 1);
+    if (ch + 1 < nch) stage(ch + 1);
     const uint64_t* rb = raw_b + (ch % kMmaNbuf) * L::RAW_B;
     const uint64_t* ra = raw_a + (ch % kMmaNbuf) * L::RAW_A;
     // ---- byte planes: babies (64 cols x 8 term quads) ------------------------
-    for (int e = threadIdx.x; e < COLS * 8; e += NT) {
+    for (int e = threadIdx.x; e < (kMmaBDirect ? 0 : COLS * 8); e += NT) {
       const int j = e % COLS, q = e / COLS;
       uint64_t v[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = rb[(4 * q + i) * COLS + j];
+      for (int i = 0; i < 4; ++i) v[i] = rb[(4 * q + i) * L::BSTR + j];
       uint32_t pl[8];
       byte_planes4(v, pl);
       const int w = j * 8 + (q ^ mma_sw(j));
@@ -1633,13 +1637,29 @@ __global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 
         if (p < nby) As[p * RT * NGC * 8 + w] = pl[p];
     }
     __syncthreads();
-    if (kMmaNbuf == 1 && ch + 1 < nch) stage(ch + 1);  // the raw buffer is converted
     // ---- MMAs: plane pairs (i, j) into shift i + j ----------------------------
     const int jb = comp * kMmaTile + xo + fr;  // this lane's B column
-    const uint32_t* bcol = Bs + jb * 8;
-    const int bw0 = fq ^ mma_sw(jb), bw1 = (fq + 4) ^ mma_sw(jb);
     uint32_t bf[8][2];
-    if constexpr (kMmaNbuf == 2) {  // all B fragments in registers (3 CTAs/SM: reloaded)
+    if constexpr (kMmaBDirect) {
+      // the lane's fragment words are byte planes of its own column's terms
+      // 4 fq .. 4 fq + 3 and 4 fq + 16 .. 4 fq + 19: no shared-memory planes
+      uint64_t v0[4], v1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v0[i] = rb[(4 * fq + i) * L::BSTR + jb];
+        v1[i] = rb[(4 * fq + 16 + i) * L::BSTR + jb];
+      }
+      uint32_t p0[8], p1[8];
+      byte_planes4(v0, p0);
+      byte_planes4(v1, p1);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        bf[p][0] = p0[p];
+        bf[p][1] = p1[p];
+      }
+    } else {
+      const uint32_t* bcol = Bs + jb * 8;
+      const int bw0 = fq ^ mma_sw(jb), bw1 = (fq + 4) ^ mma_sw(jb);
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
         bf[p][0] = bcol[p * COLS * 8 + bw0];
@@ -1658,12 +1678,7 @@ __global__ void __launch_bounds__(256 * MG, MG == 2 ? 1 : (HEGPU_MMA_1BUF ? 3 : 
       af[3] = ap[gb * 8 + ((fq + 4) ^ mma_sw(gb))];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (j < nby) {
-          if constexpr (kMmaNbuf == 2)
-            imma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
-          else
-            imma_u8(acc[i + j], af, bcol[j * COLS * 8 + bw0], bcol[j * COLS * 8 + bw1]);
-        }
+        if (j < nby) imma_u8(acc[i + j], af, bf[j][0], bf[j][1]);
       }
     }
   }
