@@ -148,6 +148,21 @@ def _pair_group(ct):
     return p0, 2 * cnt, k * n
 
 
+def _packed_view(ct):
+    """The (lead..., 2, k, N) tensor holding c0 and c1 when they are packed
+    back to back (one contiguous copy instead of two), else None."""
+    if _pair_group(ct) is None:
+        return None
+    k = ct.level + 1
+    n = ct.params.ring_degree
+    lead = tuple(_lead(ct))
+    if len(lead) > 1 or (lead and ct.c0.data.stride(0) != 2 * k * n):
+        return None
+    shape = lead + (2, k, n)
+    stride = ((2 * k * n,) if lead else ()) + (k * n, n, 1)
+    return ct.c0.data.as_strided(shape, stride)
+
+
 def stack(cts):
     """Batch a list of same-level, same-scale ciphertexts into one (B, ...) ciphertext."""
     if not cts:
@@ -159,8 +174,12 @@ def stack(cts):
         _check_scales(first.scale, c.scale)
     out = _packed(first.params, (len(cts),), first.level)
     for i, c in enumerate(cts):
-        out[i, 0].copy_(c.c0.data)
-        out[i, 1].copy_(c.c1.data)
+        pv = _packed_view(c)
+        if pv is not None:
+            out[i].copy_(pv)
+        else:
+            out[i, 0].copy_(c.c0.data)
+            out[i, 1].copy_(c.c1.data)
     return _ct(out, first.level, first.scale, first.slot_count, first.params,
                any(c.insecure_provenance for c in cts))
 
@@ -181,8 +200,12 @@ def concat(cts):
     out = _packed(first.params, (total,), first.level)
     pos = 0
     for c in parts:
-        out[pos : pos + c.batch, 0].copy_(c.c0.data)
-        out[pos : pos + c.batch, 1].copy_(c.c1.data)
+        pv = _packed_view(c)
+        if pv is not None:
+            out[pos : pos + c.batch].copy_(pv)
+        else:
+            out[pos : pos + c.batch, 0].copy_(c.c0.data)
+            out[pos : pos + c.batch, 1].copy_(c.c1.data)
         pos += c.batch
     return _ct(out, first.level, first.scale, first.slot_count, first.params,
                any(c.insecure_provenance for c in parts))
@@ -763,10 +786,13 @@ def rotate_hoisted_ext(ct, steps, keyset):
         *[kk.b[j].data_ptr() for kk in keys for j in range(dnum)])
     ka = (ctypes.c_void_p * (len(todo) * dnum))(
         *[kk.a[j].data_ptr() for kk in keys for j in range(dnum)])
-    # the rotated outputs must be packed back to back: compute into a dense
-    # block, then scatter if step 0 sits in between
-    block = out if todo == list(range(len(todo))) else _dev.empty(
-        *((len(todo),) + tuple(_lead(ct)) + (2, k + K, n)))
+    # the rotated outputs must be packed back to back: a contiguous run of
+    # nonzero steps (e.g. babies 1..n1-1 after step 0) is computed in place;
+    # otherwise into a dense block that is scattered afterwards
+    if todo == list(range(todo[0], todo[0] + len(todo))):
+        block = out[todo[0]: todo[0] + len(todo)]
+    else:
+        block = _dev.empty(*((len(todo),) + tuple(_lead(ct)) + (2, k + K, n)))
     optr = (ctypes.c_void_p * len(todo))(*[block[i].data_ptr() for i in range(len(todo))])
     for _ in todo:
         _stats.count("ks", ct.level, cnt)
@@ -775,7 +801,7 @@ def rotate_hoisted_ext(ct, steps, keyset):
         src.c0.data.data_ptr(), 2 * k * n, k * n, cnt, len(todo), gal.ctypes.data, kb, ka, dnum,
         optr, 1, _dev.stream(),
     )
-    if block is not out:
+    if block.data_ptr() != out[todo[0]].data_ptr():
         for j, i in enumerate(todo):
             out[i].copy_(block[j])
     return out
