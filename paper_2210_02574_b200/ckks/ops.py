@@ -990,12 +990,43 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
 
 def _cat_batch(cts):
     """Stack same-shape ciphertexts (each unbatched or with batch B) into one
-    batch of len(cts) (or len(cts) * B); a single one passes through."""
+    batch of len(cts) (or len(cts) * B); a single one passes through.  Parts
+    that already sit back to back in one packed tensor (the slices
+    _split_batch made of an earlier batched result, in order) are returned as
+    a view of it instead of copied (read-only use inside eval_poly_bsgs)."""
     if len(cts) == 1:
         return cts[0]
+    view = _adjacent_view(cts)
+    if view is not None:
+        first = cts[0]
+        return _ct(view, first.level, first.scale, first.slot_count, first.params,
+                   any(c.insecure_provenance for c in cts))
     if cts[0].batch is None:
         return stack(cts)
     return concat(cts)
+
+
+def _adjacent_view(cts):
+    """(total, 2, k, N) view over ciphertexts packed consecutively in memory
+    with the same level and scale, else None."""
+    first = cts[0]
+    views = []
+    for c in cts:
+        if c.level != first.level or c.scale != first.scale:
+            return None
+        v = _packed_view(c)
+        if v is None:
+            return None
+        views.append(v)
+    ptr = views[0].data_ptr()
+    base = views[0].untyped_storage().data_ptr()
+    for v in views:  # same allocation (adjacent allocations do not count)
+        if v.data_ptr() != ptr or v.untyped_storage().data_ptr() != base:
+            return None
+        ptr += v.numel() * v.element_size()
+    k, n = first.level + 1, first.params.ring_degree
+    total = sum(1 if c.batch is None else c.batch for c in cts)
+    return views[0].as_strided((total, 2, k, n), (2 * k * n, k * n, n, 1))
 
 
 def _split_batch(ct, n, like):
