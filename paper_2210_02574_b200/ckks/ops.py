@@ -946,8 +946,10 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
         return t[1] if t[0] == "const" else values[id(t)]
 
     if leaves:
-        prods = [mult_plain(giants[1], lf[2], rescale_after=False) for lf in leaves]
-        for lf, v in zip(leaves, _split_batch(rescale(_cat_batch(prods)), len(prods), y)):
+        cat = _scalar_products(giants[1], [lf[2] for lf in leaves])
+        if cat is None:
+            cat = _cat_batch([mult_plain(giants[1], lf[2], rescale_after=False) for lf in leaves])
+        for lf, v in zip(leaves, _split_batch(rescale(cat), len(leaves), y)):
             values[id(lf)] = add_plain(v, lf[1])
     for g in sorted({t[1] for t in nodes}):
         level_nodes = [t for t in nodes if t[1] == g]
@@ -986,6 +988,30 @@ def eval_poly_bsgs(ct, poly, keyset, input_prescaled=False):
     if isinstance(result, float):
         result = add_plain(mult_plain(y, 0.0), result)
     return result
+
+
+def _scalar_products(ct, scalars):
+    """_cat_batch([mult_plain(ct, c, rescale_after=False) for c in scalars])
+    written straight into one packed batch (same scalar launches, no gather
+    copy); None when a scalar does not encode as a constant."""
+    if len(scalars) < 2 or _pair_group(ct) is None or len(_lead(ct)) > 1:
+        return None
+    k = ct.level + 1
+    n = ct.params.ring_degree
+    pts = [_as_plaintext(ct, float(c)) for c in scalars]
+    cres = [pt.const_residues(k) for pt in pts]
+    if any(c is None for c in cres) or len({pt.scale for pt in pts}) != 1:
+        return None
+    b = _lead(ct)[0] if _lead(ct) else 1
+    t = _dev.empty(len(scalars) * b, 2, k, n)
+    p, cnt, stride = _pair_group(ct)
+    for i, c in enumerate(cres):
+        _ew_group(ct.params, _lib.OP_SCALAR, p, stride, None, 0, t[i * b].data_ptr(), k * n, cnt,
+                  k, c)
+    if not _lead(ct):
+        t = t.view(len(scalars), 2, k, n)
+    return _ct(t, ct.level, ct.scale * pts[0].scale, ct.slot_count, ct.params,
+               ct.insecure_provenance)
 
 
 def _cat_batch(cts):
