@@ -1,4 +1,5 @@
-"""Where the torch copies of one eager cfg4 step come from: wraps
+"""Where the torch copies of one eager bench step (PROBE_CONFIG, default the
+cfg4 train step) come from: wraps
 Tensor.copy_, torch.stack / cat, Tensor.clone / contiguous during one
 training minibatch (no graph) and counts the calls on CUDA tensors by the
 innermost package frame (non-contiguous ones launch a copy kernel)."""
@@ -13,7 +14,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-wl = bench.TrainWorkload()
+wl = bench.WORKLOADS[os.environ.get("PROBE_CONFIG", "train")]()
 wl.setup(0, 1)
 for _ in range(2):
     wl.step()
@@ -23,11 +24,14 @@ nbytes = collections.Counter()
 active = [False]
 
 
-def site():
+def site(depth=3):
+    out = []
     for fr in reversed(traceback.extract_stack()[:-2]):
         if "paper_2210_02574_b200" in fr.filename or fr.filename.endswith("bench.py"):
-            return f"{os.path.basename(fr.filename)}:{fr.lineno} {fr.name}"
-    return "(outside)"
+            out.append(f"{os.path.basename(fr.filename)}:{fr.lineno} {fr.name}")
+            if len(out) == depth:
+                break
+    return " <- ".join(out) or "(outside)"
 
 
 def wrap(owner, name, kind):
@@ -50,6 +54,19 @@ def wrap(owner, name, kind):
     setattr(owner, name, f)
 
 
+_orig_to = torch.Tensor.to
+
+
+def _to(self, *a, **k):
+    out = _orig_to(self, *a, **k)
+    if active[0] and out.is_cuda and not self.is_cuda:
+        key = f"h2d to @ {site()}"
+        where[key] += 1
+        nbytes[key] += out.numel() * out.element_size()
+    return out
+
+
+torch.Tensor.to = _to
 wrap(torch.Tensor, "copy_", "copy_")
 wrap(torch.Tensor, "clone", "clone")
 wrap(torch.Tensor, "contiguous", "contiguous")
