@@ -327,20 +327,29 @@ __global__ void __launch_bounds__(kEwThreads) k_tensor(const __grid_constant__ T
   const int row = blockIdx.y + blockIdx.z * 65535;
   if (row >= P.rows) return;
   const int poly = row / P.k, limb = row - poly * P.k;
-  const int x = blockIdx.x * kEwThreads + threadIdx.x;
+  // two adjacent coefficients per thread: 16-byte loads and stores
+  const int x = (blockIdx.x * kEwThreads + threadIdx.x) * 2;
   if (x >= N) return;
   const PrimeConst pc = P.pc[limb];
   const size_t l = (size_t)limb * N + x;
   const int64_t ap = (int64_t)(poly % P.amod) * P.as;
-  const uint64_t a0 = P.a0[ap + l], a1 = P.a1[ap + l];
-  const uint64_t b0 = P.b0[poly * P.bs + l], b1 = P.b1[poly * P.bs + l];
-  P.d0[poly * P.ds + l] = mul_mod(a0, b0, pc);
-  Mac128 acc;
-  acc.zero();
-  acc.add(a0, b1);
-  acc.add(a1, b0);
-  P.d1[poly * P.ds + l] = mont_mul(acc.redc(pc), pc.r2, pc.q, pc.qinv_neg);
-  P.d2[poly * P.ds + l] = mul_mod(a1, b1, pc);
+  auto ld2 = [](const uint64_t* p) { return *reinterpret_cast<const ulonglong2*>(p); };
+  const ulonglong2 a0 = ld2(P.a0 + ap + l), a1 = ld2(P.a1 + ap + l);
+  const ulonglong2 b0 = ld2(P.b0 + poly * P.bs + l), b1 = ld2(P.b1 + poly * P.bs + l);
+  uint64_t d1[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    Mac128 acc;
+    acc.zero();
+    acc.add(h ? a0.y : a0.x, h ? b1.y : b1.x);
+    acc.add(h ? a1.y : a1.x, h ? b0.y : b0.x);
+    d1[h] = mont_mul(acc.redc(pc), pc.r2, pc.q, pc.qinv_neg);
+  }
+  *reinterpret_cast<ulonglong2*>(P.d0 + poly * P.ds + l) =
+      make_ulonglong2(mul_mod(a0.x, b0.x, pc), mul_mod(a0.y, b0.y, pc));
+  *reinterpret_cast<ulonglong2*>(P.d1 + poly * P.ds + l) = make_ulonglong2(d1[0], d1[1]);
+  *reinterpret_cast<ulonglong2*>(P.d2 + poly * P.ds + l) =
+      make_ulonglong2(mul_mod(a1.x, b1.x, pc), mul_mod(a1.y, b1.y, pc));
 }
 
 void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int n_polys,
@@ -351,7 +360,8 @@ void launch_tensor(const PrimeConst* dpc, int log_n, const TensorParams& T0, int
   T.rows = rows;
   T.pc = dpc;
   T.log_n = log_n;
-  const dim3 grid = rows_grid(1 << log_n, rows, 1);
+  if (log_n < 1) throw HegpuError{HEGPU_E_ARG, "tensor: N >= 2"};
+  const dim3 grid = rows_grid(1 << log_n, rows, 2);
   ProfScope ps(PROF_TENSOR, st, (double)rows * (1 << log_n) * 56.0,
                (double)rows * (1 << log_n) * 8.0);
   k_tensor<<<grid, kEwThreads, 0, st>>>(T);
