@@ -1471,8 +1471,10 @@ static void launch_bsgs_run(const BsgsParams& P, int k, cudaStream_t st) {
 // 15 shifts into the exact 128-bit sum (< 256 q^2 < 2^128) before one Barrett /
 // Montgomery reduction: the limbs are identical to k_bsgs_run's.
 // CTA = 8 warps over 32 coefficients x 16 giants of one limb; warp w owns the
-// 8-column tile w (component w / 4, coefficients 8 (w % 4) ..); the byte
-// planes of a 32-term chunk are staged in shared memory (PRMT transposes).
+// 8-column tile w (component w / 4, coefficients 8 (w % 4) ..).  32-term
+// chunks of raw words arrive by cp.async (double-buffered); the diagonals'
+// byte planes are built once per CTA in shared memory, each lane builds its
+// own B fragments from its column's raw words (PRMT transposes).
 // ---------------------------------------------------------------------------
 #ifndef HEGPU_BSGS_MMA
 #define HEGPU_BSGS_MMA 1
