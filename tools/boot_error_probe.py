@@ -23,9 +23,10 @@ n = slots if MODE == "full" else 1024
 
 def make_ctx(spec):
     kw = dict(n_slots=n, input_periodic=(MODE != "full"))
-    if spec.startswith("da"):
-        r = int(spec[2:] or 3)
-        return bs.build_context(params, evalmod="double_angle", double_angle=r, **kw)
+    if spec.startswith("da"):  # "daR" or "daR:D" (R squarings, degree-D cos base)
+        r_s, _, d_s = spec[2:].partition(":")
+        return bs.build_context(params, evalmod="double_angle", double_angle=int(r_s or 3),
+                                evalmod_degree=int(d_s) if d_s else None, **kw)
     return bs.build_context(params, evalmod="sine", evalmod_degree=int(spec), **kw)
 
 
